@@ -1,0 +1,266 @@
+/*
+ * pmx.h -- C ABI of libpmx.so, the sm_100a kernels behind the pillarmix-compatible
+ * API (package paper_2601_12638_b200).
+ *
+ * The reference (pillarmix, /root/reference/pkg/src/pillarmix = "pm/") is pure
+ * Python + numpy and has no FFI: its seam is the Python functions listed per
+ * entry point below.  Each entry point replaces one of them; the Python host
+ * layer (paper_2601_12638_b200/*.py) keeps the reference names, argument meaning
+ * and exception types, and binds this header through ctypes
+ * (paper_2601_12638_b200/_native.py).  INTEGRATION.md shows the binding.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only.  Every buffer is caller-owned DEVICE memory
+ *    unless the parameter name says host; the library never allocates on the hot
+ *    path (scratch comes in through `ws`).
+ *  - Every call is stream-ordered on `stream` (a cudaStream_t) and asynchronous;
+ *    no call synchronises the device, so all of them can be captured into CUDA
+ *    graphs.
+ *  - Activations are NHWC.  Frames of a batch are independent.
+ *  - Status codes: 0 = ok.  On failure pmx_last_error() (thread-local) holds a
+ *    message; the Python layer maps PMX_ERR_INVALID to ValueError and the others
+ *    to RuntimeError, mirroring the reference's exception types.
+ *  - No CPU fallback exists: without a CUDA device every call fails with
+ *    PMX_ERR_CUDA.
+ */
+#ifndef PMX_H_
+#define PMX_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* pmx_stream_t; /* == cudaStream_t */
+
+typedef enum {
+  PMX_OK = 0,
+  PMX_ERR_INVALID = 1,     /* bad shape / argument (ValueError in Python) */
+  PMX_ERR_CUDA = 2,        /* CUDA runtime failure or no device */
+  PMX_ERR_UNSUPPORTED = 3  /* valid request outside what the kernels cover */
+} pmx_status;
+
+typedef enum { PMX_F32 = 0, PMX_F16 = 1, PMX_I8 = 2, PMX_F64 = 3 } pmx_dtype;
+
+#define PMX_ABI_VERSION 1
+
+const char* pmx_last_error(void);
+int32_t pmx_abi_version(void);
+/* Name of the conv backend pmx_conv() uses for (in_dtype, kind): "tcgen05" or "simt". */
+const char* pmx_conv_backend(int32_t in_dtype, int32_t kind);
+/* Stream-ordered zero fill (canvas clearing; cudaMemsetAsync, graph-capturable). */
+pmx_status pmx_zero(void* ptr, size_t bytes, pmx_stream_t stream);
+
+/* ------------------------------------------------------------------------
+ * K1 quantization math -- replaces pm/quant.py:98-147.
+ * Codes are bit-exact with clip(rint(f64(x) / scale), -128, 127): an f32
+ * estimate is refined by an IEEE f64 division inside a guard band around
+ * every .5 tie.
+ * ---------------------------------------------------------------------- */
+
+/* pm/quant.py:98-103 quantize(x, QuantParams(scale)) -> int codes (int32 out, like numpy).
+ * x_dtype: PMX_F32 (activations; guard-band kernel) or PMX_F64 (API inputs that
+ * are not f32, divided in f64 directly as the reference does). */
+pmx_status pmx_quantize(const void* x, int32_t x_dtype, int64_t n, double scale, int32_t* codes,
+                        pmx_stream_t stream);
+/* pm/quant.py:114-116 fake_quant(t, qp) -> f32(f64(code) * scale). */
+pmx_status pmx_fake_quant(const void* x, int32_t x_dtype, int64_t n, double scale, float* out,
+                          pmx_stream_t stream);
+/* pm/quant.py:136-141 (codes part) and pm/model.py:276-279: per-row (axis 0)
+ * weight quantization.  `scales` is a device f64 [rows] array.  Writes int8
+ * codes (may be NULL) and the dequantized f32 weight (may be NULL). */
+pmx_status pmx_quantize_rows(const float* w, int64_t rows, int64_t cols, const double* scales,
+                             int8_t* codes, float* dequant, pmx_stream_t stream);
+/* pm/quant.py:144-147 fp16_roundtrip: clip +-65504, RNE to binary16.  Either
+ * output may be NULL: f32 round-tripped values and/or raw binary16 bits. */
+pmx_status pmx_fp16_roundtrip(const float* x, int64_t n, float* out_f32, uint16_t* out_f16,
+                              pmx_stream_t stream);
+
+/* ------------------------------------------------------------------------
+ * K2 min/max observers -- replaces pm/quant.py:179-188 and the observe_fn
+ * record of pm/calibration.py:116-124.  Observers are device uint32 pairs of
+ * order-preserving float keys {min_key, max_key}; widen with atomics, so they
+ * are exact and order-independent.  Decode: key>=0x80000000 ? key^0x80000000
+ * : ~key gives the float bits.  NaN/Inf widen the pair to a non-finite value,
+ * which the host reports like the reference.
+ * ---------------------------------------------------------------------- */
+pmx_status pmx_minmax_init(uint32_t* keys, int64_t n_pairs, pmx_stream_t stream);
+pmx_status pmx_minmax(const void* x, int64_t n, int32_t dtype, uint32_t* keys,
+                      pmx_stream_t stream);
+/* f64 observer (API inputs in f64, e.g. pm/quant.py:179-188 on float64 arrays):
+ * same protocol with uint64 keys {min_key, max_key}. */
+pmx_status pmx_minmax_f64_init(uint64_t* keys, pmx_stream_t stream);
+pmx_status pmx_minmax_f64(const double* x, int64_t n, uint64_t* keys, pmx_stream_t stream);
+
+/* ------------------------------------------------------------------------
+ * K3 pillarize -- replaces pm/scenes.py:155-193 (binning, ascending flat-id
+ * pillar order, first-come truncation to max_points), extended with an origin
+ * offset and a max-pillars cap (keep the cells whose first point has the
+ * smallest scene index; identity when the cap does not bind).
+ * ---------------------------------------------------------------------- */
+typedef struct {
+  int32_t grid_h;      /* rows (y) */
+  int32_t grid_w;      /* cols (x) */
+  int32_t max_points;  /* M, points kept per pillar (1..32) */
+  int32_t max_pillars; /* P cap; <= 0 means uncapped (then Pcap must be grid_h*grid_w) */
+  float x_min, y_min;  /* origin */
+  float cell_w, cell_h;
+} pmx_grid;
+
+/* Scratch bytes for pmx_pillarize. */
+size_t pmx_pillarize_workspace(const pmx_grid* grid, int32_t batch, int64_t max_points_per_frame);
+
+/* points: [total, 4] f32 (x, y, z|intensity, r) rows, frames concatenated;
+ * frame_offsets: device int64 [batch + 1].  Outputs per frame b (Pcap slots):
+ * coords [B, Pcap, 2] int32 (row, col); counts [B, Pcap] int32 kept points;
+ * pt_idx [B, Pcap, M] int32 frame-local point index in scene order, -1 padding;
+ * n_pillars [B] int32.  Slots >= n_pillars are left untouched. */
+pmx_status pmx_pillarize(const float* points, const int64_t* frame_offsets, int32_t batch,
+                         int64_t max_points_per_frame, const pmx_grid* grid, int32_t pcap,
+                         int32_t* coords, int32_t* counts, int32_t* pt_idx, int32_t* n_pillars,
+                         void* ws, size_t ws_bytes, pmx_stream_t stream);
+
+/* Materialise padded per-pillar features [B, Pcap, M, F] f32 (zero padded) and
+ * the mask [B, Pcap, M] u8 -- the PillarSample of pm/tensor_ops.py:60-77.
+ * n_features = 5: (x, y, i, x-mx, y-my), pm/scenes.py:186-192 (points' third
+ * column is the intensity); n_features = 9: (x, y, z, r, x-mx, y-my, z-mz,
+ * x-xc, y-yc), SURVEY App. B.2. */
+pmx_status pmx_pillar_features(const float* points, const int64_t* frame_offsets, int32_t batch,
+                               const pmx_grid* grid, int32_t pcap, int32_t n_features,
+                               const int32_t* coords, const int32_t* counts,
+                               const int32_t* pt_idx, const int32_t* n_pillars, float* features,
+                               uint8_t* mask, pmx_stream_t stream);
+
+/* ------------------------------------------------------------------------
+ * Output descriptor shared by the layer kernels: the producer epilogue writes
+ * its (post-BN, post-ReLU) f32 value once per consumer format.  Heads use F32.
+ * ---------------------------------------------------------------------- */
+typedef struct {
+  void* ptr;         /* NHWC destination */
+  double scale;      /* PMX_I8 only: consumer activation scale (codes = quantize(y, scale)) */
+  int32_t dtype;     /* PMX_F32 / PMX_F16 / PMX_I8 */
+  int32_t c_stride;  /* channels per pixel in the destination */
+  int32_t c_offset;  /* first destination channel (concat slice) */
+  int32_t _reserved;
+} pmx_out;
+
+#define PMX_MAX_OUTS 3
+
+/* ------------------------------------------------------------------------
+ * K4+K5 fused pillar feature net: (feature augmentation) -> layer-1 precision
+ * transform -> linear -> folded BN -> ReLU -> masked max over points -> scatter
+ * onto the NHWC canvas in every consumer format.  Replaces pm/model.py:334-355
+ * (linear branch of _run_weight_layer :271-307, max_over_points
+ * pm/tensor_ops.py:163-173, scatter_pillars :138-160).  The canvas must be
+ * zeroed by the caller (cudaMemsetAsync) -- empty cells stay 0 in every format.
+ * ---------------------------------------------------------------------- */
+enum { PMX_PFN_FROM_POINTS9 = 0, PMX_PFN_FROM_FEATURES = 1 };
+
+typedef struct {
+  int32_t source;     /* PMX_PFN_FROM_POINTS9 or PMX_PFN_FROM_FEATURES */
+  int32_t in_dtype;   /* layer-1 precision (PMX_F32/F16/I8) */
+  int32_t n_features; /* F: 9 for POINTS9, any 1..16 for FROM_FEATURES */
+  int32_t channels;   /* C out, 1..64 */
+  int32_t max_points; /* M */
+  int32_t relu;
+  double in_scale;    /* PMX_I8: layer-1 activation scale */
+} pmx_pfn_desc;
+
+/* weight: [C, F] in the layer precision (f32 / f16 bits / int8 codes);
+ * alpha: PMX_I8 only, f32(s_x * s_w[c]) per channel; bias [C] f32 (BN folded).
+ * FROM_FEATURES reads features [B, Pcap, M, F] f32 + mask [B, Pcap, M] u8;
+ * POINTS9 recomputes the 9 features from points + pt_idx.
+ * in_keys (may be NULL): observer of layer 1's input (features incl. padding);
+ * out_keys (may be NULL): observer of the canvas (pooled values, 0 if any cell empty). */
+pmx_status pmx_pfn_scatter(const pmx_pfn_desc* desc, const pmx_grid* grid, int32_t batch,
+                           int32_t pcap, const float* points, const int64_t* frame_offsets,
+                           const float* features, const uint8_t* mask, const int32_t* coords,
+                           const int32_t* counts, const int32_t* pt_idx,
+                           const int32_t* n_pillars, const void* weight, const float* alpha,
+                           const float* bias, const float* bn_post, const pmx_out* outs,
+                           int32_t n_outs, uint32_t* in_keys, uint32_t* out_keys,
+                           pmx_stream_t stream);
+
+/* ------------------------------------------------------------------------
+ * K6-K10 implicit-GEMM layer kernel -- replaces conv2d pm/tensor_ops.py:109-131
+ * / linear :80-91 under the precision dispatch of pm/model.py:271-307, plus the
+ * KITTI neck deconvolution (kernel == stride).
+ *   INT8: int8 codes x int8 codes -> exact int32, y = f32(acc) * alpha[c] + bias[c]
+ *   FP16: binary16 x binary16 -> f32, y = acc + bias[c]
+ *   FP32: f32 x f32 -> f32,          y = acc + bias[c]
+ * then ReLU, then one store per pmx_out (int8 codes are exact quantize()).
+ * Weight layouts: CONV2D [Cout, kh, kw, Cin]; DECONV2D [(dy, dx, co), Cin]
+ * (k*k*Cout rows).  alpha/bias are per output channel (Cout).
+ * ---------------------------------------------------------------------- */
+enum { PMX_CONV2D = 0, PMX_DECONV2D = 1 };
+
+typedef struct {
+  int32_t kind;         /* PMX_CONV2D / PMX_DECONV2D */
+  int32_t in_dtype;     /* layer precision = input and weight storage type */
+  int32_t batch, in_h, in_w, in_c;
+  int32_t in_c_stride;  /* channels per input pixel in the source buffer (>= in_c) */
+  int32_t in_c_offset;  /* first source channel */
+  int32_t out_c;
+  int32_t k_h, k_w, stride_h, stride_w, pad_h, pad_w;
+  int32_t out_h, out_w; /* output extents (deconv: in * stride) */
+  int32_t relu;
+} pmx_conv_desc;
+
+size_t pmx_conv_workspace(const pmx_conv_desc* desc);
+
+/* bn_post (may be NULL): unfolded batch norm applied after the bias as
+ * (y - mean[c]) * factor[c] + beta[c] in f32 (pm/model.py:252-258); device
+ * [3, Cout] = {mean, factor, beta}.  The same argument exists on pmx_pfn_scatter.
+ * out_keys (may be NULL): observer widened with every output value y. */
+pmx_status pmx_conv(const pmx_conv_desc* desc, const void* x, const void* w, const float* alpha,
+                    const float* bias, const float* bn_post, const pmx_out* outs, int32_t n_outs,
+                    uint32_t* out_keys, void* ws, size_t ws_bytes, pmx_stream_t stream);
+
+/* Force a backend for testing: 0 = automatic, 1 = SIMT reference kernel only. */
+void pmx_set_conv_backend(int32_t mode);
+
+/* Stage an f32 [pixels, c] tensor into every consumer format (the precision
+ * transform of pm/model.py:273-285 applied to a graph input), optionally
+ * widening an observer with its values. */
+pmx_status pmx_cast_out(const float* x, int64_t pixels, int32_t c, const pmx_out* outs, int32_t n_outs,
+                        uint32_t* keys, pmx_stream_t stream);
+
+/* Nearest 2x upsample of an NHWC tensor (pm/tensor_ops.py:176-178), any dtype. */
+pmx_status pmx_upsample2x(const void* x, int32_t dtype, int32_t batch, int32_t h, int32_t w,
+                          int32_t c, void* out, pmx_stream_t stream);
+
+/* ------------------------------------------------------------------------
+ * K11 anchor decode + top-k (KITTI extension; no reference counterpart --
+ * conventions of pm/detector.py:266-307: f64-exact ordering, stable ties).
+ * Candidates: flat anchor index a = (y * W + x) * n_anchors + k, ranked by f32
+ * cls logit descending, ties to the lower index.  Boxes: SECOND delta coder.
+ * ---------------------------------------------------------------------- */
+typedef struct {
+  int32_t n_anchors;   /* A (<= 4); cls has A channels, box 7A, dir 2A */
+  int32_t k;           /* top-k (<= 512) */
+  float x_min, y_min, stride_x, stride_y;
+  float anchor_z, anchor_w, anchor_l, anchor_h;
+  float rotations[4];
+  float dir_offset;
+  float _pad;
+} pmx_anchor_desc;
+
+size_t pmx_decode_workspace(const pmx_anchor_desc* desc, int32_t batch, int32_t out_h,
+                            int32_t out_w);
+
+/* heads: f32 NHWC [B, H, W, head_c_stride]; cls/box/dir channel offsets.
+ * Outputs: topk_idx [B,k] int32, topk_logit [B,k] f32, boxes [B,k,7] f32,
+ * dir_label [B,k] int32. */
+pmx_status pmx_decode_topk(const pmx_anchor_desc* desc, int32_t batch, int32_t out_h,
+                           int32_t out_w, const float* heads, int32_t head_c_stride,
+                           int32_t cls_off, int32_t box_off, int32_t dir_off, int32_t* topk_idx,
+                           float* topk_logit, float* boxes, int32_t* dir_label, void* ws,
+                           size_t ws_bytes, pmx_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PMX_H_ */

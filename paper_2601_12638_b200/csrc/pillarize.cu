@@ -1,0 +1,444 @@
+// K3 pillarize (pm/scenes.py:155-193 + KITTI cap) and feature materialisation.
+//
+// Deterministic with atomics:
+//  1 bin      per point: cell (IEEE f32 divide, trunc, clamp), atomicMin(first[cell], i),
+//             atomicAdd(cnt[cell], 1)                           -- coalesced float4 loads
+//  2 flags    per point block: #points that are the first of their cell
+//  3 thresh   per frame: T = index of the P_max-th first-seen point (cap rule), or INT_MAX
+//  4 cellcnt  per cell block: kept = cnt>0 && first<=T; (kept, kept points) block sums
+//  5 cellscan per frame: exclusive scan of block sums -> n_pillars
+//  6 emit     per cell block: pillar id in ascending flat order, coords, segment offsets
+//  7 slot     per point: atomic slot in its pillar's CSR segment (arbitrary order)
+//  8 select   warp per pillar: the first M points of the segment by scene index
+//             (shuffle ranks; a warp threshold search when the cell holds > 32 points)
+#include <climits>
+
+#include "pmx_common.cuh"
+
+namespace pmx {
+
+namespace {
+
+constexpr int kPtBlock = 1024;   // points per flag block
+constexpr int kCellPerThr = 4;
+constexpr int kCellBlock = 1024 * kCellPerThr;
+
+struct PillarWs {
+  int32_t* first;   // [B*HW]
+  int32_t* cnt;     // [B*HW]
+  int32_t* pid;     // [B*HW]
+  int32_t* cell;    // [B*Nmax]
+  int32_t* ptblk;   // [B*NB]
+  int32_t* thresh;  // [B]
+  int2* cblk;       // [B*CB]
+  int32_t* segoff;  // [B*Pcap]
+  int32_t* fill;    // [B*Pcap]
+  int32_t* csr;     // [B*Nmax]
+};
+
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+size_t carve(const pmx_grid* g, int32_t B, int64_t nmax, int32_t pcap, void* base, PillarWs* ws) {
+  int64_t hw = (int64_t)g->grid_h * g->grid_w;
+  int64_t nb = ceil_div(nmax > 0 ? nmax : 1, kPtBlock);
+  int64_t cb = ceil_div(hw, kCellBlock);
+  size_t off = 0;
+  char* p = static_cast<char*>(base);
+  auto take = [&](size_t bytes) {
+    void* r = p ? p + off : nullptr;
+    off += align256(bytes);
+    return r;
+  };
+  PillarWs w;
+  w.first = (int32_t*)take(sizeof(int32_t) * B * hw);
+  w.cnt = (int32_t*)take(sizeof(int32_t) * B * hw);
+  w.pid = (int32_t*)take(sizeof(int32_t) * B * hw);
+  w.cell = (int32_t*)take(sizeof(int32_t) * B * (nmax > 0 ? nmax : 1));
+  w.ptblk = (int32_t*)take(sizeof(int32_t) * B * nb);
+  w.thresh = (int32_t*)take(sizeof(int32_t) * B);
+  w.cblk = (int2*)take(sizeof(int2) * B * cb);
+  w.segoff = (int32_t*)take(sizeof(int32_t) * B * pcap);
+  w.fill = (int32_t*)take(sizeof(int32_t) * B * pcap);
+  w.csr = (int32_t*)take(sizeof(int32_t) * B * (nmax > 0 ? nmax : 1));
+  if (ws) *ws = w;
+  return off;
+}
+
+__device__ __forceinline__ int bin_cell(float x, float y, const pmx_grid g) {
+  // pm/scenes.py:177-178: (f32(p) - origin) / cell in IEEE f32, astype(int64) truncates, clip
+  float fy = __fdiv_rn(__fsub_rn(y, g.y_min), g.cell_h);
+  float fx = __fdiv_rn(__fsub_rn(x, g.x_min), g.cell_w);
+  // truncation toward zero of values far outside the grid: clamp in float first
+  fy = fminf(fmaxf(fy, -1.0f), (float)g.grid_h);
+  fx = fminf(fmaxf(fx, -1.0f), (float)g.grid_w);
+  int r = (int)fy, c = (int)fx;  // (int) truncates toward zero
+  if (fy != fy) r = 0;          // NaN: reference behaviour undefined; pin to 0
+  if (fx != fx) c = 0;
+  r = r < 0 ? 0 : (r > g.grid_h - 1 ? g.grid_h - 1 : r);
+  c = c < 0 ? 0 : (c > g.grid_w - 1 ? g.grid_w - 1 : c);
+  return r * g.grid_w + c;
+}
+
+__global__ void bin_kernel(const float4* __restrict__ pts, const int64_t* __restrict__ offs, int64_t nmax,
+                           const pmx_grid g, PillarWs w) {
+  const int b = blockIdx.y;
+  const int64_t base = offs[b];
+  const int64_t n = offs[b + 1] - base;
+  const int64_t hw = (int64_t)g.grid_h * g.grid_w;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    float4 p = __ldg(pts + base + i);
+    int cell = bin_cell(p.x, p.y, g);
+    w.cell[b * nmax + i] = cell;
+    atomicMin(w.first + b * hw + cell, (int)i);
+    atomicAdd(w.cnt + b * hw + cell, 1);
+  }
+}
+
+__global__ void __launch_bounds__(kPtBlock) flag_kernel(const int64_t* __restrict__ offs, int64_t nmax,
+                                                        const pmx_grid g, PillarWs w, int nb) {
+  const int b = blockIdx.y;
+  const int64_t n = offs[b + 1] - offs[b];
+  const int64_t hw = (int64_t)g.grid_h * g.grid_w;
+  int64_t i = (int64_t)blockIdx.x * kPtBlock + threadIdx.x;
+  int flag = 0;
+  if (i < n) flag = w.first[b * hw + w.cell[b * nmax + i]] == (int)i;
+  int c = __syncthreads_count(flag);
+  if (threadIdx.x == 0) w.ptblk[b * nb + blockIdx.x] = c;
+}
+
+// inclusive block scan of one int per thread (blockDim.x == 1024)
+__device__ int block_incl_scan(int v, int* sh /*32*/) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int o = 1; o < 32; o <<= 1) {
+    int t = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += t;
+  }
+  if (lane == 31) sh[wid] = v;
+  __syncthreads();
+  if (wid == 0) {
+    int s = sh[lane];
+    for (int o = 1; o < 32; o <<= 1) {
+      int t = __shfl_up_sync(0xffffffffu, s, o);
+      if (lane >= o) s += t;
+    }
+    sh[lane] = s;
+  }
+  __syncthreads();
+  if (wid > 0) v += sh[wid - 1];
+  __syncthreads();
+  return v;
+}
+
+__global__ void __launch_bounds__(1024) thresh_kernel(const int64_t* __restrict__ offs, int64_t nmax,
+                                                      const pmx_grid g, PillarWs w, int nb) {
+  __shared__ int sh[32];
+  __shared__ int s_blk, s_need;
+  const int b = blockIdx.x;
+  const int64_t n = offs[b + 1] - offs[b];
+  const int64_t hw = (int64_t)g.grid_h * g.grid_w;
+  if (g.max_pillars <= 0) {
+    if (threadIdx.x == 0) w.thresh[b] = INT_MAX;
+    return;
+  }
+  if (threadIdx.x == 0) {
+    int cum = 0, blk = -1, need = 0;
+    for (int k = 0; k < nb; ++k) {
+      int c = w.ptblk[b * nb + k];
+      if (cum + c >= g.max_pillars + 1) {  // the cap binds only if more than max_pillars cells
+        blk = k;
+        need = g.max_pillars - cum;      // the need-th first-seen point in this block is the last kept
+        break;
+      }
+      cum += c;
+    }
+    s_blk = blk;
+    s_need = need;
+  }
+  __syncthreads();
+  if (s_blk < 0) {
+    if (threadIdx.x == 0) w.thresh[b] = INT_MAX;
+    return;
+  }
+  if (s_need == 0) {  // the cap is reached exactly before this block
+    // the last kept first-point lies in an earlier block: T = (first index of blk) - 1
+    if (threadIdx.x == 0) w.thresh[b] = s_blk * kPtBlock - 1;
+    return;
+  }
+  int64_t i = (int64_t)s_blk * kPtBlock + threadIdx.x;
+  int flag = 0;
+  if (i < n) flag = w.first[b * hw + w.cell[b * nmax + i]] == (int)i;
+  int inc = block_incl_scan(flag, sh);
+  if (flag && inc == s_need) w.thresh[b] = (int)i;
+}
+
+__global__ void __launch_bounds__(1024) cellcount_kernel(const pmx_grid g, PillarWs w, int cb) {
+  __shared__ int sh[32];
+  const int b = blockIdx.y;
+  const int64_t hw = (int64_t)g.grid_h * g.grid_w;
+  const int T = w.thresh[b];
+  int kept = 0, pts = 0;
+  int64_t c0 = (int64_t)blockIdx.x * kCellBlock + threadIdx.x * kCellPerThr;
+#pragma unroll
+  for (int j = 0; j < kCellPerThr; ++j) {
+    int64_t c = c0 + j;
+    if (c < hw) {
+      int n = w.cnt[b * hw + c];
+      if (n > 0 && w.first[b * hw + c] <= T) {
+        kept += 1;
+        pts += n;
+      }
+    }
+  }
+  int a = block_incl_scan(kept, sh);
+  int p = block_incl_scan(pts, sh);
+  if (threadIdx.x == blockDim.x - 1) w.cblk[b * cb + blockIdx.x] = make_int2(a, p);
+}
+
+__global__ void cellscan_kernel(PillarWs w, int cb, int32_t* n_pillars) {
+  const int b = blockIdx.x;
+  if (threadIdx.x != 0) return;
+  int a = 0, p = 0;
+  for (int k = 0; k < cb; ++k) {
+    int2 v = w.cblk[b * cb + k];
+    w.cblk[b * cb + k] = make_int2(a, p);
+    a += v.x;
+    p += v.y;
+  }
+  n_pillars[b] = a;
+}
+
+__global__ void __launch_bounds__(1024) emit_kernel(const pmx_grid g, PillarWs w, int cb, int32_t pcap,
+                                                    int32_t* coords, int32_t* counts) {
+  __shared__ int sh[32];
+  const int b = blockIdx.y;
+  const int64_t hw = (int64_t)g.grid_h * g.grid_w;
+  const int T = w.thresh[b];
+  int64_t c0 = (int64_t)blockIdx.x * kCellBlock + threadIdx.x * kCellPerThr;
+  int keep[kCellPerThr], n[kCellPerThr];
+  int kept = 0, pts = 0;
+#pragma unroll
+  for (int j = 0; j < kCellPerThr; ++j) {
+    int64_t c = c0 + j;
+    keep[j] = 0;
+    n[j] = 0;
+    if (c < hw) {
+      n[j] = w.cnt[b * hw + c];
+      keep[j] = n[j] > 0 && w.first[b * hw + c] <= T;
+    }
+    kept += keep[j];
+    pts += keep[j] ? n[j] : 0;
+  }
+  int a = block_incl_scan(kept, sh) - kept;
+  int p = block_incl_scan(pts, sh) - pts;
+  int2 base = w.cblk[b * cb + blockIdx.x];
+  a += base.x;
+  p += base.y;
+#pragma unroll
+  for (int j = 0; j < kCellPerThr; ++j) {
+    int64_t c = c0 + j;
+    if (c >= hw) break;
+    if (keep[j]) {
+      int64_t q = (int64_t)b * pcap + a;
+      w.pid[b * hw + c] = a;
+      coords[2 * q + 0] = (int)(c / g.grid_w);
+      coords[2 * q + 1] = (int)(c % g.grid_w);
+      counts[q] = n[j] < g.max_points ? n[j] : g.max_points;
+      w.segoff[q] = p;
+      a += 1;
+      p += n[j];
+    } else {
+      w.pid[b * hw + c] = -1;
+    }
+  }
+}
+
+__global__ void slot_kernel(const int64_t* __restrict__ offs, int64_t nmax, const pmx_grid g, PillarWs w,
+                            int32_t pcap) {
+  const int b = blockIdx.y;
+  const int64_t n = offs[b + 1] - offs[b];
+  const int64_t hw = (int64_t)g.grid_h * g.grid_w;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    int p = w.pid[b * hw + w.cell[b * nmax + i]];
+    if (p >= 0) {
+      int64_t q = (int64_t)b * pcap + p;
+      int s = atomicAdd(w.fill + q, 1);
+      w.csr[b * nmax + w.segoff[q] + s] = (int)i;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) select_kernel(const int64_t* __restrict__ offs, int64_t nmax,
+                                                     const pmx_grid g, PillarWs w, int32_t pcap,
+                                                     const int32_t* __restrict__ n_pillars, int32_t* pt_idx) {
+  __shared__ int buf[8][32];
+  const int b = blockIdx.y;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int p = blockIdx.x * 8 + wid;
+  if (p >= n_pillars[b]) return;
+  const int M = g.max_points;
+  const int64_t q = (int64_t)b * pcap + p;
+  const int c = w.fill[q];
+  const int* seg = w.csr + b * nmax + w.segoff[q];
+  int32_t* dst = pt_idx + q * M;
+  const int kept = c < M ? c : M;
+  if (lane < M && lane >= kept) dst[lane] = -1;
+  int v = INT_MAX;
+  if (c <= 32) {
+    if (lane < c) v = seg[lane];
+  } else {
+    // threshold search: t = the M-th smallest index (indices are distinct)
+    const int n = (int)(offs[b + 1] - offs[b]);
+    int lo = 0, hi = n - 1;
+    while (lo < hi) {
+      int mid = lo + ((hi - lo) >> 1);
+      int cntle = 0;
+      for (int k = lane; k < c; k += 32) cntle += seg[k] <= mid;
+      cntle = __reduce_add_sync(0xffffffffu, cntle);
+      if (cntle >= M) hi = mid; else lo = mid + 1;
+    }
+    const int t = lo;
+    int off = 0;
+    for (int k0 = 0; k0 < c; k0 += 32) {
+      int k = k0 + lane;
+      int val = k < c ? seg[k] : INT_MAX;
+      bool sel = k < c && val <= t;
+      unsigned m = __ballot_sync(0xffffffffu, sel);
+      if (sel) buf[wid][off + __popc(m & ((1u << lane) - 1u))] = val;
+      off += __popc(m);
+    }
+    __syncwarp();
+    if (lane < M) v = buf[wid][lane];
+  }
+  int rank = 0;
+  for (int j = 0; j < 32; ++j) {
+    int u = __shfl_sync(0xffffffffu, v, j);
+    rank += u < v;
+  }
+  if (v != INT_MAX && rank < M) dst[rank] = v;
+}
+
+// ---------------------------------------------------------------------------
+// feature materialisation (PillarSample.features / point_mask)
+
+__global__ void __launch_bounds__(256) features_kernel(const float4* __restrict__ pts, const int64_t* __restrict__ offs,
+                                                       const pmx_grid g, int32_t pcap, int nf,
+                                                       const int32_t* __restrict__ coords,
+                                                       const int32_t* __restrict__ counts,
+                                                       const int32_t* __restrict__ pt_idx,
+                                                       const int32_t* __restrict__ n_pillars, float* feats,
+                                                       uint8_t* mask) {
+  const int b = blockIdx.y;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int p = blockIdx.x * 8 + wid;
+  if (p >= n_pillars[b]) return;
+  const int M = g.max_points;
+  const int64_t q = (int64_t)b * pcap + p;
+  const int k = counts[q];
+  float4 pt = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (lane < k) pt = __ldg(pts + offs[b] + pt_idx[q * M + lane]);
+  // sequential f32 mean over kept points (numpy chunk.mean(axis=0), pm/scenes.py:187)
+  float sx = 0.f, sy = 0.f, sz = 0.f;
+  for (int s = 0; s < k; ++s) {
+    sx = __fadd_rn(sx, __shfl_sync(0xffffffffu, pt.x, s));
+    sy = __fadd_rn(sy, __shfl_sync(0xffffffffu, pt.y, s));
+    sz = __fadd_rn(sz, __shfl_sync(0xffffffffu, pt.z, s));
+  }
+  const float fk = (float)(k > 0 ? k : 1);
+  const float mx = __fdiv_rn(sx, fk), my = __fdiv_rn(sy, fk), mz = __fdiv_rn(sz, fk);
+  if (lane >= M) return;
+  float* f = feats + (q * M + lane) * nf;
+  const bool live = lane < k;
+  mask[q * M + lane] = live ? 1 : 0;
+  if (nf == 5) {
+    f[0] = live ? pt.x : 0.f;
+    f[1] = live ? pt.y : 0.f;
+    f[2] = live ? pt.z : 0.f;
+    f[3] = live ? __fsub_rn(pt.x, mx) : 0.f;
+    f[4] = live ? __fsub_rn(pt.y, my) : 0.f;
+  } else {
+    const float xoff = (float)((double)g.cell_w * 0.5 + (double)g.x_min);
+    const float yoff = (float)((double)g.cell_h * 0.5 + (double)g.y_min);
+    const float xc = __fadd_rn(__fmul_rn((float)coords[2 * q + 1], g.cell_w), xoff);
+    const float yc = __fadd_rn(__fmul_rn((float)coords[2 * q + 0], g.cell_h), yoff);
+    f[0] = live ? pt.x : 0.f;
+    f[1] = live ? pt.y : 0.f;
+    f[2] = live ? pt.z : 0.f;
+    f[3] = live ? pt.w : 0.f;
+    f[4] = live ? __fsub_rn(pt.x, mx) : 0.f;
+    f[5] = live ? __fsub_rn(pt.y, my) : 0.f;
+    f[6] = live ? __fsub_rn(pt.z, mz) : 0.f;
+    f[7] = live ? __fsub_rn(pt.x, xc) : 0.f;
+    f[8] = live ? __fsub_rn(pt.y, yc) : 0.f;
+  }
+}
+
+}  // namespace
+
+}  // namespace pmx
+
+using namespace pmx;
+
+extern "C" {
+
+size_t pmx_pillarize_workspace(const pmx_grid* g, int32_t batch, int64_t max_points_per_frame) {
+  if (!g || batch < 0) return 0;
+  int32_t pcap = g->max_pillars > 0 ? g->max_pillars : g->grid_h * g->grid_w;
+  return carve(g, batch, max_points_per_frame, pcap, nullptr, nullptr);
+}
+
+pmx_status pmx_pillarize(const float* points, const int64_t* frame_offsets, int32_t batch,
+                         int64_t max_points_per_frame, const pmx_grid* grid, int32_t pcap, int32_t* coords,
+                         int32_t* counts, int32_t* pt_idx, int32_t* n_pillars, void* ws, size_t ws_bytes,
+                         pmx_stream_t stream) {
+  PMX_REQUIRE(grid != nullptr, "grid is NULL");
+  const pmx_grid g = *grid;
+  PMX_REQUIRE(g.grid_h >= 1 && g.grid_w >= 1, "grid extents must be positive");
+  PMX_REQUIRE(g.max_points >= 1 && g.max_points <= 32, "max_points must be 1..32");
+  PMX_REQUIRE(g.cell_w > 0.f && g.cell_h > 0.f, "cell sizes must be positive");
+  PMX_REQUIRE(batch >= 0 && max_points_per_frame >= 0, "negative extent");
+  PMX_REQUIRE(max_points_per_frame < INT_MAX, "too many points per frame");
+  const int64_t hw = (int64_t)g.grid_h * g.grid_w;
+  PMX_REQUIRE(hw < INT_MAX / 2, "grid too large");
+  if (g.max_pillars > 0) {
+    PMX_REQUIRE(pcap >= g.max_pillars, "pcap < max_pillars");
+  } else {
+    PMX_REQUIRE(pcap >= hw, "uncapped pillarize needs pcap >= grid_h * grid_w");
+  }
+  if (batch == 0) return PMX_OK;
+  size_t need = carve(&g, batch, max_points_per_frame, pcap, nullptr, nullptr);
+  PMX_REQUIRE(ws != nullptr && ws_bytes >= need, "pillarize workspace too small");
+  PillarWs w;
+  carve(&g, batch, max_points_per_frame, pcap, ws, &w);
+  const int64_t nmax = max_points_per_frame > 0 ? max_points_per_frame : 1;
+  const int nb = (int)ceil_div(nmax, kPtBlock);
+  const int cb = (int)ceil_div(hw, kCellBlock);
+  PMX_CUDA(cudaMemsetAsync(w.first, 0x7f, sizeof(int32_t) * batch * hw, stream));
+  PMX_CUDA(cudaMemsetAsync(w.cnt, 0, sizeof(int32_t) * batch * hw, stream));
+  PMX_CUDA(cudaMemsetAsync(w.fill, 0, sizeof(int32_t) * batch * pcap, stream));
+  const int ptx = (int)std::min<int64_t>(ceil_div(nmax, 256), 4096);
+  bin_kernel<<<dim3(ptx, batch), 256, 0, stream>>>(reinterpret_cast<const float4*>(points), frame_offsets, nmax, g, w);
+  flag_kernel<<<dim3(nb, batch), kPtBlock, 0, stream>>>(frame_offsets, nmax, g, w, nb);
+  thresh_kernel<<<batch, 1024, 0, stream>>>(frame_offsets, nmax, g, w, nb);
+  cellcount_kernel<<<dim3(cb, batch), 1024, 0, stream>>>(g, w, cb);
+  cellscan_kernel<<<batch, 32, 0, stream>>>(w, cb, n_pillars);
+  emit_kernel<<<dim3(cb, batch), 1024, 0, stream>>>(g, w, cb, pcap, coords, counts);
+  slot_kernel<<<dim3(ptx, batch), 256, 0, stream>>>(frame_offsets, nmax, g, w, pcap);
+  select_kernel<<<dim3((int)ceil_div(pcap, 8), batch), 256, 0, stream>>>(frame_offsets, nmax, g, w, pcap, n_pillars, pt_idx);
+  return check_launch("pmx_pillarize");
+}
+
+pmx_status pmx_pillar_features(const float* points, const int64_t* frame_offsets, int32_t batch,
+                               const pmx_grid* grid, int32_t pcap, int32_t n_features, const int32_t* coords,
+                               const int32_t* counts, const int32_t* pt_idx, const int32_t* n_pillars,
+                               float* features, uint8_t* mask, pmx_stream_t stream) {
+  PMX_REQUIRE(grid != nullptr, "grid is NULL");
+  PMX_REQUIRE(n_features == 5 || n_features == 9, "n_features must be 5 or 9");
+  PMX_REQUIRE(grid->max_points >= 1 && grid->max_points <= 32, "max_points must be 1..32");
+  if (batch == 0 || pcap == 0) return PMX_OK;
+  features_kernel<<<dim3((int)ceil_div(pcap, 8), batch), 256, 0, stream>>>(
+      reinterpret_cast<const float4*>(points), frame_offsets, *grid, pcap, n_features, coords, counts, pt_idx,
+      n_pillars, features, mask);
+  return check_launch("pmx_pillar_features");
+}
+
+}  // extern "C"

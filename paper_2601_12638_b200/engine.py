@@ -1,0 +1,772 @@
+"""Graph compiler + executor: ModelGraph -> a static schedule of libpmx launches.
+
+The reference executes its chain layer by layer in numpy (pm/model.py:310-367),
+applying each weight layer's precision transform to that layer's *input*
+(pm/model.py:271-307).  This executor compiles the same semantics once:
+
+* every tensor (value) is stored NHWC in HBM in each format its consumers need:
+  int8 codes at the consumer's activation scale, binary16, or f32 -- so the
+  transform is fused into the *producer's* epilogue and never re-reads HBM;
+* precision-free glue is folded away: maxpool + scatter fuse into the PFN
+  kernel (quantize/fp16 are monotone, so they commute with max; zeros map to
+  zeros), ``concat`` is zero-copy (producers write channel slices), heads read
+  the concat directly;
+* observers (calibration) are min/max key slots widened inside the producing
+  kernels; a weight layer's observer is its source value's slot;
+* the launch list is fixed for a (graph, plan, stats, batch) so the whole frame
+  pipeline -- pillarize, PFN+scatter, 16 convs, 3 deconvs, heads, top-k -- is
+  captured into one CUDA graph and replayed.
+
+No CPU fallback: every op is a libpmx call; compile() fails loudly without CUDA.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as N
+from .quant import DType, PerChannelQuantParams, to_fp16_bits, weight_codes
+from .tensor_ops import PillarSample
+
+__all__ = ["CompiledGraph", "GridSpec", "AnchorSpec", "run_graph"]
+
+
+def _prec(layer) -> str:
+    p = layer.precision
+    return getattr(p, "value", p)
+
+
+@dataclass(frozen=True)
+class GridSpec:
+    """Pillar geometry handed to pmx_pillarize (pmx_grid)."""
+
+    grid: tuple[int, int]
+    origin: tuple[float, float]
+    cell: tuple[float, float]
+    max_points: int
+    max_pillars: int | None
+
+    def to_c(self) -> N.Grid:
+        return N.Grid(grid_h=self.grid[0], grid_w=self.grid[1], max_points=self.max_points,
+                      max_pillars=self.max_pillars or 0, x_min=self.origin[0], y_min=self.origin[1],
+                      cell_w=self.cell[0], cell_h=self.cell[1])
+
+
+@dataclass(frozen=True)
+class AnchorSpec:
+    """Anchor decode parameters (pmx_anchor_desc) + which heads hold cls/box/dir."""
+
+    k: int
+    origin: tuple[float, float]
+    out_stride: tuple[float, float]
+    anchor_z: float
+    anchor_size: tuple[float, float, float]  # (w, l, h)
+    rotations: tuple[float, ...]
+    dir_offset: float
+    cls_head: str
+    box_head: str
+    dir_head: str
+
+    def to_c(self) -> N.AnchorDesc:
+        rot = (ctypes.c_float * 4)(*(list(self.rotations) + [0.0] * (4 - len(self.rotations))))
+        return N.AnchorDesc(n_anchors=len(self.rotations), k=self.k, x_min=self.origin[0], y_min=self.origin[1],
+                            stride_x=self.out_stride[0], stride_y=self.out_stride[1], anchor_z=self.anchor_z,
+                            anchor_w=self.anchor_size[0], anchor_l=self.anchor_size[1],
+                            anchor_h=self.anchor_size[2], rotations=rot, dir_offset=self.dir_offset)
+
+
+# ---------------------------------------------------------------------------
+
+
+class _Value:
+    def __init__(self, name: str, shape: tuple[int, int, int, int], logical=None):
+        self.name = name
+        self.shape = shape              # (B, H, W, C) NHWC
+        self.logical = logical          # leading dims for row-tensors (linear), None for images
+        self.need: dict = {}            # fmt key -> None (ordered set)
+        self.bufs: dict = {}            # fmt key -> (tensor, c_stride, c_offset)
+        self.alias = None               # (concat value, channel offset)
+        self.slot: int | None = None    # observer slot
+        self.upsample_of: "_Value | None" = None
+
+
+def _fmt_of(layer, stats) -> tuple:
+    p = _prec(layer)
+    if p == "int8":
+        if stats is None or layer.index not in stats:
+            raise RuntimeError(
+                f"layer {layer.index} ({layer.name!r}) is tagged int8 but calibration "
+                "stats supply no quant params for it"
+            )
+        return ("int8", float(stats[layer.index].act_qp.scale))
+    return (p, None)
+
+
+_F32 = ("fp32", None)
+_DT = {"fp32": N.PMX_F32, "fp16": N.PMX_F16, "int8": N.PMX_I8}
+
+
+class CompiledGraph:
+    """A graph compiled for one input kind and batch size.
+
+    source:
+      "sample" -- one PillarSample (features given, pm/model.py:323-324 path)
+      "points" -- raw point clouds [B frames], pillarized on the GPU (engine path)
+      "array"  -- a plain NCHW / row tensor (chain graphs without a pillar stage)
+    """
+
+    def __init__(self, graph, stats=None, *, source: str, batch: int = 1, grid: GridSpec | None = None,
+                 pcap: int | None = None, max_points_per_frame: int | None = None, n_features: int | None = None,
+                 in_shape: tuple | None = None, observe: bool = False, keep_inputs_f32: bool = False,
+                 anchors: AnchorSpec | None = None):
+        import torch
+
+        self.lib = N.require_cuda()
+        self.torch = torch
+        self.graph = graph
+        self.stats = stats
+        self.source = source
+        self.B = batch
+        self.grid = grid
+        self.anchors = anchors
+        self.observe = observe or keep_inputs_f32
+        self.keep_inputs_f32 = keep_inputs_f32
+        self.ops: list = []
+        self.op_info: dict = {}
+        self.values: dict[str, _Value] = {}
+        self.layer_src: dict[str, list[str]] = {}
+        self.n_slots = 0
+        self._keep = []  # ctypes objects that must outlive the launches
+        self.weights: dict = {}
+        self.head_names: list[str] = []
+        self.final_name: str | None = None
+        self.graph_exec = None
+        self._resolve_sources(in_shape, pcap, n_features, max_points_per_frame)
+        self._shapes()
+        self._needs()
+        self._allocate()
+        self._prep_weights()
+        self._build_ops()
+
+    # ---------------- analysis
+
+    def _resolve_sources(self, in_shape, pcap, n_features, nmax):
+        layers = self.graph.layers
+        self.pfn = None
+        start = 0
+        if self.source in ("sample", "points"):
+            if not (len(layers) >= 3 and layers[0].kind == "linear" and layers[1].kind == "maxpool"
+                    and layers[2].kind == "scatter"):
+                raise NotImplementedError(
+                    "pillar inputs need the graph to start with linear -> maxpool -> scatter "
+                    "(the pillar feature net); got " + ", ".join(l.kind for l in layers[:3]))
+            for l in layers[1:3]:
+                if l.inputs not in (None, (layers[layers.index(l) - 1].name,)):
+                    raise NotImplementedError("maxpool/scatter must consume the previous layer")
+            self.pfn = layers[0]
+            self.pcap = pcap
+            self.nmax = nmax
+            self.n_features = n_features if n_features is not None else layers[0].weight.shape[1]
+            start = 3
+            H, W = self.grid.grid
+            self.input_value = None
+            canvas = _Value(layers[2].name, (self.B, H, W, layers[0].weight.shape[0]))
+            self.values[canvas.name] = canvas
+            self.values[layers[0].name] = _Value(layers[0].name, (self.B, pcap, self.grid.max_points,
+                                                                  layers[0].weight.shape[0]), logical="pfn")
+            self.values[layers[1].name] = self.values[layers[0].name]
+            current = canvas.name
+        else:
+            shp = tuple(in_shape)
+            if len(shp) == 4:
+                v = _Value("__input__", (shp[0], shp[2], shp[3], shp[1]))
+            elif len(shp) >= 1:
+                rows = int(np.prod(shp[:-1])) if len(shp) > 1 else 1
+                v = _Value("__input__", (1, 1, rows, shp[-1]), logical=tuple(shp[:-1]))
+            else:
+                raise ValueError("scalar graph input")
+            self.values[v.name] = v
+            self.input_value = v
+            current = v.name
+        trunk = None
+        for l in layers[start:]:
+            if l.kind in ("maxpool", "scatter"):
+                raise NotImplementedError(f"{l.kind} layer {l.name!r} outside the pillar feature net")
+            if l.inputs:
+                srcs = list(l.inputs)
+            elif l.is_head:
+                trunk = current if trunk is None else trunk
+                srcs = [trunk]
+            else:
+                srcs = [current]
+            self.layer_src[l.name] = srcs
+            if l.is_head:
+                self.head_names.append(l.name)
+            else:
+                current = l.name
+        self.final_name = current
+
+    def _shapes(self):
+        vals = self.values
+        for l in self.graph.layers:
+            if l.name not in self.layer_src:
+                continue
+            srcs = [vals[s] for s in self.layer_src[l.name]]
+            v0 = srcs[0]
+            B, H, W, C = v0.shape
+            if l.kind == "linear":
+                if l.weight.shape[1] != C:
+                    raise ValueError(f"linear input features {C} != weight in-features {l.weight.shape[1]}")
+                out = _Value(l.name, (B, H, W, l.weight.shape[0]), logical=v0.logical)
+            elif l.kind == "conv2d":
+                if v0.logical is not None:
+                    raise ValueError(f"conv2d expects 4D input/weight, got rows input for {l.name!r}")
+                if l.weight.shape[1] != C:
+                    raise ValueError(f"conv2d input channels {C} != weight channels {l.weight.shape[1]}")
+                ho, wo = l.conv.out_size((H, W), l.weight.shape[2:])
+                out = _Value(l.name, (B, ho, wo, l.weight.shape[0]))
+            elif l.kind == "deconv2d":
+                if l.weight.shape[1] != C:
+                    raise ValueError(f"deconv2d input channels {C} != weight channels {l.weight.shape[1]}")
+                k = l.weight.shape[2:]
+                if tuple(k) != tuple(l.conv.stride) or any(p != 0 for p in l.conv.padding):
+                    raise NotImplementedError("deconv2d supports kernel == stride without padding")
+                out = _Value(l.name, (B, H * k[0], W * k[1], l.weight.shape[0]))
+            elif l.kind == "upsample2x":
+                out = _Value(l.name, (B, 2 * H, 2 * W, C))
+                out.upsample_of = v0
+            elif l.kind == "concat":
+                if any(s.shape[:3] != v0.shape[:3] for s in srcs):
+                    raise ValueError(f"concat {l.name!r} inputs differ in spatial extent")
+                out = _Value(l.name, (B, H, W, sum(s.shape[3] for s in srcs)))
+            else:
+                raise ValueError(f"unknown kind {l.kind!r}")
+            vals[l.name] = out
+
+    def _consumers(self):
+        cons: dict[str, list] = {}
+        for l in self.graph.layers:
+            for s in self.layer_src.get(l.name, []):
+                cons.setdefault(s, []).append(l)
+        return cons
+
+    def _needs(self):
+        cons = self._consumers()
+        self.cons = cons
+        # reverse topological order (layers are listed topologically; the input comes first)
+        order = list(reversed((["__input__"] if self.input_value is not None else []) +
+                              [l.name for l in self.graph.layers if l.name in self.values]))
+        for name in order:
+            v = self.values[name]
+            if self.pfn is not None and name in (self.pfn.name, self.graph.layers[1].name):
+                continue
+            if name in self.head_names or name == self.final_name:
+                v.need[_F32] = None
+            for c in cons.get(name, []):
+                if c.is_weight_layer:
+                    v.need[_fmt_of(c, self.stats)] = None
+                    if self.keep_inputs_f32:
+                        v.need[_F32] = None
+                else:
+                    out = self.values[c.name]
+                    for f in out.need:
+                        v.need[f] = None
+        # observer slots: one per value that feeds a weight layer (concat inputs share)
+        if self.observe:
+            slot_of: dict[str, int] = {}
+
+            def slot_for(name):
+                v = self.values[name]
+                if v.upsample_of is not None:
+                    return slot_for(v.upsample_of.name)
+                if name not in slot_of:
+                    slot_of[name] = self.n_slots
+                    self.n_slots += 1
+                return slot_of[name]
+
+            self.layer_slot = {}
+            if self.pfn is not None:
+                self.pfn_in_slot = self.n_slots
+                self.n_slots += 1
+                self.layer_slot[self.pfn.index] = self.pfn_in_slot
+            for l in self.graph.layers:
+                if l.is_weight_layer and l.name in self.layer_src:
+                    self.layer_slot[l.index] = slot_for(self.layer_src[l.name][0])
+            for name, s in slot_of.items():
+                v = self.values[name]
+                v.slot = s
+                if v.logical is None and self._is_concat(name):
+                    for src in self.layer_src[name]:
+                        self.values[src].slot = s
+
+    def _is_concat(self, name):
+        for l in self.graph.layers:
+            if l.name == name:
+                return l.kind == "concat"
+        return False
+
+    # ---------------- memory
+
+    def _empty(self, shape, fmt):
+        torch = self.torch
+        dt = {"fp32": torch.float32, "fp16": torch.float16, "int8": torch.int8}[fmt[0]]
+        return torch.empty(shape, dtype=dt, device="cuda")
+
+    def _allocate(self):
+        torch = self.torch
+        if self.anchors is not None:
+            # the three heads write straight into one NHWC f32 block [B, H, W, A + 7A + 2A]
+            a = self.anchors
+            A = len(a.rotations)
+            self.head_ctot = 10 * A
+            cls_v = self.values[a.cls_head]
+            B, H, W, _ = cls_v.shape
+            self.heads_cat = torch.empty((B, H, W, self.head_ctot), dtype=torch.float32, device="cuda")
+            for name, off, c in ((a.cls_head, 0, A), (a.box_head, A, 7 * A), (a.dir_head, 8 * A, 2 * A)):
+                v = self.values[name]
+                if v.shape != (B, H, W, c) or list(v.need) != [_F32]:
+                    raise ValueError(f"head {name!r} has shape {v.shape}, expected {(B, H, W, c)}")
+                v.bufs[_F32] = (self.heads_cat, self.head_ctot, off)
+        # concat buffers first; their inputs alias channel slices
+        for l in self.graph.layers:
+            if l.kind != "concat" or l.name not in self.values:
+                continue
+            v = self.values[l.name]
+            off = 0
+            for s in self.layer_src[l.name]:
+                u = self.values[s]
+                u.alias = (v, off)
+                for f in v.need:
+                    u.need[f] = None
+                off += u.shape[3]
+        for name, v in self.values.items():
+            if v.logical == "pfn":
+                continue
+            if v.alias is not None:
+                continue
+            for f in v.need:
+                if f not in v.bufs:
+                    v.bufs[f] = (self._empty(v.shape, f), v.shape[3], 0)
+        for name, v in self.values.items():
+            if v.alias is not None:
+                cv, off = v.alias
+                for f in list(v.need):
+                    if f not in cv.bufs:
+                        # a fan-out consumer of a concat input needs a format the concat does not
+                        raise NotImplementedError(f"value {name!r} needs format {f} outside its concat")
+                    t, cs, _ = cv.bufs[f]
+                    v.bufs[f] = (t, cs, off)
+        self.keys = torch.empty((max(self.n_slots, 1), 2), dtype=torch.int32, device="cuda")
+        if self.source == "points":
+            B, pcap, M = self.B, self.pcap, self.grid.max_points
+            self.points = torch.zeros((self.B * self.nmax, 4), dtype=torch.float32, device="cuda")
+            self.offsets = torch.zeros((self.B + 1,), dtype=torch.int64, device="cuda")
+            self.coords = torch.empty((B, pcap, 2), dtype=torch.int32, device="cuda")
+            self.counts = torch.empty((B, pcap), dtype=torch.int32, device="cuda")
+            self.pt_idx = torch.empty((B, pcap, M), dtype=torch.int32, device="cuda")
+            self.n_pillars = torch.zeros((B,), dtype=torch.int32, device="cuda")
+            g = self.grid.to_c()
+            self._keep.append(g)
+            self.pws_bytes = self.lib.pmx_pillarize_workspace(ctypes.byref(g), B, self.nmax)
+            self.pws = torch.empty(max(self.pws_bytes, 1), dtype=torch.uint8, device="cuda")
+        elif self.source == "sample":
+            pcap, M = self.pcap, self.grid.max_points
+            self.features = torch.zeros((1, max(pcap, 1), M, self.n_features), dtype=torch.float32, device="cuda")
+            self.mask = torch.zeros((1, max(pcap, 1), M), dtype=torch.uint8, device="cuda")
+            self.coords = torch.zeros((1, max(pcap, 1), 2), dtype=torch.int32, device="cuda")
+            self.counts = torch.zeros((1, max(pcap, 1)), dtype=torch.int32, device="cuda")
+            self.n_pillars = torch.zeros((1,), dtype=torch.int32, device="cuda")
+        else:
+            self.input_f32 = torch.empty(self.input_value.shape, dtype=torch.float32, device="cuda")
+        if self.anchors is not None:
+            a = self.anchors
+            B = self.B
+            self.topk_idx = torch.empty((B, a.k), dtype=torch.int32, device="cuda")
+            self.topk_logit = torch.empty((B, a.k), dtype=torch.float32, device="cuda")
+            self.topk_boxes = torch.empty((B, a.k, 7), dtype=torch.float32, device="cuda")
+            self.topk_dir = torch.empty((B, a.k), dtype=torch.int32, device="cuda")
+
+    # ---------------- weights (one-time prep on the device)
+
+    def _prep_weights(self):
+        torch = self.torch
+        for l in self.graph.layers:
+            if not l.is_weight_layer or (l.name not in self.layer_src and l is not self.pfn):
+                continue
+            p = _prec(l)
+            w = np.asarray(l.weight, np.float32)
+            cout = w.shape[0]
+            if l.kind == "deconv2d":
+                kh, kw = w.shape[2:]
+                w2 = np.ascontiguousarray(w.transpose(2, 3, 0, 1).reshape(kh * kw * cout, w.shape[1]))
+                row_rep = kh * kw
+            elif l.kind == "conv2d":
+                w2 = np.ascontiguousarray(w.transpose(0, 2, 3, 1).reshape(cout, -1))
+                row_rep = 1
+            else:
+                w2 = np.ascontiguousarray(w.reshape(cout, -1))
+                row_rep = 1
+            rec = {"precision": p, "alpha": None}
+            if p == "int8":
+                entry = self.stats[l.index]
+                act = float(entry.act_qp.scale)
+                wqp = entry.weight_qp
+                if isinstance(wqp, PerChannelQuantParams) or hasattr(wqp, "scales"):
+                    ws = np.asarray(wqp.scales, np.float64)
+                    if ws.shape != (cout,):
+                        raise ValueError(f"layer {l.name!r}: {ws.shape[0]} weight scales for {cout} channels")
+                    qp = PerChannelQuantParams(scales=np.tile(ws, row_rep))
+                else:
+                    ws = np.full(cout, float(wqp.scale))
+                    qp = PerChannelQuantParams(scales=np.full(w2.shape[0], float(wqp.scale)))
+                rec["w"] = weight_codes(w2, qp)
+                rec["alpha"] = torch.from_numpy((act * ws).astype(np.float32)).cuda()
+            elif p == "fp16":
+                rec["w"] = to_fp16_bits(w2)
+            else:
+                rec["w"] = torch.from_numpy(w2).cuda()
+            rec["bias"] = torch.from_numpy(np.ascontiguousarray(l.bias, np.float32)).cuda()
+            rec["bn"] = None
+            if l.bn is not None:
+                bn = l.bn
+                factor = (bn.gamma / np.sqrt(bn.var + np.float32(bn.eps))).astype(np.float32)
+                rec["bn"] = torch.from_numpy(np.stack([bn.mean.astype(np.float32), factor,
+                                                       bn.beta.astype(np.float32)])).cuda().contiguous()
+            self.weights[l.name] = rec
+
+    # ---------------- schedule
+
+    def _outs_for(self, v: _Value):
+        outs = []
+        for f in v.need:
+            t, cs, off = v.bufs[f]
+            outs.append(N.Out(ptr=t.data_ptr(), scale=f[1] or 0.0, dtype=_DT[f[0]], c_stride=cs, c_offset=off))
+        if len(outs) > N.PMX_MAX_OUTS:
+            raise NotImplementedError(f"value {v.name!r} needs {len(outs)} formats (max {N.PMX_MAX_OUTS})")
+        arr, n = N.outs_array(outs)
+        self._keep.append(arr)
+        return arr, n
+
+    def _key_ptr(self, slot):
+        if slot is None or not self.observe:
+            return None
+        return self.keys.data_ptr() + 8 * slot
+
+    def _build_ops(self):
+        lib = self.lib
+        ops = self.ops
+        if self.observe and self.n_slots:
+            ops.append(("minmax_init", lambda s: N.check(lib.pmx_minmax_init(self.keys.data_ptr(), self.n_slots, s),
+                                                          "minmax_init")))
+        if self.source == "points":
+            g = self._keep[0]
+            co, cn, pi, npil = self.coords, self.counts, self.pt_idx, self.n_pillars
+            ops.append(("pillarize", lambda s: N.check(lib.pmx_pillarize(
+                self.points.data_ptr(), self.offsets.data_ptr(), self.B, self.nmax, ctypes.byref(g), self.pcap,
+                co.data_ptr(), cn.data_ptr(), pi.data_ptr(), npil.data_ptr(), self.pws.data_ptr(), self.pws_bytes,
+                s), "pillarize")))
+        if self.pfn is not None:
+            self._op_pfn()
+        elif self.input_value is not None:
+            self._op_input()
+        for l in self.graph.layers:
+            if l.name not in self.layer_src:
+                continue
+            if l.is_weight_layer:
+                self._op_conv(l)
+            elif l.kind == "upsample2x":
+                self._op_upsample(l)
+        if self.anchors is not None:
+            self._op_decode()
+
+    def _op_input(self):
+        v = self.input_value
+        arr, n = self._outs_for(v)
+        pix = v.shape[0] * v.shape[1] * v.shape[2]
+        lib = self.lib
+        keys = self._key_ptr(v.slot)
+        self.ops.append(("stage_input", lambda s: N.check(lib.pmx_cast_out(
+            self.input_f32.data_ptr(), pix, v.shape[3], arr, n, keys, s), "stage input")))
+
+    def _op_pfn(self):
+        l = self.pfn
+        lib = self.lib
+        canvas = self.values[self.graph.layers[2].name]
+        rec = self.weights[l.name]
+        p = rec["precision"]
+        in_scale = float(self.stats[l.index].act_qp.scale) if p == "int8" else 0.0
+        d = N.PfnDesc(source=N.PMX_PFN_FROM_POINTS9 if self.source == "points" else N.PMX_PFN_FROM_FEATURES,
+                      in_dtype=_DT[p], n_features=self.n_features, channels=l.weight.shape[0],
+                      max_points=self.grid.max_points, relu=int(l.relu), in_scale=in_scale)
+        g = self.grid.to_c()
+        self._keep += [d, g]
+        arr, n = self._outs_for(canvas)
+        zero = [(t.data_ptr(), t.numel() * t.element_size()) for (t, _, _) in canvas.bufs.values()]
+        in_keys = self._key_ptr(getattr(self, "pfn_in_slot", None))
+        out_keys = self._key_ptr(canvas.slot)
+        pts = self.points.data_ptr() if self.source == "points" else None
+        offs = self.offsets.data_ptr() if self.source == "points" else None
+        feats = self.features.data_ptr() if self.source == "sample" else None
+        mask = self.mask.data_ptr() if self.source == "sample" else None
+        pt_idx = self.pt_idx.data_ptr() if self.source == "points" else None
+        pcap = max(self.pcap, 1)
+
+        def run(s):
+            for ptr_, nbytes in zero:
+                N.check(lib.pmx_zero(ptr_, nbytes, s), "zero canvas")
+            N.check(lib.pmx_pfn_scatter(
+                ctypes.byref(d), ctypes.byref(g), self.B, pcap, pts, offs, feats, mask, self.coords.data_ptr(),
+                self.counts.data_ptr(), pt_idx, self.n_pillars.data_ptr(), rec["w"].data_ptr(),
+                N.ptr(rec["alpha"]), rec["bias"].data_ptr(), N.ptr(rec["bn"]), arr, n, in_keys, out_keys, s),
+                f"pfn {l.name}")
+
+        self.ops.append(("pfn", run))
+
+    def _src_buf(self, l):
+        src = self.values[self.layer_src[l.name][0]]
+        f = _fmt_of(l, self.stats)
+        t, cs, off = src.bufs[f]
+        return src, t, cs, off
+
+    def _op_conv(self, l):
+        lib = self.lib
+        src, t, cs, off = self._src_buf(l)
+        out = self.values[l.name]
+        rec = self.weights[l.name]
+        B, H, W, C = src.shape
+        _, Ho, Wo, Co = out.shape
+        if l.kind == "linear":
+            kind, kh, kw, sh, sw, ph, pw = N.PMX_CONV2D, 1, 1, 1, 1, 0, 0
+        elif l.kind == "conv2d":
+            kind = N.PMX_CONV2D
+            kh, kw = l.weight.shape[2:]
+            (sh, sw), (ph, pw) = l.conv.stride, l.conv.padding
+        else:
+            kind = N.PMX_DECONV2D
+            kh, kw = l.weight.shape[2:]
+            sh, sw, ph, pw = kh, kw, 0, 0
+        d = N.ConvDesc(kind=kind, in_dtype=_DT[rec["precision"]], batch=B, in_h=H, in_w=W, in_c=C, in_c_stride=cs,
+                       in_c_offset=off, out_c=Co, k_h=kh, k_w=kw, stride_h=sh, stride_w=sw, pad_h=ph, pad_w=pw,
+                       out_h=Ho, out_w=Wo, relu=int(l.relu))
+        self._keep.append(d)
+        arr, n = self._outs_for(out)
+        keys = self._key_ptr(out.slot)
+        # algorithmic work of this launch (roofline bookkeeping)
+        m = B * (H * W if kind == N.PMX_DECONV2D else Ho * Wo)
+        n_gemm = Co * (kh * kw if kind == N.PMX_DECONV2D else 1)
+        k_gemm = C * (1 if kind == N.PMX_DECONV2D else kh * kw)
+        esz = {"fp32": 4, "fp16": 2, "int8": 1}
+        out_bytes = sum(B * Ho * Wo * Co * esz[f[0]] for f in out.need)
+        self.op_info[f"conv {l.name}"] = {
+            "flops": 2.0 * m * n_gemm * k_gemm, "precision": rec["precision"],
+            "bytes": B * H * W * C * esz[rec["precision"]] + n_gemm * k_gemm * esz[rec["precision"]] + out_bytes}
+        ws_bytes = lib.pmx_conv_workspace(ctypes.byref(d))
+        ws = self.torch.empty(max(ws_bytes, 1), dtype=self.torch.uint8, device="cuda")
+        self._keep.append(ws)
+        self.ops.append((f"conv {l.name}", lambda s: N.check(lib.pmx_conv(
+            ctypes.byref(d), t.data_ptr(), rec["w"].data_ptr(), N.ptr(rec["alpha"]), rec["bias"].data_ptr(),
+            N.ptr(rec["bn"]), arr, n, keys, ws.data_ptr(), ws_bytes, s), f"layer {l.name}")))
+
+    def _op_upsample(self, l):
+        lib = self.lib
+        out = self.values[l.name]
+        src = out.upsample_of
+        B, H, W, C = src.shape
+        for f in out.need:
+            t_in, cs, off = src.bufs[f]
+            if cs != C or off != 0:
+                raise NotImplementedError("upsample2x of a channel slice")
+            t_out = out.bufs[f][0]
+            self.ops.append((f"upsample {l.name}", lambda s, a=t_in, b=t_out, dt=_DT[f[0]]: N.check(
+                lib.pmx_upsample2x(a.data_ptr(), dt, B, H, W, C, b.data_ptr(), s), "upsample2x")))
+
+    def _op_decode(self):
+        a = self.anchors
+        lib = self.lib
+        B, H, W, _ = self.heads_cat.shape
+        A = len(a.rotations)
+        d = a.to_c()
+        self._keep.append(d)
+        ws_bytes = lib.pmx_decode_workspace(ctypes.byref(d), B, H, W)
+        ws = self.torch.empty(max(ws_bytes, 1), dtype=self.torch.uint8, device="cuda")
+        self._keep.append(ws)
+        ctot = self.head_ctot
+        self.ops.append(("decode", lambda s: N.check(lib.pmx_decode_topk(
+            ctypes.byref(d), B, H, W, self.heads_cat.data_ptr(), ctot, 0, A, 8 * A, self.topk_idx.data_ptr(),
+            self.topk_logit.data_ptr(), self.topk_boxes.data_ptr(), self.topk_dir.data_ptr(), ws.data_ptr(),
+            ws_bytes, s), "decode_topk")))
+
+    # ---------------- execution
+
+    def launch(self, stream=None):
+        s = N.stream_ptr(stream)
+        for _, fn in self.ops:
+            fn(s)
+
+    def timed_launch(self, reps: int = 5) -> dict:
+        """Eager launch with CUDA events around every op on the current stream -> mean ms per op."""
+        torch = self.torch
+        s = N.stream_ptr()
+        acc = {name: 0.0 for name, _ in self.ops}
+        for _ in range(reps):
+            evs = []
+            for name, fn in self.ops:
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record()
+                fn(s)
+                b.record()
+                evs.append((name, a, b))
+            torch.cuda.synchronize()
+            for name, a, b in evs:
+                acc[name] += a.elapsed_time(b)
+        return {k: v / reps for k, v in acc.items()}
+
+    def kernels_per_launch(self) -> int:
+        """Number of libpmx kernels one launch() issues (memsets excluded)."""
+        n = 0
+        for name, _ in self.ops:
+            if name == "pillarize":
+                n += 8
+            elif name == "decode":
+                a = self.anchors
+                B, H, W, _ = self.heads_cat.shape
+                ncand = H * W * len(a.rotations)
+                chunks = -(-ncand // 2048)
+                rounds = 1
+                while chunks > 1:
+                    chunks = -(-(chunks * a.k) // 2048)
+                    rounds += 1
+                n += rounds + 1
+            else:
+                n += 1
+        return n
+
+    def capture(self):
+        """Capture the launch list into a CUDA graph (static buffers, replayable)."""
+        torch = self.torch
+        st = torch.cuda.Stream()
+        st.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(st):
+            self.launch(st)  # warm-up outside capture (lazy module loads)
+        torch.cuda.current_stream().wait_stream(st)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=st):
+            self.launch(st)
+        self.graph_exec = g
+        return g
+
+    def replay(self):
+        self.graph_exec.replay()
+
+    @property
+    def n_launches(self) -> int:
+        return len(self.ops)
+
+    def head_output(self, name: str):
+        """NHWC f32 device view of a head map."""
+        v = self.values[name]
+        t, cs, off = v.bufs[_F32]
+        return t[..., off:off + v.shape[3]]
+
+    def slot_ranges(self) -> np.ndarray:
+        """Observer slots -> float32 [n_slots, 2] (min, max)."""
+        k = self.keys[: self.n_slots].cpu().numpy().view(np.uint32)
+        return N.decode_keys(k)
+
+    def layer_ranges(self) -> dict[int, tuple[float, float]]:
+        r = self.slot_ranges()
+        return {idx: (float(r[s, 0]), float(r[s, 1])) for idx, s in self.layer_slot.items()}
+
+    def value_f32(self, name: str):
+        v = self.values[name]
+        t, cs, off = v.bufs[_F32]
+        return t[..., off:off + v.shape[3]]
+
+
+# ---------------------------------------------------------------------------
+# drop-in forward (pm/model.py:310-367)
+
+
+def _nhwc_to_api(t, v: _Value) -> np.ndarray:
+    a = t.cpu().numpy()
+    if v.logical is not None and v.logical != "pfn":
+        return np.ascontiguousarray(a.reshape(tuple(v.logical) + (v.shape[3],)))
+    return np.ascontiguousarray(a.transpose(0, 3, 1, 2))
+
+
+def _check_sample(graph, sample: PillarSample):
+    """Host-side argument validation with the reference's messages."""
+    layers = graph.layers
+    if len(layers) >= 3 and layers[2].kind == "scatter":
+        grid_l = layers[2].grid
+        if grid_l is not None and tuple(grid_l) != tuple(sample.grid):
+            raise ValueError(f"scatter grid {grid_l} does not match sample grid {sample.grid}")
+    p = sample.features.shape[0]
+    if p and not np.asarray(sample.point_mask).any(axis=1).all():
+        raise ValueError("pillar with no real points cannot be max-pooled")
+    coords = np.asarray(sample.coords, dtype=np.int64).reshape(-1, 2)
+    if coords.shape[0] != p:
+        raise ValueError(f"scatter got {p} pillars but {coords.shape[0]} coords")
+    h, w = sample.grid
+    if p:
+        rows, cols = coords[:, 0], coords[:, 1]
+        bad = (rows < 0) | (rows >= h) | (cols < 0) | (cols >= w)
+        if bad.any():
+            i = int(np.argmax(bad))
+            raise ValueError(f"pillar coord {tuple(coords[i])} outside grid {tuple(sample.grid)}")
+        if len(np.unique(rows * w + cols)) != p:
+            raise ValueError("duplicate pillar coords")
+
+
+def run_graph(graph, x, stats=None, observe_fn=None):
+    import torch
+
+    N.require_cuda()
+    if hasattr(x, "point_mask"):
+        sample = x
+        _check_sample(graph, sample)
+        feats = np.ascontiguousarray(sample.features, np.float32)
+        P, M, F = feats.shape
+        grid = GridSpec(grid=tuple(sample.grid), origin=(0.0, 0.0), cell=(1.0, 1.0), max_points=M,
+                        max_pillars=None)
+        cg = CompiledGraph(graph, stats, source="sample", batch=1, grid=grid, pcap=P, n_features=F,
+                           keep_inputs_f32=observe_fn is not None)
+        if P:
+            cg.features[0, :P].copy_(torch.from_numpy(feats))
+            cg.mask[0, :P].copy_(torch.from_numpy(np.asarray(sample.point_mask, np.uint8)))
+            cg.coords[0, :P].copy_(torch.from_numpy(np.asarray(sample.coords, np.int64).astype(np.int32)))
+        cg.n_pillars.fill_(P)
+        cg.launch()
+    else:
+        arr = np.asarray(x, dtype=np.float32)
+        cg = CompiledGraph(graph, stats, source="array", in_shape=arr.shape, keep_inputs_f32=observe_fn is not None)
+        v = cg.input_value
+        if arr.ndim == 4:
+            cg.input_f32.copy_(torch.from_numpy(np.ascontiguousarray(arr.transpose(0, 2, 3, 1))))
+        else:
+            cg.input_f32.copy_(torch.from_numpy(np.ascontiguousarray(arr)).reshape(v.shape))
+        cg.launch()
+    torch.cuda.synchronize()
+    if observe_fn is not None:
+        for l in graph.layers:
+            if not l.is_weight_layer:
+                continue
+            if cg.pfn is not None and l is cg.pfn:
+                observe_fn(l, x.features)
+                continue
+            src = cg.values[cg.layer_src[l.name][0]]
+            t, cs, off = src.bufs[_F32]
+            t = t[..., off:off + src.shape[3]]
+            observe_fn(l, _nhwc_to_api(t, src))
+    if cg.head_names:
+        outs = []
+        for h in cg.head_names:
+            outs.append(_nhwc_to_api(cg.head_output(h), cg.values[h]))
+        return tuple(outs)
+    v = cg.values[cg.final_name]
+    t, cs, off = v.bufs[_F32]
+    return _nhwc_to_api(t[..., off:off + v.shape[3]], v)

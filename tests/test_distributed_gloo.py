@@ -1,0 +1,57 @@
+"""N>1 host logic on CPU: world_size-2 gloo process group, frame sharding, top-k record
+gather and max-over-ranks timing (the NCCL calls bench.py makes on the GPU box)."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.multiprocessing as mp
+
+from paper_2601_12638_b200 import distributed as D
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world),
+                      LOCAL_RANK=str(rank))
+    r, w, _ = D.init_from_env("gloo")
+    frames = list(D.shard_range(2 * 32, r, w))
+    k = 5
+    topk = {"idx": torch.arange(len(frames) * k, dtype=torch.int32).reshape(len(frames), k) + 1000 * r,
+            "logit": torch.full((len(frames), k), float(r)), "boxes": torch.zeros((len(frames), k, 7)),
+            "dir": torch.ones((len(frames), k), dtype=torch.int32)}
+    rec = D.gather_records(D.pack_topk(topk))
+    t = D.max_over_ranks(1.5 + r)
+    sc = D.gather_scalars([r, 2.0 * r])
+    plans = D.shard_round_robin(list(range(7)), r, w)
+    q.put((r, frames[0], frames[-1], rec.shape, float(rec[32, 0, 0]), float(rec[0, 0, 1]), t, sc.tolist(), plans))
+    torch.distributed.destroy_process_group()
+
+
+def test_two_rank_gather_and_sharding():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    (r0, a0, b0, shape0, idx_r1, logit_r0, t0, sc0, pl0), (r1, a1, b1, shape1, _, _, t1, sc1, pl1) = res
+    assert (a0, b0, a1, b1) == (0, 31, 32, 63)
+    assert tuple(shape0) == (64, 5, D.RECORD) == tuple(shape1)
+    assert idx_r1 == 1000.0 and logit_r0 == 0.0
+    assert t0 == t1 == 2.5
+    assert sc0 == sc1 == [[0.0, 0.0], [1.0, 2.0]]
+    assert pl0 == [0, 2, 4, 6] and pl1 == [1, 3, 5]

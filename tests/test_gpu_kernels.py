@@ -1,0 +1,233 @@
+"""T0 parity of the element-wise / index kernels against the oracle and the reference's
+golden vectors: quantize codes, fake_quant, fp16, observers, pillarize, top-k."""
+
+import json
+
+import numpy as np
+import pytest
+
+from oracle import pillars_oracle as O
+from tests.conftest import GOLDEN
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pm():
+    import paper_2601_12638_b200 as pm
+
+    return pm
+
+
+def test_quantize_golden_bit_exact(pm, golden):
+    g = golden("ref_quant.npz")
+    i = 0
+    while f"x{i}" in g:
+        qp = pm.QuantParams(scale=float(g[f"scale{i}"]))
+        np.testing.assert_array_equal(pm.quantize(g[f"x{i}"], qp), g[f"codes{i}"])
+        np.testing.assert_array_equal(pm.fake_quant(g[f"x{i}"], qp), g[f"fq{i}"])
+        i += 1
+
+
+def test_quantize_near_ties_bit_exact(pm):
+    """f32 estimates alone mismatch ~30% of near-tie codes; the guard band must fix all."""
+    rng = np.random.default_rng(7)
+    for s in (0.0123456789, 0.37, 1.0 / 3.0, 2.54 / 127.0, 5.5):
+        k = rng.integers(-140, 140, size=1_000_000)
+        x = ((k + 0.5) * s * (1.0 + rng.normal(scale=3e-7, size=k.size))).astype(np.float32)
+        x = np.concatenate([x, np.nextafter(x, np.inf), np.nextafter(x, -np.inf)])
+        np.testing.assert_array_equal(pm.quantize(x, pm.QuantParams(scale=s)), O.quantize(x, s))
+        y = rng.normal(scale=50 * s, size=2_000_000).astype(np.float32)
+        np.testing.assert_array_equal(pm.quantize(y, pm.QuantParams(scale=s)), O.quantize(y, s))
+
+
+def test_reference_quant_known_answers(pm):
+    qp = pm.QuantParams(scale=1.0)
+    assert [pm.quantize(v, qp) for v in (2.5, 3.5, -2.5, 1000.0, -1000.0)] == [2, 4, -2, 127, -128]
+    qp = pm.QuantParams(scale=0.03125)
+    t = np.arange(-127, 128, dtype=np.float32) * np.float32(0.03125)
+    np.testing.assert_array_equal(pm.fake_quant(t, qp), t)
+    assert pm.fp16_roundtrip(np.float32(2049.0)) == 2048.0
+    assert pm.fp16_roundtrip(np.float32(1e6)) == 65504.0
+    np.testing.assert_array_equal(pm.fp16_roundtrip(np.array([1e30, -1e30, 65519.0], np.float32)),
+                                  [65504.0, -65504.0, 65504.0])
+    ints = np.arange(-2048, 2049, dtype=np.float32)
+    np.testing.assert_array_equal(pm.fp16_roundtrip(ints), ints)
+    obs = pm.observe(pm.MinMaxObserver(), np.array([-0.5, 2.54]))
+    assert obs.quant_params().scale == 2.54 / 127.0
+    with pytest.raises(ValueError, match="non-finite"):
+        pm.observe(pm.MinMaxObserver(), np.array([1.0, np.nan], np.float32))
+
+
+def test_fp16_golden_and_weight_quant(pm, golden):
+    g = golden("ref_quant.npz")
+    np.testing.assert_array_equal(pm.fp16_roundtrip(g["fp16_in"]), g["fp16_out"])
+    qp = pm.weight_quant_params(g["w"], per_channel=True)
+    np.testing.assert_array_equal(pm.fake_quant_per_channel(g["w"], qp), g["w_fq_pc"])
+    codes = pm.quant.weight_codes(g["w"], qp).cpu().numpy()
+    np.testing.assert_array_equal(codes, O.weight_codes_per_channel(g["w"], qp.scales))
+
+
+def _rne_f16_bits(u):
+    """Independent integer model of clip(+-65504) + round-to-nearest-even f32 -> f16.
+
+    u: int64 tensor of f32 bit patterns.  Returns (f16 bits, is_nan)."""
+    import torch
+
+    sign = (u >> 31) & 1
+    e = (u >> 23) & 0xFF
+    m = u & 0x7FFFFF
+    mant = m | 0x800000
+    ue = e - 127
+    one = torch.ones_like(u)
+
+    def rne_shift(v, sh):
+        q = v >> sh
+        rem = v - (q << sh)
+        half = one << (sh - 1)
+        up = (rem > half) | ((rem == half) & ((q & 1) == 1))
+        return q + up.to(v.dtype)
+
+    normal = ((ue + 15) << 10) + rne_shift(mant, torch.full_like(u, 13)) - 1024
+    sub = rne_shift(mant, (-ue - 1).clamp(14, 40))
+    bits = torch.where(ue >= -14, normal, sub)
+    bits = torch.where(e == 0, torch.zeros_like(bits), bits)
+    big = (ue > 15) | ((ue == 15) & (m > (0x3FF << 13)))
+    bits = torch.where(big | (e == 0xFF), torch.full_like(bits, 0x7BFF), bits)
+    nan = (e == 0xFF) & (m != 0)
+    return (sign << 15) | bits, nan
+
+
+def test_fp16_exhaustive_all_f32_bit_patterns(pm):
+    """All 2^32 f32 inputs: the device cast vs an independent integer RNE model."""
+    import torch
+
+    from paper_2601_12638_b200 import _native as N
+
+    lib = N.load()
+    chunk = 1 << 28
+    for c in range(1 << 4):
+        u = torch.arange(c * chunk, (c + 1) * chunk, dtype=torch.int64, device="cuda")
+        x = (u - (u >= (1 << 31)).long() * (1 << 32)).to(torch.int32).view(torch.float32)
+        out = torch.empty(chunk, dtype=torch.float16, device="cuda")
+        N.check(lib.pmx_fp16_roundtrip(x.data_ptr(), chunk, None, out.data_ptr(), N.stream_ptr()))
+        got = out.view(torch.int16).to(torch.int64) & 0xFFFF
+        want, nan = _rne_f16_bits(u)
+        ok = (got == want) | (nan & ((got & 0x7C00) == 0x7C00) & ((got & 0x3FF) != 0))
+        bad = (~ok).nonzero()
+        assert bad.numel() == 0, (c, hex(int(u[bad[0]])), hex(int(got[bad[0]])), hex(int(want[bad[0]])))
+        del u, x, out, got, want, nan, ok
+
+
+def test_minmax_observer_exact(pm):
+    rng = np.random.default_rng(3)
+    for n in (1, 31, 1000, 1_000_003):
+        x = rng.normal(size=n).astype(np.float32)
+        assert pm.quant.device_minmax(x) == (float(x.min()), float(x.max()))
+
+
+# ----------------------------------------------------------------------------- pillarize
+
+
+def test_pillarize_toy_golden_bit_exact(pm, golden):
+    g = golden("ref_toy.npz")
+    meta = json.loads((GOLDEN / "ref_toy_meta.json").read_text())
+    det = meta["detector"]
+    for i in range(meta["n_samples"]):
+        s = pm.pillarize(pm.Scene(points=g[f"pts{i}"]), tuple(det["grid"]), det["max_points_per_pillar"],
+                         det["field_size"])
+        np.testing.assert_array_equal(s.coords, g[f"coords{i}"])
+        np.testing.assert_array_equal(s.point_mask, g[f"mask{i}"])
+        np.testing.assert_array_equal(s.features, g[f"feat{i}"])
+
+
+def _kitti_case(pm, n, seed, cfg, clustered=False):
+    pts = pm.make_frame(n, seed, cfg)
+    if clustered:  # many points per cell: exercises the M=32 truncation and > 32-point cells
+        rng = np.random.default_rng(seed)
+        c = pts[: n // 4].copy()
+        c[:, 0] = cfg.x_range[0] + 1.0 + rng.uniform(0, 0.3, len(c))
+        c[:, 1] = cfg.y_range[0] + 1.0 + rng.uniform(0, 0.5, len(c))
+        pts = np.concatenate([pts, c]).astype(np.float32)
+        pts = pts[rng.permutation(len(pts))]
+    return pts
+
+
+@pytest.mark.parametrize("n,max_pillars,clustered", [
+    (3000, 1500, False), (3000, 50000, False), (4000, 800, True), (1, 10, False), (0, 10, False),
+])
+def test_pillarize_kitti_vs_oracle(pm, n, max_pillars, clustered):
+    cfg = pm.PointPillarsConfig.small(max_pillars=max_pillars)
+    pts = _kitti_case(pm, n, 11, cfg, clustered) if n else np.zeros((0, 4), np.float32)
+    spec = cfg.grid_spec()
+    got = pm.scenes.pillar_index(pts, spec)
+    flat = O.bin_points(pts[:, :2], spec.grid, spec.origin, spec.cell)
+    want = O.pillar_index(flat, spec.grid, spec.max_points, spec.max_pillars)
+    P = len(want.coords)
+    assert got["n_pillars"] == P
+    np.testing.assert_array_equal(got["coords"], want.coords)
+    np.testing.assert_array_equal(got["counts"], want.counts)
+    np.testing.assert_array_equal(got["pt_idx"], want.pt_idx)
+    if P:
+        s = pm.pillarize_points(pts, spec)
+        f, m = O.pillar_features9(pts, want, spec.origin, spec.cell)
+        np.testing.assert_array_equal(s.features, f)
+        np.testing.assert_array_equal(s.point_mask, m)
+
+
+def test_pillarize_out_of_range_points_clamp(pm):
+    cfg = pm.PointPillarsConfig.small(max_pillars=5000)
+    pts = np.array([[-5.0, -30.0, 0, 0], [1e6, 1e6, 0, 0], [-0.01, 0.0, 0, 0], [7.679, 5.1199, 0, 0]], np.float32)
+    spec = cfg.grid_spec()
+    got = pm.scenes.pillar_index(pts, spec)
+    want = O.pillar_index(O.bin_points(pts[:, :2], spec.grid, spec.origin, spec.cell), spec.grid, 32, 5000)
+    np.testing.assert_array_equal(got["coords"], want.coords)
+    np.testing.assert_array_equal(got["pt_idx"], want.pt_idx)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("n,cap", [(20000, 12000), (120000, 16000), (150000, 16000)])
+def test_pillarize_full_size(pm, n, cap):
+    cfg = pm.PointPillarsConfig(max_pillars=cap)
+    pts = pm.make_frame(n, 5, cfg, outlier_frac=0.01)
+    spec = cfg.grid_spec()
+    got = pm.scenes.pillar_index(pts, spec)
+    want = O.pillar_index(O.bin_points(pts[:, :2], spec.grid, spec.origin, spec.cell), spec.grid, 32, cap)
+    np.testing.assert_array_equal(got["coords"], want.coords)
+    np.testing.assert_array_equal(got["counts"], want.counts)
+    np.testing.assert_array_equal(got["pt_idx"], want.pt_idx)
+
+
+# ----------------------------------------------------------------------------- decode
+
+
+class _Geom:
+    def __init__(self, spec):
+        self.out_stride = spec.out_stride
+        self.origin = spec.origin
+        self.anchor_size = spec.anchor_size
+        self.anchor_z = spec.anchor_z
+        self.anchor_rotations = spec.rotations
+        self.dir_offset = spec.dir_offset
+
+
+@pytest.mark.parametrize("H,W,k,ties", [(248, 216, 100, False), (32, 24, 100, True), (8, 6, 200, False)])
+def test_decode_topk_exact_index_set(pm, H, W, k, ties):
+    spec = pm.PointPillarsConfig(topk=k).anchor_spec()
+    rng = np.random.default_rng(H * W)
+    A = len(spec.rotations)
+    cls = rng.normal(size=(A, H, W)).astype(np.float32)
+    if ties:
+        cls = np.round(cls * 2) / 2  # many equal logits: ties resolve to the lower index
+    box = (0.1 * rng.normal(size=(7 * A, H, W))).astype(np.float32)
+    dr = rng.normal(size=(2 * A, H, W)).astype(np.float32)
+    out = pm.decode_topk(cls, box, dr, spec)
+    kk = min(k, A * H * W)
+    idx, logit, _, boxes, labels = O.decode_topk(cls, box, dr, _Geom(spec), kk)
+    got_idx = out["idx"][0].cpu().numpy()[:kk]
+    np.testing.assert_array_equal(got_idx, idx)
+    np.testing.assert_array_equal(out["logit"][0].cpu().numpy()[:kk], logit)
+    np.testing.assert_array_equal(out["dir"][0].cpu().numpy()[:kk], labels)
+    np.testing.assert_allclose(out["boxes"][0].cpu().numpy()[:kk], boxes, rtol=2e-6, atol=2e-6)
+    if kk < k:
+        assert (out["idx"][0].cpu().numpy()[kk:] == -1).all()
