@@ -113,10 +113,35 @@ def minmax(t) -> tuple[float, float]:
 # tensor ops: pm/tensor_ops.py (f32 NCHW, f32 accumulate)
 
 
+# Accumulation dtype of the dense kernels.  float32 is the reference (numpy sgemm);
+# float64 gives the re-association noise floor SURVEY §8(d) T2 asks to report.
+_ACC = {"dtype": np.float32}
+
+
+class accumulate_in:
+    """Context manager: run linear/conv2d/deconv2d products in another dtype, round to f32."""
+
+    def __init__(self, dtype):
+        self.dtype = dtype
+
+    def __enter__(self):
+        self.prev = _ACC["dtype"]
+        _ACC["dtype"] = self.dtype
+
+    def __exit__(self, *exc):
+        _ACC["dtype"] = self.prev
+
+
+def _mm(a, b):
+    if _ACC["dtype"] is np.float32:
+        return a @ b
+    return (a.astype(_ACC["dtype"]) @ b.astype(_ACC["dtype"])).astype(np.float32)
+
+
 def linear(x, weight, bias):
     """pm/tensor_ops.py:80-91."""
     x = np.asarray(x, dtype=np.float32)
-    return x @ weight.T + bias
+    return _mm(x, weight.T) + bias
 
 
 def out_size(in_hw, k_hw, stride, padding):
@@ -149,7 +174,7 @@ def conv2d(x, weight, bias, stride=(1, 1), padding=(0, 0)):
         raise ValueError(f"conv2d input channels {c} != weight channels {cw}")
     ho, wo = out_size((h, w), (kh, kw), stride, padding)
     cols = im2col(x, (kh, kw), stride, padding)
-    out = cols @ weight.reshape(f, -1).T + bias
+    out = _mm(cols, weight.reshape(f, -1).T) + bias
     return np.ascontiguousarray(out.reshape(n, ho, wo, f).transpose(0, 3, 1, 2))
 
 

@@ -144,6 +144,9 @@ class CompiledGraph:
         self.head_names: list[str] = []
         self.final_name: str | None = None
         self.graph_exec = None
+        for l in graph.weight_layers:  # first missing INT8 stats in chain order, like pm/model.py:261-268
+            if _prec(l) == "int8":
+                _fmt_of(l, stats)
         self._resolve_sources(in_shape, pcap, n_features, max_points_per_frame)
         self._shapes()
         self._needs()
