@@ -133,9 +133,12 @@ class accumulate_in:
 
 
 def _mm(a, b):
-    if _ACC["dtype"] is np.float32:
+    dt = _ACC["dtype"]
+    if dt is np.float32:
         return a @ b
-    return (a.astype(_ACC["dtype"]) @ b.astype(_ACC["dtype"])).astype(np.float32)
+    if isinstance(dt, str):  # "int" probe: non-INT8 layers accumulate in f64
+        dt = np.float64
+    return (a.astype(dt) @ b.astype(dt)).astype(np.float32)
 
 
 def linear(x, weight, bias):
@@ -472,8 +475,43 @@ def transform_weight(layer, stats):
     return layer.weight
 
 
+def _int8_layer_integer(layer, x, stats):
+    """Integer-execution probe of an INT8 layer (TensorRT-style: exact int32 accumulation of
+    codes, then y = f32(acc) * f32(s_x * s_w[c]) + bias in one rounding).  Used only inside
+    ``accumulate_in("int")`` to measure how far two valid executions of the same plan drift."""
+    act, ws, per_channel = _stat_scales(layer, stats)
+    cx = quantize(x, act).astype(np.float64)
+    w = np.asarray(layer.weight)
+    cw = (weight_codes_per_channel(w, ws) if per_channel else quantize(w, ws)).astype(np.float64)
+    cout = w.shape[0]
+    alpha = np.asarray(np.float32(act * np.broadcast_to(np.asarray(ws, np.float64), (cout,))), np.float64)
+    if layer.kind == "linear":
+        acc = cx @ cw.T
+        shape = (1,) * (acc.ndim - 1) + (-1,)
+    elif layer.kind == "conv2d":
+        n, c, h, wd = cx.shape
+        ho, wo = out_size((h, wd), w.shape[2:], layer.conv.stride, layer.conv.padding)
+        cols = im2col(cx, w.shape[2:], layer.conv.stride, layer.conv.padding)
+        acc = (cols @ cw.reshape(cout, -1).T).reshape(n, ho, wo, cout).transpose(0, 3, 1, 2)
+        shape = (1, -1, 1, 1)
+    else:
+        n, cin, h, wd = cx.shape
+        kh, kw = w.shape[2:]
+        rows = cx.transpose(0, 2, 3, 1).reshape(-1, cin)
+        acc = rows @ cw.transpose(0, 2, 3, 1).reshape(cout * kh * kw, cin).T
+        acc = acc.reshape(n, h, wd, cout, kh, kw).transpose(0, 3, 1, 4, 2, 5).reshape(n, cout, h * kh, wd * kw)
+        shape = (1, -1, 1, 1)
+    y = (acc * alpha.reshape(shape) + np.asarray(layer.bias, np.float64).reshape(shape)).astype(np.float32)
+    return np.ascontiguousarray(y)
+
+
 def run_weight_layer(layer, x, stats):
     """pm/model.py:271-307 (kernel dispatch extended with deconv2d)."""
+    if isinstance(_ACC["dtype"], str) and _ACC["dtype"] == "int" and _prec(layer) == "int8":
+        out = _int8_layer_integer(layer, x, stats)
+        if layer.bn is not None:
+            out = apply_bn(out, layer.bn, layer.kind)
+        return relu(out) if layer.relu else out
     x_used = transform_input(layer, x, stats)
     w_used = transform_weight(layer, stats)
     if layer.kind == "linear":

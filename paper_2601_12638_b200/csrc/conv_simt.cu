@@ -141,7 +141,7 @@ __global__ void __launch_bounds__(256) conv_simt_kernel(const ConvArgs a, const 
         pix = m;
       }
       float y;
-      if constexpr (DT == PMX_I8) y = __fadd_rn(__fmul_rn((float)acc[i][j], a.alpha[co]), a.bias[co]);
+      if constexpr (DT == PMX_I8) y = __fmaf_rn((float)acc[i][j], a.alpha[co], a.bias[co]);
       else y = __fadd_rn(acc[i][j], a.bias[co]);
       if (a.bn_post)
         y = __fadd_rn(__fmul_rn(__fsub_rn(y, a.bn_post[co]), a.bn_post[cout + co]), a.bn_post[2 * cout + co]);

@@ -67,6 +67,16 @@ __device__ __forceinline__ int quantize_exact(float x, double s, float inv) {
   return c < -128 ? -128 : (c > 127 ? 127 : c);
 }
 
+// Same result as quantize_exact with a short common path: away from ties
+// (|frac - .5| >= 1e-3) and inside |q| < 127 the f32 estimate is already exact and
+// needs no clamp; everything else (ties, saturation, NaN) takes the exact path.
+__device__ __forceinline__ int quantize_fast(float x, double s, float inv) {
+  const float q = __fmul_rn(x, inv);
+  const float r = rintf(q);
+  if (fabsf(__fsub_rn(q, r)) < 0.499f && fabsf(q) < 127.0f) return (int)r;
+  return quantize_exact(x, s, inv);
+}
+
 // fp16_roundtrip (pm/quant.py:144-147): saturate at +-65504, then RNE.
 __device__ __forceinline__ __half f16_sat(float x) {
   if (x != x) return __float2half_rn(x);

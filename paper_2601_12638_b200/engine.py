@@ -475,8 +475,13 @@ class CompiledGraph:
             self._op_pfn()
         elif self.input_value is not None:
             self._op_input()
+        fused = self._fusable_heads()
         for l in self.graph.layers:
             if l.name not in self.layer_src:
+                continue
+            if fused and l in fused:
+                if l is fused[-1]:
+                    self._op_heads_fused(fused)
                 continue
             if l.is_weight_layer:
                 self._op_conv(l)
@@ -484,6 +489,51 @@ class CompiledGraph:
                 self._op_upsample(l)
         if self.anchors is not None:
             self._op_decode()
+
+    def _fusable_heads(self):
+        """cls/box/dir heads -> one GEMM (N = 10A) writing the heads block, when they are
+        1x1 convs on the same tensor in the same input format (same precision and scale)."""
+        if self.anchors is None:
+            return None
+        a = self.anchors
+        by_name = {l.name: l for l in self.graph.layers}
+        hs = [by_name[n] for n in (a.cls_head, a.box_head, a.dir_head)]
+        src = {tuple(self.layer_src[h.name]) for h in hs}
+        fmts = {_fmt_of(h, self.stats) for h in hs}
+        ok = (len(src) == 1 and len(fmts) == 1 and all(
+            h.kind == "conv2d" and h.weight.shape[2:] == (1, 1) and tuple(h.conv.stride) == (1, 1)
+            and tuple(h.conv.padding) == (0, 0) and h.bn is None and not h.relu for h in hs))
+        if not ok:
+            return None
+        order = sorted(hs, key=lambda h: self.graph.layers.index(h))
+        self._fused_order = hs  # channel order of the heads block: cls, box, dir
+        return order
+
+    def _op_heads_fused(self, order):
+        torch = self.torch
+        lib = self.lib
+        hs = self._fused_order
+        recs = [self.weights[h.name] for h in hs]
+        w = torch.cat([r["w"] for r in recs], dim=0).contiguous()
+        bias = torch.cat([r["bias"] for r in recs]).contiguous()
+        alpha = torch.cat([r["alpha"] for r in recs]).contiguous() if recs[0]["alpha"] is not None else None
+        self._keep += [w, bias, alpha]
+        src, t, cs, off = self._src_buf(hs[0])
+        B, H, W, C = src.shape
+        ctot = self.head_ctot
+        d = N.ConvDesc(kind=N.PMX_CONV2D, in_dtype=_DT[recs[0]["precision"]], batch=B, in_h=H, in_w=W, in_c=C,
+                       in_c_stride=cs, in_c_offset=off, out_c=ctot, k_h=1, k_w=1, stride_h=1, stride_w=1, pad_h=0,
+                       pad_w=0, out_h=H, out_w=W, relu=0)
+        self._keep.append(d)
+        arr, n = N.outs_array([N.Out(ptr=self.heads_cat.data_ptr(), scale=0.0, dtype=N.PMX_F32, c_stride=ctot,
+                                     c_offset=0)])
+        self._keep.append(arr)
+        esz = {"fp32": 4, "fp16": 2, "int8": 1}[recs[0]["precision"]]
+        self.op_info["conv heads(fused)"] = {"flops": 2.0 * B * H * W * ctot * C, "precision": recs[0]["precision"],
+                                              "bytes": B * H * W * C * esz + ctot * C * esz + B * H * W * ctot * 4}
+        self.ops.append(("conv heads(fused)", lambda s: N.check(lib.pmx_conv(
+            ctypes.byref(d), t.data_ptr(), w.data_ptr(), N.ptr(alpha), bias.data_ptr(), None, arr, n, None, None, 0,
+            s), "fused heads")))
 
     def _op_input(self):
         v = self.input_value

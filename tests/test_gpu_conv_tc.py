@@ -1,0 +1,99 @@
+"""tcgen05 implicit-GEMM kernel vs the SIMT kernel on every PointPillars layer class.
+
+INT8: the int32 accumulators are exact in both kernels and the epilogue formula is
+identical, so every output format (int8 codes, f16, f32) must match BIT FOR BIT.
+FP16: f16 x f16 products are exact; only the f32 summation order differs (<= 1e-5 rel).
+Also checks the kernel is really the tcgen05 one (pmx_conv_backend)."""
+
+import ctypes
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+CASES = [  # kind, cin, cout, k, stride, (h, w), batch
+    ("conv", 64, 64, 3, 2, (40, 36), 2),     # blocks.0.0 (s2, Cin 64 int8 -> SW64)
+    ("conv", 64, 64, 3, 1, (20, 18), 1),     # blocks.0.x
+    ("conv", 64, 128, 3, 2, (20, 18), 1),    # blocks.1.0
+    ("conv", 128, 128, 3, 1, (21, 13), 2),   # blocks.1.x (ragged tiles)
+    ("conv", 128, 256, 3, 2, (12, 10), 1),   # blocks.2.0
+    ("conv", 256, 256, 3, 1, (7, 9), 1),     # blocks.2.x
+    ("deconv", 64, 128, 1, 1, (9, 7), 1),    # deblocks.0
+    ("deconv", 128, 128, 2, 2, (6, 5), 2),   # deblocks.1
+    ("deconv", 256, 128, 4, 4, (3, 4), 1),   # deblocks.2
+    ("conv", 384, 4, 1, 1, (11, 13), 1),     # conv_dir_cls
+    ("conv", 384, 14, 1, 1, (11, 13), 1),    # conv_reg
+    ("conv", 384, 2, 1, 1, (11, 13), 1),     # conv_cls
+    ("conv", 384, 20, 1, 1, (248, 216), 1),  # fused heads, full size
+    ("conv", 64, 64, 3, 2, (496, 432), 1),   # blocks.0.0 full size
+]
+
+
+def _run(lib, N, torch, desc, x, w, alpha, bias, outs_spec, mode):
+    outs = []
+    bufs = []
+    for dt, scale in outs_spec:
+        t = torch.zeros((desc.batch, desc.out_h, desc.out_w, desc.out_c),
+                        dtype={N.PMX_F32: torch.float32, N.PMX_F16: torch.float16, N.PMX_I8: torch.int8}[dt],
+                        device="cuda")
+        bufs.append(t)
+        outs.append(N.Out(ptr=t.data_ptr(), scale=scale, dtype=dt, c_stride=desc.out_c, c_offset=0))
+    arr, n = N.outs_array(outs)
+    lib.pmx_set_conv_backend(mode)
+    keys = torch.empty(2, dtype=torch.int32, device="cuda")
+    N.check(lib.pmx_minmax_init(keys.data_ptr(), 1, N.stream_ptr()))
+    try:
+        N.check(lib.pmx_conv(ctypes.byref(desc), x.data_ptr(), w.data_ptr(), None if alpha is None else alpha.data_ptr(),
+                             bias.data_ptr(), None, arr, n, keys.data_ptr(), None, 0, N.stream_ptr()), "conv")
+        torch.cuda.synchronize()
+    finally:
+        lib.pmx_set_conv_backend(0)
+    return bufs, N.decode_keys(keys.cpu().numpy().view(np.uint32))
+
+
+@pytest.mark.parametrize("case", CASES, ids=lambda c: f"{c[0]}{c[1]}x{c[2]}k{c[3]}s{c[4]}_{c[5][0]}x{c[5][1]}")
+@pytest.mark.parametrize("prec", ["int8", "fp16"])
+def test_tcgen05_matches_simt(case, prec):
+    import torch
+
+    from paper_2601_12638_b200 import _native as N
+
+    lib = N.load()
+    kind, cin, cout, k, s, (h, w), batch = case
+    rng = np.random.default_rng(cin * 7 + cout + k + s + h)
+    deconv = kind == "deconv"
+    if deconv:
+        oh, ow = h * s, w * s
+        ngemm = k * k * cout
+        wshape = (ngemm, cin)
+    else:
+        pad = 1 if k == 3 else 0
+        oh, ow = (h + 2 * pad - k) // s + 1, (w + 2 * pad - k) // s + 1
+        wshape = (cout, k * k * cin)
+    desc = N.ConvDesc(kind=N.PMX_DECONV2D if deconv else N.PMX_CONV2D, in_dtype=N.DTYPE_CODE[prec], batch=batch,
+                      in_h=h, in_w=w, in_c=cin, in_c_stride=cin, in_c_offset=0, out_c=cout, k_h=k, k_w=k,
+                      stride_h=s, stride_w=s, pad_h=0 if deconv or k == 1 else 1, pad_w=0 if deconv or k == 1 else 1,
+                      out_h=oh, out_w=ow, relu=1)
+    if prec == "int8":
+        x = torch.from_numpy(rng.integers(-128, 128, size=(batch, h, w, cin), dtype=np.int8)).cuda()
+        wt = torch.from_numpy(rng.integers(-128, 128, size=wshape, dtype=np.int8)).cuda()
+        alpha = torch.from_numpy((rng.uniform(0.5, 2.0, cout) * 1e-4).astype(np.float32)).cuda()
+    else:
+        x = torch.from_numpy(rng.normal(size=(batch, h, w, cin)).astype(np.float16)).cuda()
+        wt = torch.from_numpy((rng.normal(size=wshape) / np.sqrt(wshape[1])).astype(np.float16)).cuda()
+        alpha = None
+    bias = torch.from_numpy(rng.normal(scale=0.1, size=cout).astype(np.float32)).cuda()
+    spec = [(N.PMX_F32, 0.0), (N.PMX_I8, 0.013), (N.PMX_F16, 0.0)]
+    assert lib.pmx_conv_backend(desc.in_dtype, desc.kind).decode() == "tcgen05"
+    tc, ktc = _run(lib, N, torch, desc, x, wt, alpha, bias, spec, 0)
+    ref, kref = _run(lib, N, torch, desc, x, wt, alpha, bias, spec, 1)
+    if prec == "int8":
+        for a, b in zip(tc, ref):
+            assert torch.equal(a, b), (a.float() - b.float()).abs().max()
+        np.testing.assert_array_equal(ktc, kref)
+    else:
+        a, b = tc[0].double(), ref[0].double()
+        assert float((a - b).norm() / b.norm()) <= 1e-5
+        codes = (tc[1].int() - ref[1].int()).abs()
+        assert int(codes.max()) <= 1 and float((codes != 0).float().mean()) < 1e-3

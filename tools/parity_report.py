@@ -51,6 +51,8 @@ def main():
         want = O.forward(og, sample, stats=stats, observe_fn=lambda l, x: seen_o.__setitem__(l.index, x))
         with O.accumulate_in(np.float64):
             want64 = O.forward(og, sample, stats=stats)
+        with O.accumulate_in("int"):
+            wantint = O.forward(og, sample, stats=stats)
         got = pm.forward(planned, psample, stats=stats, observe_fn=lambda l, x: seen_e.__setitem__(l.index, x))
         flips = {}
         for l in planned.weight_layers:
@@ -63,6 +65,8 @@ def main():
             "engine_vs_ref": {h: rel(g, w) for h, g, w in zip(pm.pointpillars.HEADS, got, want)},
             "ref_f32_vs_f64": {h: rel(w, w64) for h, w, w64 in zip(pm.pointpillars.HEADS, want, want64)},
             "engine_vs_f64": {h: rel(g, w64) for h, g, w64 in zip(pm.pointpillars.HEADS, got, want64)},
+            "ref_f32_vs_int": {h: rel(w, wi) for h, w, wi in zip(pm.pointpillars.HEADS, want, wantint)},
+            "engine_vs_int": {h: rel(g, wi) for h, g, wi in zip(pm.pointpillars.HEADS, got, wantint)},
             "int8_input_flip_rate": flips,
         }
     print(json.dumps(report, indent=1))
