@@ -218,8 +218,12 @@ pmx_status pmx_conv(const pmx_conv_desc* desc, const void* x, const void* w, con
                     const float* bias, const float* bn_post, const pmx_out* outs, int32_t n_outs,
                     uint32_t* out_keys, void* ws, size_t ws_bytes, pmx_stream_t stream);
 
-/* Force a backend for testing: 0 = automatic, 1 = SIMT reference kernel only. */
+/* Force a backend for testing: 0 = automatic, 1 = SIMT reference kernel only,
+ * 2 = tcgen05 without the halo variant. */
 void pmx_set_conv_backend(int32_t mode);
+/* Debug: when non-NULL, tcgen05 conv launches record per-role clock64 stamps of
+ * CTA 0 into buf[8][64] (producer/MMA/epilogue hand-offs). */
+void pmx_debug_trace(unsigned long long* buf);
 
 /* Stage an f32 [pixels, c] tensor into every consumer format (the precision
  * transform of pm/model.py:273-285 applied to a graph input), optionally

@@ -25,6 +25,7 @@
 namespace pmx {
 
 extern int g_conv_backend_mode;
+unsigned long long* g_trace = nullptr;  // pmx_debug_trace
 
 namespace {
 
@@ -76,6 +77,15 @@ __device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap* map
       : "memory");
 }
 
+__device__ __forceinline__ void tma_load_5d(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
+                                            int c4, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, %6}], "
+      "[%7];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(bar)
+      : "memory");
+}
+
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
@@ -109,11 +119,13 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-// K-major smem operand descriptor (tcgen05 format: version 1 at bit 46, layout at 61)
-__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t sbo, uint32_t layout) {
+// K-major smem operand descriptor (tcgen05 format: version 1 at bit 46, layout at 61).
+// LBO = byte stride between K-adjacent 8x16B core matrices (no-swizzle layouts only),
+// SBO = byte stride between M/N-adjacent 8-row core-matrix groups.
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t sbo, uint32_t layout, uint32_t lbo = 16) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr & 0x3FFFFu) >> 4);
-  d |= (uint64_t)1u << 16;  // LBO (unused for swizzled K-major)
+  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
   d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
   d |= (uint64_t)1u << 46;
   d |= (uint64_t)layout << 61;
@@ -122,7 +134,13 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t sbo, uint32_t
 
 // ------------------------------------------------------------------ kernel
 
-enum : int { MODE_CONV3 = 0, MODE_GEMM = 1 };  // GEMM = 1x1 conv / deconv over flattened pixels
+// CONV3: 3x3 conv, one shifted input box per tap (implicit im2col by TMA coordinates)
+// GEMM : 1x1 conv / deconv over flattened pixels
+// HALO : stride-1 3x3 conv whose 128-pixel tile (16 rows x 8 cols) is fed from ONE
+//        (18 x 10)-pixel halo box per tile stored as un-swizzled 8x16B core matrices,
+//        so each tap's A operand is just a descriptor offset (9x less L2 traffic);
+//        the weights stay resident in smem for the whole persistent kernel
+enum : int { MODE_CONV3 = 0, MODE_GEMM = 1, MODE_HALO = 2 };
 
 struct TcParams {
   // geometry
@@ -132,6 +150,8 @@ struct TcParams {
   int tw, th;      // conv output tile (tw * th = 128)
   int tiles_x, tiles_y;
   int m_tiles, n_tiles;  // tile grid (tile t -> m = t / n_tiles, n = t % n_tiles)
+  int oc_shift;          // log2(out_c) when a power of two, else -1 (deconv tap split)
+  int st_shift;          // log2(stride) (deconv stride is a power of two)
   int64_t m_total;  // GEMM mode: number of rows (input pixels)
   int n_gemm;       // GEMM N (deconv: k*k*Cout)
   int kc;           // channels per K-block
@@ -143,12 +163,24 @@ struct TcParams {
   uint32_t sbo, layout;       // smem descriptor params (same for A and B)
   uint32_t idesc;
   uint32_t tmem_cols;
+  // HALO mode
+  uint32_t halo_tx;     // halo bytes per tile (TMA transaction size)
+  uint32_t hp, hw;      // halo pixels, halo row width (pixels)
+  uint32_t cin_bytes;   // bytes of channels per pixel
+  uint32_t bblk_bytes;  // resident weight block (one tap, one channel block)
+  uint32_t bres_bytes;  // all resident weights
   int relu;
   const float* alpha;
   const float* bias;
   const float* bn_post;
   uint32_t* keys;
+  unsigned long long* trace;  // debug: per-role clock64 stamps of CTA 0 (pmx_debug_trace)
 };
+
+#define PMX_TRACE(ev, idx)                                                              \
+  do {                                                                                  \
+    if (p.trace && blockIdx.x == 0 && (idx) < 64) p.trace[(ev) * 64 + (idx)] = clock64(); \
+  } while (0)
 
 struct TcMaps {
   CUtensorMap a[4];  // conv: [parity] maps (stride 2) or a[0]; GEMM: a[0] 2D
@@ -163,16 +195,20 @@ constexpr int kThreads = 32 * (2 + kEpiWarps);  // + TMA producer warp + MMA war
 // two's-complement code; one predicate per 16 values sends near-ties (|frac-.5|
 // < 1e-3), |q| >= 127 and NaN to the exact f64 path (quantize_exact).
 __device__ __forceinline__ uint4 quant16(const float (&y)[16], double s, float inv) {
-  const float M = 12582912.0f;
+  // packed f32x2 arithmetic (sm_100): q = y*inv, t = q + M, d = q - (t - M)
+  const float2 M2 = make_float2(12582912.0f, 12582912.0f), I2 = make_float2(inv, inv);
+  const float2 NEG1 = make_float2(-1.0f, -1.0f);
   uint32_t tb[16];
   bool good = true;
 #pragma unroll
-  for (int j = 0; j < 16; ++j) {
-    const float qv = __fmul_rn(y[j], inv);
-    const float t = __fadd_rn(qv, M);
-    const float d = __fsub_rn(qv, __fsub_rn(t, M));
-    good = good && (fabsf(d) < 0.499f) && (fabsf(qv) < 127.0f);
-    tb[j] = __float_as_uint(t);
+  for (int j = 0; j < 16; j += 2) {
+    const float2 qv = __fmul2_rn(make_float2(y[j], y[j + 1]), I2);
+    const float2 t = __fadd2_rn(qv, M2);
+    const float2 d = __fadd2_rn(qv, __ffma2_rn(t, NEG1, M2));  // q + (M - t), both exact
+    good = good && (fabsf(d.x) < 0.499f) && (fabsf(d.y) < 0.499f) && (fabsf(qv.x) < 127.0f) &&
+           (fabsf(qv.y) < 127.0f);
+    tb[j] = __float_as_uint(t.x);
+    tb[j + 1] = __float_as_uint(t.y);
   }
   if (!good) {
 #pragma unroll
@@ -198,7 +234,7 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
 // Persistent: grid = min(tiles, SMs); every role walks the same static tile sequence.
 // Accumulators are double-buffered in TMEM so the epilogue of tile i overlaps the
 // TMA + MMA of tile i+1; the smem ring runs across tile boundaries.
-template <int DT>
+template <int DT, int OUTK, int KCB, int CINB>
 __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_constant__ TcMaps maps, const TcParams p,
                                                               const Outs outs) {
   extern __shared__ uint8_t smem_raw[];
@@ -207,8 +243,10 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
   uint8_t* gbase = smem_raw + (base - raw);
   const uint32_t a_smem = base;
   const uint32_t b_smem = base + p.stages * p.a_bytes;
-  const uint32_t bar_base = b_smem + p.stages * p.b_bytes;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + (bar_base - base) + 8 * (2 * p.stages + 4));
+  const uint32_t bres = b_smem + p.stages * p.b_bytes;  // HALO: resident weights (1024-aligned)
+  const uint32_t bar_base = bres + p.bres_bytes;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + (bar_base - base) + 8 * (2 * p.stages + 5));
+  const uint32_t bfull = bar_base + 8u * (2 * p.stages + 4);
   auto full = [&](int s) { return bar_base + 8u * s; };
   auto empty = [&](int s) { return bar_base + 8u * (p.stages + s); };
   auto tfull = [&](int a) { return bar_base + 8u * (2 * p.stages + a); };
@@ -227,6 +265,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
       mbar_init(tfull(a), 1);
       mbar_init(tempty(a), kEpiWarps);
     }
+    mbar_init(bfull, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -244,7 +283,27 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
     if (lane == 0) {
       // ---------------- TMA producer
       uint32_t it = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      if (p.mode == MODE_HALO) {
+        mbar_expect_tx(bfull, p.bres_bytes);
+        for (int kb = 0; kb < nk; ++kb) {
+          const int tap = kb / p.cblocks, cb = kb % p.cblocks;
+          tma_load_2d(bres + kb * p.bblk_bytes, &maps.b, tap * (p.cblocks * p.kc) + cb * p.kc, 0, bfull);
+        }
+        for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
+          int r = t;
+          const int tx = r % p.tiles_x;
+          r /= p.tiles_x;
+          const int oy0 = (r % p.tiles_y) * p.th, tb = r / p.tiles_y, ox0 = tx * p.tw;
+          const int s = it % p.stages;
+          const uint32_t ph = (it / p.stages) & 1;
+          PMX_TRACE(0, it);
+          mbar_wait(empty(s), ph ^ 1);
+          mbar_expect_tx(full(s), p.halo_tx);
+          tma_load_5d(a_smem + s * p.a_bytes, &maps.a[0], 0, ox0 - 1, oy0 - 1, 0, tb, full(s));
+          PMX_TRACE(1, it);
+        }
+      }
+      for (int t = blockIdx.x; t < total && p.mode != MODE_HALO; t += gridDim.x) {
         const int mt = t / p.n_tiles, nt = t % p.n_tiles;
         const int n0 = nt * p.bn;
         int tb = 0, oy0 = 0, ox0 = 0, m0 = 0;
@@ -285,28 +344,71 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
     __syncwarp();
   } else if (warp == 1) {
     if (lane == 0) {
-      // ---------------- MMA issuer
-      const int ksteps = (p.kc * (DT == PMX_I8 ? 1 : 2)) / 32;  // 32 bytes of K per instruction
+      // ---------------- MMA issuer (descriptor high words hoisted; only the start
+      // address changes per instruction -- the issue path is ~50 cycles/MMA)
+      constexpr int ksteps = KCB / 32;  // 32 bytes of K per instruction
+      const uint32_t idesc = p.idesc;
+      const uint32_t bn = (uint32_t)p.bn;
+      const uint64_t dsw = sdesc(0, p.sbo, p.layout);  // swizzled operands (address field 0)
       uint32_t it = 0, i = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x, ++i) {
-        const uint32_t acc = i & 1, aph = (i >> 1) & 1;
-        mbar_wait(tempty(acc), aph ^ 1);
+      if constexpr (CINB > 0) {
+        constexpr int HW = 10, HP = 180, CB = CINB / KCB;
+        const uint64_t dhalo = sdesc(0, HW * 16u, 0u, HP * 16u);
+        const uint32_t bblk = p.bblk_bytes;
+        mbar_wait(bfull, 0);
         tc_fence_after();
-        const uint32_t d = tmem + acc * (uint32_t)p.bn;
-        for (int kb = 0; kb < nk; ++kb, ++it) {
-          const int s = it % p.stages;
-          const uint32_t ph = (it / p.stages) & 1;
-          mbar_wait(full(s), ph);
+        for (int t = blockIdx.x; t < total; t += gridDim.x, ++i, ++it) {
+          const uint32_t acc = i & 1, aph = (i >> 1) & 1;
+          mbar_wait(tempty(acc), aph ^ 1);
           tc_fence_after();
-          const uint32_t abase = a_smem + s * p.a_bytes, bbase = b_smem + s * p.b_bytes;
-          for (int k = 0; k < ksteps; ++k) {
-            const uint64_t ad = sdesc(abase + 32u * k, p.sbo, p.layout);
-            const uint64_t bd = sdesc(bbase + 32u * k, p.sbo, p.layout);
-            tc_mma<DT>(d, ad, bd, p.idesc, (kb | k) != 0);
+          const uint32_t d = tmem + acc * bn;
+          const int s = it % p.stages;
+          PMX_TRACE(2, i);
+          mbar_wait(full(s), (it / p.stages) & 1);
+          tc_fence_after();
+          PMX_TRACE(3, i);
+          const uint32_t abase = a_smem + s * p.a_bytes;
+#pragma unroll
+          for (int tap = 0; tap < 9; ++tap) {
+#pragma unroll
+            for (int k = 0; k < CINB / 32; ++k) {
+              // two 16-byte channel groups per instruction (core matrices at +LBO)
+              const uint32_t aoff = (uint32_t)(((2 * k) * HP + (tap / 3) * HW + (tap % 3)) * 16);
+              const uint32_t boff = (uint32_t)((tap * CB + (k * 32) / KCB)) * bblk + (uint32_t)((k * 32) % KCB);
+              const uint64_t ad = dhalo | (uint64_t)(((abase + aoff) & 0x3FFFFu) >> 4);
+              const uint64_t bd = dsw | (uint64_t)(((bres + boff) & 0x3FFFFu) >> 4);
+              tc_mma<DT>(d, ad, bd, idesc, (tap | k) != 0);
+            }
           }
           tc_commit(empty(s));
+          tc_commit(tfull(acc));
+          PMX_TRACE(4, i);
         }
-        tc_commit(tfull(acc));
+      } else {
+        for (int t = blockIdx.x; t < total; t += gridDim.x, ++i) {
+          const uint32_t acc = i & 1, aph = (i >> 1) & 1;
+          mbar_wait(tempty(acc), aph ^ 1);
+          tc_fence_after();
+          const uint32_t d = tmem + acc * bn;
+          PMX_TRACE(2, i);
+          for (int kb = 0; kb < nk; ++kb, ++it) {
+            const int s = it % p.stages;
+            const uint32_t ph = (it / p.stages) & 1;
+            mbar_wait(full(s), ph);
+            tc_fence_after();
+            if (kb == 0) PMX_TRACE(3, i);
+            const uint32_t abase = a_smem + s * p.a_bytes, bbase = b_smem + s * p.b_bytes;
+#pragma unroll
+            for (int k = 0; k < ksteps; ++k) {
+              const uint64_t ad = dsw | (uint64_t)(((abase + 32u * k) & 0x3FFFFu) >> 4);
+              const uint64_t bd = dsw | (uint64_t)(((bbase + 32u * k) & 0x3FFFFu) >> 4);
+              tc_mma<DT>(d, ad, bd, idesc, (kb | k) != 0);
+            }
+            tc_commit(empty(s));
+          }
+          tc_commit(tfull(acc));
+          PMX_TRACE(4, i);
+        }
       }
     }
     __syncwarp();
@@ -324,29 +426,31 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
       const int mt = t / p.n_tiles, nt = t % p.n_tiles;
       const int n0 = nt * p.bn;
       bool valid;
-      int64_t pix_in;
-      int iy = 0, ix = 0, ib = 0;
-      if (p.mode == MODE_CONV3) {
-        int r = mt;
-        const int tx = r % p.tiles_x;
-        r /= p.tiles_x;
-        const int oy = (r % p.tiles_y) * p.th + row / p.tw;
-        const int tb = r / p.tiles_y;
-        const int ox = tx * p.tw + row % p.tw;
-        valid = oy < p.out_h && ox < p.out_w;
-        pix_in = ((int64_t)tb * p.out_h + oy) * p.out_w + ox;
+      uint32_t pix_in;  // < 2^31 (checked on the host)
+      uint32_t iy = 0, ix = 0, ib = 0;
+      if (p.mode != MODE_GEMM) {
+        uint32_t r = (uint32_t)mt;
+        const uint32_t tx = r % (uint32_t)p.tiles_x;
+        r /= (uint32_t)p.tiles_x;
+        const uint32_t oy = (r % (uint32_t)p.tiles_y) * p.th + row / p.tw;
+        const uint32_t tb = r / (uint32_t)p.tiles_y;
+        const uint32_t ox = tx * p.tw + row % p.tw;
+        valid = oy < (uint32_t)p.out_h && ox < (uint32_t)p.out_w;
+        pix_in = (tb * p.out_h + oy) * p.out_w + ox;
       } else {
-        pix_in = (int64_t)mt * 128 + row;
-        valid = pix_in < p.m_total;
+        pix_in = (uint32_t)mt * 128u + row;
+        valid = pix_in < (uint32_t)p.m_total;
         if (p.deconv) {
-          ix = (int)(pix_in % p.in_w);
-          const int64_t tt = pix_in / p.in_w;
-          iy = (int)(tt % p.in_h);
-          ib = (int)(tt / p.in_h);
+          ix = pix_in % (uint32_t)p.in_w;
+          const uint32_t tt = pix_in / (uint32_t)p.in_w;
+          iy = tt % (uint32_t)p.in_h;
+          ib = tt / (uint32_t)p.in_h;
         }
       }
+      if (warp == 2 && lane == 0) PMX_TRACE(5, i);
       mbar_wait(tfull(acc), aph);
       tc_fence_after();
+      if (warp == 2 && lane == 0) PMX_TRACE(6, i);
       const uint32_t trow = tmem + acc * (uint32_t)p.bn + ((uint32_t)(q * 32) << 16);
       for (int c = g; c < nchunks; c += 4) {
         uint32_t v[16];
@@ -354,13 +458,19 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
         const int nbase = n0 + 16 * c;
         if (!valid || nbase >= p.n_gemm) continue;
         // deconv: 16 consecutive GEMM columns share one tap (Cout % 16 == 0)
-        int64_t pix = pix_in;
+        uint32_t pix = pix_in;
         int cobase = nbase;
         if (p.deconv) {
-          const int tap = nbase / p.out_c;
-          cobase = nbase % p.out_c;
-          const int ddy = tap / p.stride, ddx = tap % p.stride;
-          pix = ((int64_t)ib * p.out_h + (int64_t)iy * p.stride + ddy) * p.out_w + (int64_t)ix * p.stride + ddx;
+          int tap;
+          if (p.oc_shift >= 0) {
+            tap = nbase >> p.oc_shift;
+            cobase = nbase & (p.out_c - 1);
+          } else {
+            tap = nbase / p.out_c;
+            cobase = nbase - tap * p.out_c;
+          }
+          const uint32_t ddy = (uint32_t)tap >> p.st_shift, ddx = (uint32_t)tap & (uint32_t)(p.stride - 1);
+          pix = (ib * p.out_h + iy * p.stride + ddy) * p.out_w + ix * p.stride + ddx;
         }
         const bool full16 = (nbase + 16) <= p.n_gemm;
         float y[16];
@@ -368,18 +478,23 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
 #pragma unroll
           for (int j4 = 0; j4 < 4; ++j4) {
             const float4 b4 = __ldg(reinterpret_cast<const float4*>(p.bias + cobase) + j4);
+            float2 r0, r1;
             if constexpr (DT == PMX_I8) {
               const float4 a4 = __ldg(reinterpret_cast<const float4*>(p.alpha + cobase) + j4);
-              y[4 * j4 + 0] = __fmaf_rn((float)(int)v[4 * j4 + 0], a4.x, b4.x);
-              y[4 * j4 + 1] = __fmaf_rn((float)(int)v[4 * j4 + 1], a4.y, b4.y);
-              y[4 * j4 + 2] = __fmaf_rn((float)(int)v[4 * j4 + 2], a4.z, b4.z);
-              y[4 * j4 + 3] = __fmaf_rn((float)(int)v[4 * j4 + 3], a4.w, b4.w);
+              r0 = __ffma2_rn(make_float2((float)(int)v[4 * j4], (float)(int)v[4 * j4 + 1]), make_float2(a4.x, a4.y),
+                              make_float2(b4.x, b4.y));
+              r1 = __ffma2_rn(make_float2((float)(int)v[4 * j4 + 2], (float)(int)v[4 * j4 + 3]),
+                              make_float2(a4.z, a4.w), make_float2(b4.z, b4.w));
             } else {
-              y[4 * j4 + 0] = __fadd_rn(__uint_as_float(v[4 * j4 + 0]), b4.x);
-              y[4 * j4 + 1] = __fadd_rn(__uint_as_float(v[4 * j4 + 1]), b4.y);
-              y[4 * j4 + 2] = __fadd_rn(__uint_as_float(v[4 * j4 + 2]), b4.z);
-              y[4 * j4 + 3] = __fadd_rn(__uint_as_float(v[4 * j4 + 3]), b4.w);
+              r0 = __fadd2_rn(make_float2(__uint_as_float(v[4 * j4]), __uint_as_float(v[4 * j4 + 1])),
+                              make_float2(b4.x, b4.y));
+              r1 = __fadd2_rn(make_float2(__uint_as_float(v[4 * j4 + 2]), __uint_as_float(v[4 * j4 + 3])),
+                              make_float2(b4.z, b4.w));
             }
+            y[4 * j4] = r0.x;
+            y[4 * j4 + 1] = r0.y;
+            y[4 * j4 + 2] = r1.x;
+            y[4 * j4 + 3] = r1.y;
           }
         } else {
 #pragma unroll
@@ -413,26 +528,39 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
               hi = nmax(hi, y[j]);
             }
         }
-#pragma unroll
-        for (int o = 0; o < PMX_MAX_OUTS; ++o) {
-          if (o >= outs.n) break;
-          const OutDev& od = outs.o[o];
-          const int64_t off = pix * od.c_stride + od.c_offset + cobase;
-          if (full16 && od.dtype == PMX_I8 && (off & 15) == 0) {
-            *reinterpret_cast<uint4*>(reinterpret_cast<int8_t*>(od.ptr) + off) = quant16(y, od.scale, od.inv);
-          } else if (full16 && od.dtype == PMX_F16 && (off & 7) == 0) {
-            uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__half*>(od.ptr) + off);
-            dst[0] = make_uint4(f16x2_sat(y[0], y[1]), f16x2_sat(y[2], y[3]), f16x2_sat(y[4], y[5]),
-                                f16x2_sat(y[6], y[7]));
-            dst[1] = make_uint4(f16x2_sat(y[8], y[9]), f16x2_sat(y[10], y[11]), f16x2_sat(y[12], y[13]),
-                                f16x2_sat(y[14], y[15]));
-          } else if (full16 && od.dtype == PMX_F32 && (off & 3) == 0) {
-            float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(od.ptr) + off);
-#pragma unroll
-            for (int qq = 0; qq < 4; ++qq) dst[qq] = make_float4(y[4 * qq], y[4 * qq + 1], y[4 * qq + 2], y[4 * qq + 3]);
+        if constexpr (OUTK == 1) {
+          // single int8 consumer, 16-byte aligned rows (checked on the host)
+          const OutDev& od = outs.o[0];
+          if (full16) {
+            *reinterpret_cast<uint4*>(reinterpret_cast<int8_t*>(od.ptr) + (size_t)pix * od.c_stride + od.c_offset +
+                                      cobase) = quant16(y, od.scale, od.inv);
           } else {
             for (int j = 0; j < 16; ++j)
               if (nbase + j < p.n_gemm) store_one(od, pix, cobase + j, y[j]);
+          }
+        } else {
+#pragma unroll
+          for (int o = 0; o < PMX_MAX_OUTS; ++o) {
+            if (o >= outs.n) break;
+            const OutDev& od = outs.o[o];
+            const int64_t off = (int64_t)pix * od.c_stride + od.c_offset + cobase;
+            if (full16 && od.dtype == PMX_I8 && (off & 15) == 0) {
+              *reinterpret_cast<uint4*>(reinterpret_cast<int8_t*>(od.ptr) + off) = quant16(y, od.scale, od.inv);
+            } else if (full16 && od.dtype == PMX_F16 && (off & 7) == 0) {
+              uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__half*>(od.ptr) + off);
+              dst[0] = make_uint4(f16x2_sat(y[0], y[1]), f16x2_sat(y[2], y[3]), f16x2_sat(y[4], y[5]),
+                                  f16x2_sat(y[6], y[7]));
+              dst[1] = make_uint4(f16x2_sat(y[8], y[9]), f16x2_sat(y[10], y[11]), f16x2_sat(y[12], y[13]),
+                                  f16x2_sat(y[14], y[15]));
+            } else if (full16 && od.dtype == PMX_F32 && (off & 3) == 0) {
+              float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(od.ptr) + off);
+#pragma unroll
+              for (int qq = 0; qq < 4; ++qq)
+                dst[qq] = make_float4(y[4 * qq], y[4 * qq + 1], y[4 * qq + 2], y[4 * qq + 3]);
+            } else {
+              for (int j = 0; j < 16; ++j)
+                if (nbase + j < p.n_gemm) store_one(od, pix, cobase + j, y[j]);
+            }
           }
         }
       }
@@ -440,6 +568,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(tempty(acc));
+      if (warp == 2 && lane == 0) PMX_TRACE(7, i);
     }
     if (p.keys) block_minmax_commit<kThreads>(lo, hi, p.keys);
   }
@@ -537,7 +666,14 @@ Plan plan_for(const pmx_conv_desc& d) {
     if (p.deconv && (d.out_c % 16 != 0)) return pl;
     p.m_total = (int64_t)d.batch * d.in_h * d.in_w;
     p.m_tiles = (int)ceil_div(p.m_total, 128);
+    if (p.deconv && (p.stride & (p.stride - 1))) return pl;  // stride must be a power of two
   }
+  // the epilogue indexes pixels in 32 bits
+  if ((int64_t)d.batch * d.out_h * d.out_w >= (int64_t)1 << 31 ||
+      (int64_t)d.batch * d.in_h * d.in_w >= (int64_t)1 << 31)
+    return pl;
+  p.oc_shift = (d.out_c & (d.out_c - 1)) == 0 ? __builtin_ctz((unsigned)d.out_c) : -1;
+  p.st_shift = __builtin_ctz((unsigned)(p.stride > 0 ? p.stride : 1));
   // N tile: the whole GEMM N up to 256 (the A tile is then read once); TMEM holds two
   int bn = (int)(ceil_div(p.n_gemm, 16) * 16);
   if (bn > 256) bn = 256;
@@ -553,6 +689,35 @@ Plan plan_for(const pmx_conv_desc& d) {
   if (stages > 12) stages = 12;
   if (stages < 2) stages = 2;
   p.stages = stages;
+  p.bres_bytes = 0;
+  if (conv3 && p.stride == 1 && g_conv_backend_mode != 2 && cin_bytes == kc_bytes && p.n_tiles == 1 &&
+      d.out_w >= 8) {
+    const uint32_t hw = 10, hh = 18, hp = hw * hh;  // (16 + 2) x (8 + 2) halo of a 16 x 8 tile
+    const uint32_t halo = hp * (uint32_t)cin_bytes;
+    const uint32_t halo_al = (halo + 1023u) & ~1023u;
+    const uint32_t bblk = (uint32_t)bn * kc_bytes;
+    const uint32_t bres_total = 9u * p.cblocks * bblk;
+    if (bres_total + 2 * halo_al <= 200u * 1024u) {
+      p.mode = MODE_HALO;
+      p.tw = 8;
+      p.th = 16;
+      p.tiles_x = (int)ceil_div(d.out_w, 8);
+      p.tiles_y = (int)ceil_div(d.out_h, 16);
+      p.m_tiles = d.batch * p.tiles_x * p.tiles_y;
+      const int64_t t2 = (int64_t)p.m_tiles;
+      pl.grid_x = (int)(t2 < kNumSMs ? t2 : kNumSMs);
+      p.a_bytes = halo_al;
+      p.b_bytes = 0;
+      int hs = (int)((200u * 1024u - bres_total) / halo_al);
+      p.stages = hs > 6 ? 6 : hs;
+      p.halo_tx = halo;
+      p.hp = hp;
+      p.hw = hw;
+      p.cin_bytes = (uint32_t)cin_bytes;
+      p.bblk_bytes = bblk;
+      p.bres_bytes = bres_total;
+    }
+  }
   const int cols = 2 * bn;  // double-buffered accumulator
   p.tmem_cols = cols <= 32 ? 32 : (cols <= 64 ? 64 : (cols <= 128 ? 128 : (cols <= 256 ? 256 : 512)));
   const uint32_t m_enc = 128u >> 4, n_enc = (uint32_t)bn >> 3;
@@ -560,7 +725,7 @@ Plan plan_for(const pmx_conv_desc& d) {
     p.idesc = (2u << 4) | (1u << 7) | (1u << 10) | (n_enc << 17) | (m_enc << 24);
   else
     p.idesc = (1u << 4) | (0u << 7) | (0u << 10) | (n_enc << 17) | (m_enc << 24);
-  pl.smem = 1024 + (size_t)stages * stage + (2 * stages + 4) * 8 + 16;
+  pl.smem = 1024 + (size_t)p.stages * (p.a_bytes + p.b_bytes) + p.bres_bytes + (2 * p.stages + 5) * 8 + 16;
   pl.ok = true;
   return pl;
 }
@@ -573,7 +738,16 @@ pmx_status build_maps(const pmx_conv_desc& d, const Plan& pl, const void* x, con
   const char* xb = static_cast<const char*>(x) + (size_t)d.in_c_offset * esz;
   const cuuint64_t cs = (cuuint64_t)d.in_c_stride * esz;
   pmx_status st;
-  if (p.mode == MODE_CONV3) {
+  if (p.mode == MODE_HALO) {
+    // [channel group][halo pixel][16 bytes]: dims {16B of channels, W, H, channel groups, B}
+    const cuuint32_t cpg = 16 / esz;
+    cuuint64_t dims[5] = {cpg, (cuuint64_t)d.in_w, (cuuint64_t)d.in_h, (cuuint64_t)(p.cin_bytes / 16),
+                          (cuuint64_t)d.batch};
+    cuuint64_t str[4] = {cs, cs * d.in_w, 16, cs * d.in_w * d.in_h};
+    cuuint32_t box[5] = {cpg, p.hw, p.hp / p.hw, p.cin_bytes / 16, 1};
+    st = encode(&maps->a[0], dt, 5, xb, dims, str, box, CU_TENSOR_MAP_SWIZZLE_NONE);
+    if (st != PMX_OK) return st;
+  } else if (p.mode == MODE_CONV3) {
     if (p.stride == 1) {
       cuuint64_t dims[4] = {(cuuint64_t)d.in_c, (cuuint64_t)d.in_w, (cuuint64_t)d.in_h, (cuuint64_t)d.batch};
       cuuint64_t str[3] = {cs, cs * d.in_w, cs * d.in_w * d.in_h};
@@ -609,7 +783,7 @@ pmx_status build_maps(const pmx_conv_desc& d, const Plan& pl, const void* x, con
 }  // namespace
 
 const char* conv_tc_backend(int dtype, int) {
-  if (g_conv_backend_mode == 1) return "simt";
+  if (g_conv_backend_mode == 1) return "simt";  // 2 = tcgen05 without the halo variant (tests)
   return (dtype == PMX_I8 || dtype == PMX_F16) ? "tcgen05" : "simt";
 }
 
@@ -632,16 +806,37 @@ pmx_status conv_tc_try(const pmx_conv_desc& d, const void* x, const void* w, con
   pl.p.bias = bias;
   pl.p.bn_post = bn_post;
   pl.p.keys = keys;
+  pl.p.trace = g_trace;
   dim3 grid(pl.grid_x, pl.grid_y);
+  // OUTK 1: the common single int8 consumer with 16-byte aligned pixel rows
+  const bool one_i8 = outs.n == 1 && outs.o[0].dtype == PMX_I8 && outs.o[0].c_stride % 16 == 0 &&
+                      outs.o[0].c_offset % 16 == 0 && (reinterpret_cast<uintptr_t>(outs.o[0].ptr) & 15) == 0;
+  auto launch = [&](auto kern) -> pmx_status {
+    PMX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
+    kern<<<grid, kThreads, pl.smem, st>>>(maps, pl.p, outs);
+    return PMX_OK;
+  };
+  const int kcb = (int)(pl.p.sbo / 8);  // K-block bytes (64 or 128)
+  const int cinb = pl.p.mode == MODE_HALO ? (int)pl.p.cin_bytes : 0;
+#define PMX_TC_LAUNCH(DTV, KB, CB)                                                                    \
+  s = one_i8 ? launch(conv_tc_kernel<DTV, 1, KB, CB>) : launch(conv_tc_kernel<DTV, 0, KB, CB>)
+#define PMX_TC_SHAPES(DTV)                                        \
+  if (cinb == 64) PMX_TC_LAUNCH(DTV, 64, 64);                     \
+  else if (cinb == 128) PMX_TC_LAUNCH(DTV, 128, 128);             \
+  else if (kcb == 64) PMX_TC_LAUNCH(DTV, 64, 0);                  \
+  else PMX_TC_LAUNCH(DTV, 128, 0);
   if (d.in_dtype == PMX_I8) {
-    PMX_CUDA(cudaFuncSetAttribute(conv_tc_kernel<PMX_I8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
-    conv_tc_kernel<PMX_I8><<<grid, kThreads, pl.smem, st>>>(maps, pl.p, outs);
+    PMX_TC_SHAPES(PMX_I8)
   } else {
-    PMX_CUDA(cudaFuncSetAttribute(conv_tc_kernel<PMX_F16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
-    conv_tc_kernel<PMX_F16><<<grid, kThreads, pl.smem, st>>>(maps, pl.p, outs);
+    PMX_TC_SHAPES(PMX_F16)
   }
+#undef PMX_TC_SHAPES
+#undef PMX_TC_LAUNCH
+  if (s != PMX_OK) return s;
   *launched = true;
   return check_launch("pmx_conv(tcgen05)");
 }
 
 }  // namespace pmx
+
+extern "C" void pmx_debug_trace(unsigned long long* buf) { pmx::g_trace = buf; }

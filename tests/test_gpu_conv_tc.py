@@ -54,7 +54,8 @@ def _run(lib, N, torch, desc, x, w, alpha, bias, outs_spec, mode):
 
 @pytest.mark.parametrize("case", CASES, ids=lambda c: f"{c[0]}{c[1]}x{c[2]}k{c[3]}s{c[4]}_{c[5][0]}x{c[5][1]}")
 @pytest.mark.parametrize("prec", ["int8", "fp16"])
-def test_tcgen05_matches_simt(case, prec):
+@pytest.mark.parametrize("tc_mode", [0, 2], ids=["auto", "nohalo"])
+def test_tcgen05_matches_simt(case, prec, tc_mode):
     import torch
 
     from paper_2601_12638_b200 import _native as N
@@ -86,7 +87,7 @@ def test_tcgen05_matches_simt(case, prec):
     bias = torch.from_numpy(rng.normal(scale=0.1, size=cout).astype(np.float32)).cuda()
     spec = [(N.PMX_F32, 0.0), (N.PMX_I8, 0.013), (N.PMX_F16, 0.0)]
     assert lib.pmx_conv_backend(desc.in_dtype, desc.kind).decode() == "tcgen05"
-    tc, ktc = _run(lib, N, torch, desc, x, wt, alpha, bias, spec, 0)
+    tc, ktc = _run(lib, N, torch, desc, x, wt, alpha, bias, spec, tc_mode)
     ref, kref = _run(lib, N, torch, desc, x, wt, alpha, bias, spec, 1)
     if prec == "int8":
         for a, b in zip(tc, ref):
