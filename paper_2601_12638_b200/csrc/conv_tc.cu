@@ -234,7 +234,7 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
 // Persistent: grid = min(tiles, SMs); every role walks the same static tile sequence.
 // Accumulators are double-buffered in TMEM so the epilogue of tile i overlaps the
 // TMA + MMA of tile i+1; the smem ring runs across tile boundaries.
-template <int DT, int OUTK, int KCB, int CINB>
+template <int DT, int OUTK, int KCB, int CINB, int HS>
 __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_constant__ TcMaps maps, const TcParams p,
                                                               const Outs outs) {
   extern __shared__ uint8_t smem_raw[];
@@ -299,7 +299,19 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
           PMX_TRACE(0, it);
           mbar_wait(empty(s), ph ^ 1);
           mbar_expect_tx(full(s), p.halo_tx);
-          tma_load_5d(a_smem + s * p.a_bytes, &maps.a[0], 0, ox0 - 1, oy0 - 1, 0, tb, full(s));
+          const uint32_t slot = a_smem + s * p.a_bytes;
+          if (p.stride == 1) {
+            tma_load_5d(slot, &maps.a[0], 0, ox0 - 1, oy0 - 1, 0, tb, full(s));
+          } else {
+            // four parity planes (py, px): (16 + py) x (8 + px) pixels from (oy0 - py, ox0 - px)
+            uint32_t off = 0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const int py = q >> 1, px = q & 1;
+              tma_load_5d(slot + off, &maps.a[q], 0, ox0 - px, oy0 - py, 0, tb, full(s));
+              off += (uint32_t)((16 + py) * (8 + px)) * p.cin_bytes;
+            }
+          }
           PMX_TRACE(1, it);
         }
       }
@@ -352,8 +364,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
       const uint64_t dsw = sdesc(0, p.sbo, p.layout);  // swizzled operands (address field 0)
       uint32_t it = 0, i = 0;
       if constexpr (CINB > 0) {
-        constexpr int HW = 10, HP = 180, CB = CINB / KCB;
-        const uint64_t dhalo = sdesc(0, HW * 16u, 0u, HP * 16u);
+        constexpr int CB = CINB / KCB;
         const uint32_t bblk = p.bblk_bytes;
         mbar_wait(bfull, 0);
         tc_fence_after();
@@ -370,10 +381,19 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
           const uint32_t abase = a_smem + s * p.a_bytes;
 #pragma unroll
           for (int tap = 0; tap < 9; ++tap) {
+            // A operand of this tap inside the halo: plane base, pixel offset, row width
+            const int dy = tap / 3 - 1, dx = tap % 3 - 1;
+            const int py = HS == 2 ? (dy != 0) : 0, px = HS == 2 ? (dx != 0) : 0;
+            const int HW = HS == 2 ? 8 + px : 10;              // halo row width (pixels)
+            const int HPX = HS == 2 ? (16 + py) * HW : 180;    // pixels in this plane
+            const int q = py * 2 + px;
+            const int plane_px = HS == 2 ? (q == 0 ? 0 : (q == 1 ? 128 : (q == 2 ? 272 : 408))) : 0;
+            const int pix0 = HS == 2 ? (dy == 1) * HW + (dx == 1) : (dy + 1) * HW + (dx + 1);
+            const uint64_t dhalo = sdesc(0, HW * 16u, 0u, HPX * 16u);
 #pragma unroll
             for (int k = 0; k < CINB / 32; ++k) {
               // two 16-byte channel groups per instruction (core matrices at +LBO)
-              const uint32_t aoff = (uint32_t)(((2 * k) * HP + (tap / 3) * HW + (tap % 3)) * 16);
+              const uint32_t aoff = (uint32_t)(plane_px * CINB + ((2 * k) * HPX + pix0) * 16);
               const uint32_t boff = (uint32_t)((tap * CB + (k * 32) / KCB)) * bblk + (uint32_t)((k * 32) % KCB);
               const uint64_t ad = dhalo | (uint64_t)(((abase + aoff) & 0x3FFFFu) >> 4);
               const uint64_t bd = dsw | (uint64_t)(((bres + boff) & 0x3FFFFu) >> 4);
@@ -690,14 +710,16 @@ Plan plan_for(const pmx_conv_desc& d) {
   if (stages < 2) stages = 2;
   p.stages = stages;
   p.bres_bytes = 0;
-  if (conv3 && p.stride == 1 && g_conv_backend_mode != 2 && cin_bytes == kc_bytes && p.n_tiles == 1 &&
-      d.out_w >= 8) {
-    const uint32_t hw = 10, hh = 18, hp = hw * hh;  // (16 + 2) x (8 + 2) halo of a 16 x 8 tile
+  if (conv3 && g_conv_backend_mode != 2 && cin_bytes == kc_bytes && p.n_tiles == 1 && d.out_w >= 8) {
+    // stride 1: one (16 + 2) x (8 + 2) halo; stride 2: four parity planes of
+    // (16 + py) x (8 + px) pixels (561 in total) -- see the producer
+    const uint32_t hw = 10, hp = p.stride == 1 ? 180u : 561u;
     const uint32_t halo = hp * (uint32_t)cin_bytes;
     const uint32_t halo_al = (halo + 1023u) & ~1023u;
     const uint32_t bblk = (uint32_t)bn * kc_bytes;
     const uint32_t bres_total = 9u * p.cblocks * bblk;
-    if (bres_total + 2 * halo_al <= 200u * 1024u) {
+    const uint32_t budget = 227u * 1024u - 2048u;  // dynamic smem minus alignment + barriers
+    if (bres_total + 2 * halo_al <= budget) {
       p.mode = MODE_HALO;
       p.tw = 8;
       p.th = 16;
@@ -708,7 +730,7 @@ Plan plan_for(const pmx_conv_desc& d) {
       pl.grid_x = (int)(t2 < kNumSMs ? t2 : kNumSMs);
       p.a_bytes = halo_al;
       p.b_bytes = 0;
-      int hs = (int)((200u * 1024u - bres_total) / halo_al);
+      int hs = (int)((budget - bres_total) / halo_al);
       p.stages = hs > 6 ? 6 : hs;
       p.halo_tx = halo;
       p.hp = hp;
@@ -738,7 +760,21 @@ pmx_status build_maps(const pmx_conv_desc& d, const Plan& pl, const void* x, con
   const char* xb = static_cast<const char*>(x) + (size_t)d.in_c_offset * esz;
   const cuuint64_t cs = (cuuint64_t)d.in_c_stride * esz;
   pmx_status st;
-  if (p.mode == MODE_HALO) {
+  if (p.mode == MODE_HALO && p.stride == 2) {
+    // parity plane (py, px) of the input: x[2i + py, 2j + px] -> plane[i, j];
+    // [channel group][plane pixel][16 bytes], box (16 + py) x (8 + px)
+    const cuuint32_t cpg = 16 / esz;
+    for (int q = 0; q < 4; ++q) {
+      const int py = q >> 1, px = q & 1;
+      cuuint64_t dims[5] = {cpg, (cuuint64_t)(d.in_w / 2), (cuuint64_t)(d.in_h / 2), (cuuint64_t)(p.cin_bytes / 16),
+                            (cuuint64_t)d.batch};
+      cuuint64_t str[4] = {2 * cs, 2 * cs * d.in_w, 16, cs * d.in_w * d.in_h};
+      cuuint32_t box[5] = {cpg, (cuuint32_t)(8 + px), (cuuint32_t)(16 + py), p.cin_bytes / 16, 1};
+      const char* basep = xb + (size_t)(py * d.in_w + px) * cs;
+      st = encode(&maps->a[q], dt, 5, basep, dims, str, box, CU_TENSOR_MAP_SWIZZLE_NONE);
+      if (st != PMX_OK) return st;
+    }
+  } else if (p.mode == MODE_HALO) {
     // [channel group][halo pixel][16 bytes]: dims {16B of channels, W, H, channel groups, B}
     const cuuint32_t cpg = 16 / esz;
     cuuint64_t dims[5] = {cpg, (cuuint64_t)d.in_w, (cuuint64_t)d.in_h, (cuuint64_t)(p.cin_bytes / 16),
@@ -818,13 +854,16 @@ pmx_status conv_tc_try(const pmx_conv_desc& d, const void* x, const void* w, con
   };
   const int kcb = (int)(pl.p.sbo / 8);  // K-block bytes (64 or 128)
   const int cinb = pl.p.mode == MODE_HALO ? (int)pl.p.cin_bytes : 0;
-#define PMX_TC_LAUNCH(DTV, KB, CB)                                                                    \
-  s = one_i8 ? launch(conv_tc_kernel<DTV, 1, KB, CB>) : launch(conv_tc_kernel<DTV, 0, KB, CB>)
+  const int hs = pl.p.mode == MODE_HALO ? pl.p.stride : 0;
+#define PMX_TC_LAUNCH(DTV, KB, CB, HSV)                                                                     \
+  s = one_i8 ? launch(conv_tc_kernel<DTV, 1, KB, CB, HSV>) : launch(conv_tc_kernel<DTV, 0, KB, CB, HSV>)
 #define PMX_TC_SHAPES(DTV)                                        \
-  if (cinb == 64) PMX_TC_LAUNCH(DTV, 64, 64);                     \
-  else if (cinb == 128) PMX_TC_LAUNCH(DTV, 128, 128);             \
-  else if (kcb == 64) PMX_TC_LAUNCH(DTV, 64, 0);                  \
-  else PMX_TC_LAUNCH(DTV, 128, 0);
+  if (cinb == 64 && hs == 1) PMX_TC_LAUNCH(DTV, 64, 64, 1);       \
+  else if (cinb == 64) PMX_TC_LAUNCH(DTV, 64, 64, 2);             \
+  else if (cinb == 128 && hs == 1) PMX_TC_LAUNCH(DTV, 128, 128, 1); \
+  else if (cinb == 128) PMX_TC_LAUNCH(DTV, 128, 128, 2);          \
+  else if (kcb == 64) PMX_TC_LAUNCH(DTV, 64, 0, 0);               \
+  else PMX_TC_LAUNCH(DTV, 128, 0, 0);
   if (d.in_dtype == PMX_I8) {
     PMX_TC_SHAPES(PMX_I8)
   } else {
