@@ -190,43 +190,6 @@ struct TcMaps {
 constexpr int kEpiWarps = 16;                  // warps 2..17: four per TMEM lane quarter
 constexpr int kThreads = 32 * (2 + kEpiWarps);  // + TMA producer warp + MMA warp
 
-// 16 f32 values -> 16 exact int8 codes (quantize() semantics), packed.  Common
-// path: q = y * inv rounded by the 1.5*2^23 magic add, whose low byte IS the
-// two's-complement code; one predicate per 16 values sends near-ties (|frac-.5|
-// < 1e-3), |q| >= 127 and NaN to the exact f64 path (quantize_exact).
-__device__ __forceinline__ uint4 quant16(const float (&y)[16], double s, float inv) {
-  // packed f32x2 arithmetic (sm_100): q = y*inv, t = q + M, d = q - (t - M)
-  const float2 M2 = make_float2(12582912.0f, 12582912.0f), I2 = make_float2(inv, inv);
-  const float2 NEG1 = make_float2(-1.0f, -1.0f);
-  uint32_t tb[16];
-  bool good = true;
-#pragma unroll
-  for (int j = 0; j < 16; j += 2) {
-    const float2 qv = __fmul2_rn(make_float2(y[j], y[j + 1]), I2);
-    const float2 t = __fadd2_rn(qv, M2);
-    const float2 d = __fadd2_rn(qv, __ffma2_rn(t, NEG1, M2));  // q + (M - t), both exact
-    good = good && (fabsf(d.x) < 0.499f) && (fabsf(d.y) < 0.499f) && (fabsf(qv.x) < 127.0f) &&
-           (fabsf(qv.y) < 127.0f);
-    tb[j] = __float_as_uint(t.x);
-    tb[j + 1] = __float_as_uint(t.y);
-  }
-  if (!good) {
-#pragma unroll
-    for (int j = 0; j < 16; ++j) tb[j] = (uint32_t)quantize_exact(y[j], s, inv);
-  }
-  return make_uint4(__byte_perm(__byte_perm(tb[0], tb[1], 0x0040), __byte_perm(tb[2], tb[3], 0x0040), 0x5410),
-                    __byte_perm(__byte_perm(tb[4], tb[5], 0x0040), __byte_perm(tb[6], tb[7], 0x0040), 0x5410),
-                    __byte_perm(__byte_perm(tb[8], tb[9], 0x0040), __byte_perm(tb[10], tb[11], 0x0040), 0x5410),
-                    __byte_perm(__byte_perm(tb[12], tb[13], 0x0040), __byte_perm(tb[14], tb[15], 0x0040), 0x5410));
-}
-
-// fp16_roundtrip semantics for a pair: satfinite == clip(+-65504) then RNE; NaN stays NaN
-__device__ __forceinline__ uint32_t f16x2_sat(float lo_v, float hi_v) {
-  uint32_t r;
-  asm("cvt.rn.satfinite.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi_v), "f"(lo_v));
-  return r;
-}
-
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }

@@ -1,14 +1,18 @@
 // K4+K5 fused pillar feature net + BEV scatter.
 //
-// One warp per pillar, lane = point slot (M <= 32).  The 9 features are built in
-// registers (sequential f32 mean via shuffle broadcast, matching numpy's
-// chunk.mean(axis=0) bit for bit), transformed to layer 1's precision (exact int8
-// codes / binary16 / f32), then every live point is broadcast in turn and each
-// lane accumulates its output channels (lane, lane+32).  The running max over
-// points stays in registers; the pooled value is written once per consumer
-// format straight onto the NHWC canvas (scatter fused, no [P, C] round trip).
+// Four threads per pillar, 16 output channels each (64 pillars per 256-thread
+// block).  A KITTI pillar holds ~1-3 points, so a lane-per-point warp would idle
+// >90% of its lanes; here every thread walks its pillar's points itself: the 9
+// features are rebuilt in registers (sequential f32 mean in slot order, matching
+// numpy's chunk.mean(axis=0) bit for bit), transformed to layer 1's precision
+// (exact int8 codes / binary16 / f32), multiplied against the weights staged once
+// per block in shared memory (feature-major, 16-channel float4 rows), max-pooled
+// in registers, and the pooled column is written once per consumer format straight
+// onto the NHWC canvas (scatter fused; 16-byte vector stores).
 // Replaces pm/model.py:334-355 -> _run_weight_layer :271-307 -> linear
 // pm/tensor_ops.py:80-91, relu :134, max_over_points :163-173, scatter :138-160.
+// INT8: features and weights are integer codes; the 9-term dot product of codes
+// (|sum| < 2^18) is exact in f32 FMA, then y = fma(acc, s_x * s_w[c], bias[c]).
 #include "pmx_common.cuh"
 
 namespace pmx {
@@ -17,6 +21,9 @@ namespace {
 
 constexpr int kMaxF = 16;
 constexpr int kMaxC = 64;
+constexpr int kTPP = 4;                      // threads per pillar
+constexpr int kThreads = 256;
+constexpr int kPPB = kThreads / kTPP;        // pillars per block
 
 struct PfnArgs {
   pmx_pfn_desc d;
@@ -39,17 +46,39 @@ struct PfnArgs {
   uint32_t* out_keys;
 };
 
+template <int DT>
+__device__ __forceinline__ float transform_in(float v, const PfnArgs& a) {
+  if constexpr (DT == PMX_I8) return (float)quantize_fast(v, a.d.in_scale, a.in_inv);
+  else if constexpr (DT == PMX_F16) return __half2float(f16_sat(v));
+  else return v;
+}
+
 template <int DT, int NF, bool FROM_POINTS>
-__global__ void __launch_bounds__(256) pfn_kernel(const PfnArgs a, const Outs outs) {
+__global__ void __launch_bounds__(kThreads) pfn_kernel(const PfnArgs a, const Outs outs) {
+  __shared__ __align__(16) float ws[kMaxF][kMaxC];  // weights, feature-major
+  __shared__ __align__(16) float ps[3][kMaxC];      // alpha (I8), bias, unused
   const int b = blockIdx.y;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int p = blockIdx.x * 8 + wid;
-  const int P = a.n_pillars[b];
-  const int M = a.d.max_points;
   const int F = FROM_POINTS ? 9 : NF;
   const int C = a.d.channels;
-  const int64_t hw = (int64_t)a.g.grid_h * a.g.grid_w;
+  const int M = a.d.max_points;
+  for (int e = threadIdx.x; e < kMaxF * kMaxC; e += kThreads) {
+    const int j = e / kMaxC, c = e % kMaxC;
+    float w = 0.f;
+    if (j < F && c < C) {
+      if constexpr (DT == PMX_I8) w = (float)reinterpret_cast<const int8_t*>(a.weight)[c * F + j];
+      else if constexpr (DT == PMX_F16) w = __half2float(reinterpret_cast<const __half*>(a.weight)[c * F + j]);
+      else w = reinterpret_cast<const float*>(a.weight)[c * F + j];
+    }
+    ws[j][c] = w;
+  }
+  for (int c = threadIdx.x; c < kMaxC; c += kThreads) {
+    ps[0][c] = (DT == PMX_I8 && c < C) ? a.alpha[c] : 1.f;
+    ps[1][c] = c < C ? a.bias[c] : 0.f;
+  }
+  __syncthreads();
 
+  const int P = a.n_pillars[b];
+  const int64_t hw = (int64_t)a.g.grid_h * a.g.grid_w;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     const uint32_t zk = f2key(0.0f);
     if (a.out_keys && P < hw) {  // empty cells stay 0 on the canvas
@@ -61,176 +90,140 @@ __global__ void __launch_bounds__(256) pfn_kernel(const PfnArgs a, const Outs ou
       atomicMax(a.in_keys + 1, zk);
     }
   }
-  if (p >= P) return;
-  const int64_t q = (int64_t)b * a.pcap + p;
+  const int p = blockIdx.x * kPPB + threadIdx.x / kTPP;
+  const int cq = threadIdx.x % kTPP;
+  const int c0 = cq * 16;
+  const bool live = p < P && c0 < C;
+  const int64_t q = (int64_t)b * a.pcap + (p < P ? p : 0);
+  const float INF = __int_as_float(0x7f800000);
+  float in_lo = INF, in_hi = -INF;
 
-  // ---- features of this lane's slot
-  float f[kMaxF];
+  float mx[16];
 #pragma unroll
-  for (int j = 0; j < kMaxF; ++j) f[j] = 0.f;
-  bool live;
-  if (FROM_POINTS) {
-    const int k = a.counts[q];
-    live = lane < k;
-    float4 pt = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (live) pt = __ldg(a.points + a.offs[b] + a.pt_idx[q * M + lane]);
-    float sx = 0.f, sy = 0.f, sz = 0.f;
-    for (int s = 0; s < k; ++s) {
-      sx = __fadd_rn(sx, __shfl_sync(0xffffffffu, pt.x, s));
-      sy = __fadd_rn(sy, __shfl_sync(0xffffffffu, pt.y, s));
-      sz = __fadd_rn(sz, __shfl_sync(0xffffffffu, pt.z, s));
-    }
-    const float fk = (float)(k > 0 ? k : 1);
-    const float mx = __fdiv_rn(sx, fk), my = __fdiv_rn(sy, fk), mz = __fdiv_rn(sz, fk);
-    const float xoff = (float)((double)a.g.cell_w * 0.5 + (double)a.g.x_min);
-    const float yoff = (float)((double)a.g.cell_h * 0.5 + (double)a.g.y_min);
-    const float xc = __fadd_rn(__fmul_rn((float)a.coords[2 * q + 1], a.g.cell_w), xoff);
-    const float yc = __fadd_rn(__fmul_rn((float)a.coords[2 * q + 0], a.g.cell_h), yoff);
-    if (live) {
-      f[0] = pt.x; f[1] = pt.y; f[2] = pt.z; f[3] = pt.w;
-      f[4] = __fsub_rn(pt.x, mx); f[5] = __fsub_rn(pt.y, my); f[6] = __fsub_rn(pt.z, mz);
-      f[7] = __fsub_rn(pt.x, xc); f[8] = __fsub_rn(pt.y, yc);
-    }
-    if (a.in_keys) {  // layer-1 observer: real rows, plus the zero padding rows if any
-      float lo = 0.f, hi = 0.f;
-      if (live) {
-        lo = f[0]; hi = f[0];
-#pragma unroll
-        for (int j = 1; j < 9; ++j) { lo = nmin(lo, f[j]); hi = nmax(hi, f[j]); }
+  for (int j = 0; j < 16; ++j) mx[j] = -INF;
+
+  if (live) {
+    int k;
+    float4 ctr = make_float4(0.f, 0.f, 0.f, 0.f);  // cluster mean (x, y, z), pillar centre offsets
+    float xc = 0.f, yc = 0.f;
+    const float4* fp = nullptr;
+    if (FROM_POINTS) {
+      k = a.counts[q];
+      fp = a.points + a.offs[b];
+      float sx = 0.f, sy = 0.f, sz = 0.f;
+      for (int s = 0; s < k; ++s) {
+        const float4 pt = __ldg(fp + a.pt_idx[q * M + s]);
+        sx = __fadd_rn(sx, pt.x);
+        sy = __fadd_rn(sy, pt.y);
+        sz = __fadd_rn(sz, pt.z);
       }
-      const bool has_pad = k < M;
-      if (!live && !has_pad) { lo = __int_as_float(0x7f800000); hi = -lo; }
-      if (lane >= M) { lo = __int_as_float(0x7f800000); hi = -lo; }
-      block_minmax_commit<256>(lo, hi, a.in_keys);
+      const float fk = (float)(k > 0 ? k : 1);
+      ctr = make_float4(__fdiv_rn(sx, fk), __fdiv_rn(sy, fk), __fdiv_rn(sz, fk), 0.f);
+      const float xoff = (float)((double)a.g.cell_w * 0.5 + (double)a.g.x_min);
+      const float yoff = (float)((double)a.g.cell_h * 0.5 + (double)a.g.y_min);
+      xc = __fadd_rn(__fmul_rn((float)a.coords[2 * q + 1], a.g.cell_w), xoff);
+      yc = __fadd_rn(__fmul_rn((float)a.coords[2 * q + 0], a.g.cell_h), yoff);
+      if (k < M) { in_lo = 0.f; in_hi = 0.f; }  // zero padding rows are part of layer 1's input
+    } else {
+      k = M;
     }
-  } else {
-    live = false;
-    if (lane < M) {
-      live = a.mask[q * M + lane] != 0;
-      const float* src = a.features + (q * M + lane) * F;
+    for (int s = 0; s < k; ++s) {
+      float f[kMaxF];
 #pragma unroll
-      for (int j = 0; j < kMaxF; ++j)
-        if (j < F) f[j] = src[j];
-    }
-    if (a.in_keys) {
-      float lo = __int_as_float(0x7f800000), hi = -lo;
-      if (lane < M) {
+      for (int j = 0; j < kMaxF; ++j) f[j] = 0.f;
+      if (FROM_POINTS) {
+        const float4 pt = __ldg(fp + a.pt_idx[q * M + s]);
+        f[0] = pt.x; f[1] = pt.y; f[2] = pt.z; f[3] = pt.w;
+        f[4] = __fsub_rn(pt.x, ctr.x); f[5] = __fsub_rn(pt.y, ctr.y); f[6] = __fsub_rn(pt.z, ctr.z);
+        f[7] = __fsub_rn(pt.x, xc); f[8] = __fsub_rn(pt.y, yc);
+      } else {
+        const float* src = a.features + (q * M + s) * F;
 #pragma unroll
         for (int j = 0; j < kMaxF; ++j)
-          if (j < F) { lo = nmin(lo, f[j]); hi = nmax(hi, f[j]); }
+          if (j < F) f[j] = src[j];
       }
-      block_minmax_commit<256>(lo, hi, a.in_keys);
-    }
-  }
-
-  // ---- precision transform of the layer input (pm/model.py:273-285)
-  int fq[kMaxF];
-  if (DT == PMX_I8) {
+      if (a.in_keys) {
 #pragma unroll
-    for (int j = 0; j < kMaxF; ++j) fq[j] = j < F ? quantize_exact(f[j], a.d.in_scale, a.in_inv) : 0;
-  } else if (DT == PMX_F16) {
+        for (int j = 0; j < kMaxF; ++j)
+          if (j < F) { in_lo = nmin(in_lo, f[j]); in_hi = nmax(in_hi, f[j]); }
+      }
+      if (!FROM_POINTS && a.mask[q * M + s] == 0) continue;  // padding row: no effect on the max
 #pragma unroll
-    for (int j = 0; j < kMaxF; ++j) f[j] = __half2float(f16_sat(f[j]));
-  }
-
-  // ---- per-lane channels: c0 = lane, c1 = lane + 32
-  float w0[kMaxF], w1[kMaxF];
-  int iw0[kMaxF], iw1[kMaxF];
-  const int c0 = lane, c1 = lane + 32;
-  const bool h0 = c0 < C, h1 = c1 < C;
+      for (int j = 0; j < kMaxF; ++j)
+        if (j < F) f[j] = transform_in<DT>(f[j], a);
+      float acc[16];
 #pragma unroll
-  for (int j = 0; j < kMaxF; ++j) {
-    w0[j] = w1[j] = 0.f;
-    iw0[j] = iw1[j] = 0;
-    if (j < F) {
-      if (DT == PMX_I8) {
-        const int8_t* W = reinterpret_cast<const int8_t*>(a.weight);
-        if (h0) iw0[j] = W[c0 * F + j];
-        if (h1) iw1[j] = W[c1 * F + j];
-      } else if (DT == PMX_F16) {
-        const __half* W = reinterpret_cast<const __half*>(a.weight);
-        if (h0) w0[j] = __half2float(W[c0 * F + j]);
-        if (h1) w1[j] = __half2float(W[c1 * F + j]);
+      for (int c = 0; c < 16; ++c) acc[c] = 0.f;
+#pragma unroll
+      for (int j = 0; j < kMaxF; ++j) {
+        if (j < F) {
+#pragma unroll
+          for (int c4 = 0; c4 < 4; ++c4) {
+            const float4 w4 = *reinterpret_cast<const float4*>(&ws[j][c0 + 4 * c4]);
+            acc[4 * c4 + 0] = __fmaf_rn(f[j], w4.x, acc[4 * c4 + 0]);
+            acc[4 * c4 + 1] = __fmaf_rn(f[j], w4.y, acc[4 * c4 + 1]);
+            acc[4 * c4 + 2] = __fmaf_rn(f[j], w4.z, acc[4 * c4 + 2]);
+            acc[4 * c4 + 3] = __fmaf_rn(f[j], w4.w, acc[4 * c4 + 3]);
+          }
+        }
+      }
+      if (a.bn_post == nullptr) {
+        // y = fl(acc * alpha + bias) (alpha > 0) and ReLU are monotone, so the max over
+        // points commutes with the epilogue: pool the raw sums, finish once below
+#pragma unroll
+        for (int c = 0; c < 16; ++c) mx[c] = nmax(mx[c], acc[c]);
       } else {
-        const float* W = reinterpret_cast<const float*>(a.weight);
-        if (h0) w0[j] = W[c0 * F + j];
-        if (h1) w1[j] = W[c1 * F + j];
-      }
-    }
-  }
-  const float al0 = (DT == PMX_I8 && h0) ? a.alpha[c0] : 1.f;
-  const float al1 = (DT == PMX_I8 && h1) ? a.alpha[c1] : 1.f;
-  const float b0 = h0 ? a.bias[c0] : 0.f, b1 = h1 ? a.bias[c1] : 0.f;
-  float bm0 = 0.f, bf0 = 1.f, bb0 = 0.f, bm1 = 0.f, bf1 = 1.f, bb1 = 0.f;
-  if (a.bn_post) {
-    if (h0) { bm0 = a.bn_post[c0]; bf0 = a.bn_post[C + c0]; bb0 = a.bn_post[2 * C + c0]; }
-    if (h1) { bm1 = a.bn_post[c1]; bf1 = a.bn_post[C + c1]; bb1 = a.bn_post[2 * C + c1]; }
-  }
-
-  const float NEG_INF = -__int_as_float(0x7f800000);
-  float m0 = NEG_INF, m1 = NEG_INF;
-  unsigned vm = __ballot_sync(0xffffffffu, live && lane < M);
-  while (vm) {
-    const int s = __ffs(vm) - 1;
-    vm &= vm - 1;
-    float y0, y1;
-    if (DT == PMX_I8) {
-      int acc0 = 0, acc1 = 0;
+        // unfolded BN may have a negative gamma: finish every point (rare path)
 #pragma unroll
-      for (int j = 0; j < kMaxF; ++j) {
-        if (j < F) {
-          const int v = __shfl_sync(0xffffffffu, fq[j], s);
-          acc0 += v * iw0[j];
-          acc1 += v * iw1[j];
+        for (int c = 0; c < 16; ++c) {
+          float y;
+          if constexpr (DT == PMX_I8) y = __fmaf_rn(acc[c], ps[0][c0 + c], ps[1][c0 + c]);
+          else y = __fadd_rn(acc[c], ps[1][c0 + c]);
+          if (c0 + c < C)
+            y = __fadd_rn(__fmul_rn(__fsub_rn(y, a.bn_post[c0 + c]), a.bn_post[C + c0 + c]),
+                          a.bn_post[2 * C + c0 + c]);
+          if (a.d.relu) y = fmaxf(y, 0.f);
+          mx[c] = nmax(mx[c], y);
         }
       }
-      y0 = __fadd_rn(__fmul_rn((float)acc0, al0), b0);
-      y1 = __fadd_rn(__fmul_rn((float)acc1, al1), b1);
-    } else {
-      float acc0 = 0.f, acc1 = 0.f;
+    }
+    if (a.bn_post == nullptr) {
 #pragma unroll
-      for (int j = 0; j < kMaxF; ++j) {
-        if (j < F) {
-          const float v = __shfl_sync(0xffffffffu, f[j], s);
-          acc0 = __fmaf_rn(v, w0[j], acc0);
-          acc1 = __fmaf_rn(v, w1[j], acc1);
-        }
+      for (int c = 0; c < 16; ++c) {
+        float y;
+        if constexpr (DT == PMX_I8) y = __fmaf_rn(mx[c], ps[0][c0 + c], ps[1][c0 + c]);
+        else y = __fadd_rn(mx[c], ps[1][c0 + c]);
+        if (a.d.relu) y = fmaxf(y, 0.f);
+        mx[c] = y;
       }
-      y0 = __fadd_rn(acc0, b0);
-      y1 = __fadd_rn(acc1, b1);
     }
-    if (a.bn_post) {
-      y0 = __fadd_rn(__fmul_rn(__fsub_rn(y0, bm0), bf0), bb0);
-      y1 = __fadd_rn(__fmul_rn(__fsub_rn(y1, bm1), bf1), bb1);
-    }
-    if (a.d.relu) {
-      y0 = fmaxf(y0, 0.f);
-      y1 = fmaxf(y1, 0.f);
-    }
-    m0 = nmax(m0, y0);
-    m1 = nmax(m1, y1);
+    // scatter the pooled 16-channel run onto the canvas, every consumer format
+    const int64_t pix = ((int64_t)b * a.g.grid_h + a.coords[2 * q]) * a.g.grid_w + a.coords[2 * q + 1];
+    const int n_live = C - c0 < 16 ? C - c0 : 16;
+#pragma unroll
+    for (int o = 0; o < PMX_MAX_OUTS; ++o)
+      if (o < outs.n) store16(outs.o[o], pix, c0, mx, n_live);
   }
-
-  // ---- scatter the pooled column onto the canvas, every consumer format
-  const int64_t pix = ((int64_t)b * a.g.grid_h + a.coords[2 * q]) * a.g.grid_w + a.coords[2 * q + 1];
-  if (h0) store_all(outs, pix, c0, m0);
-  if (h1) store_all(outs, pix, c1, m1);
+  if (a.in_keys) block_minmax_commit<kThreads>(in_lo, in_hi, a.in_keys);
   if (a.out_keys) {
-    float lo = h0 ? m0 : __int_as_float(0x7f800000), hi = h0 ? m0 : -__int_as_float(0x7f800000);
-    if (h1) { lo = nmin(lo, m1); hi = nmax(hi, m1); }
-    block_minmax_commit<256>(lo, hi, a.out_keys);
+    float lo = INF, hi = -INF;
+    if (live) {
+      const int n_live = C - c0 < 16 ? C - c0 : 16;
+      for (int c = 0; c < n_live; ++c) { lo = nmin(lo, mx[c]); hi = nmax(hi, mx[c]); }
+    }
+    block_minmax_commit<kThreads>(lo, hi, a.out_keys);
   }
 }
 
 template <int DT>
 pmx_status launch_dt(const PfnArgs& a, const Outs& outs, dim3 grid, cudaStream_t st) {
   if (a.d.source == PMX_PFN_FROM_POINTS9) {
-    pfn_kernel<DT, 9, true><<<grid, 256, 0, st>>>(a, outs);
+    pfn_kernel<DT, 9, true><<<grid, kThreads, 0, st>>>(a, outs);
   } else {
     switch (a.d.n_features) {
 #define PMX_F_CASE(N) \
   case N:             \
-    pfn_kernel<DT, N, false><<<grid, 256, 0, st>>>(a, outs); break;
+    pfn_kernel<DT, N, false><<<grid, kThreads, 0, st>>>(a, outs); break;
       PMX_F_CASE(1) PMX_F_CASE(2) PMX_F_CASE(3) PMX_F_CASE(4) PMX_F_CASE(5) PMX_F_CASE(6)
       PMX_F_CASE(7) PMX_F_CASE(8) PMX_F_CASE(9) PMX_F_CASE(10) PMX_F_CASE(11) PMX_F_CASE(12)
       PMX_F_CASE(13) PMX_F_CASE(14) PMX_F_CASE(15) PMX_F_CASE(16)
@@ -292,7 +285,7 @@ extern "C" pmx_status pmx_pfn_scatter(const pmx_pfn_desc* desc, const pmx_grid* 
   a.in_keys = in_keys;
   a.out_keys = out_keys;
   Outs o = make_outs(outs, n_outs);
-  dim3 g((unsigned)ceil_div(pcap, 8), (unsigned)batch);
+  dim3 g((unsigned)ceil_div(pcap, kPPB), (unsigned)batch);
   if (d.in_dtype == PMX_I8) return launch_dt<PMX_I8>(a, o, g, stream);
   if (d.in_dtype == PMX_F16) return launch_dt<PMX_F16>(a, o, g, stream);
   return launch_dt<PMX_F32>(a, o, g, stream);

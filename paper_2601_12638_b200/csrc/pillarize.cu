@@ -34,6 +34,8 @@ struct PillarWs {
   int32_t* segoff;  // [B*Pcap]
   int32_t* fill;    // [B*Pcap]
   int32_t* csr;     // [B*Nmax]
+  int32_t* ovf_n;   // [1] pillars with > 32 points (rare: dense clusters)
+  int2* ovf;        // [B*Pcap] (frame, pillar) of those
 };
 
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -60,6 +62,8 @@ size_t carve(const pmx_grid* g, int32_t B, int64_t nmax, int32_t pcap, void* bas
   w.segoff = (int32_t*)take(sizeof(int32_t) * B * pcap);
   w.fill = (int32_t*)take(sizeof(int32_t) * B * pcap);
   w.csr = (int32_t*)take(sizeof(int32_t) * B * (nmax > 0 ? nmax : 1));
+  w.ovf_n = (int32_t*)take(sizeof(int32_t));
+  w.ovf = (int2*)take(sizeof(int2) * B * pcap);
   if (ws) *ws = w;
   return off;
 }
@@ -267,14 +271,44 @@ __global__ void slot_kernel(const int64_t* __restrict__ offs, int64_t nmax, cons
   }
 }
 
+// Thread per pillar: a KITTI pillar holds 1-3 points, so the first-M-by-scene-index
+// selection is a tiny rank count over the segment.  Segments longer than 32 points
+// go to an overflow list handled warp-wide by select_kernel below.
+__global__ void __launch_bounds__(256) select_small_kernel(int64_t nmax, const pmx_grid g, PillarWs w, int32_t pcap,
+                                                           const int32_t* __restrict__ n_pillars, int32_t* pt_idx) {
+  const int b = blockIdx.y;
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n_pillars[b]) return;
+  const int M = g.max_points;
+  const int64_t q = (int64_t)b * pcap + p;
+  const int c = w.fill[q];
+  if (c > 32) {
+    w.ovf[atomicAdd(w.ovf_n, 1)] = make_int2(b, p);
+    return;
+  }
+  const int* seg = w.csr + b * nmax + w.segoff[q];
+  int32_t* dst = pt_idx + q * M;
+  if ((M & 3) == 0) {
+    for (int s = 0; s < M; s += 4) *reinterpret_cast<int4*>(dst + s) = make_int4(-1, -1, -1, -1);
+  } else {
+    for (int s = 0; s < M; ++s) dst[s] = -1;
+  }
+  for (int i = 0; i < c; ++i) {
+    const int v = seg[i];
+    int r = 0;
+    for (int j = 0; j < c; ++j) r += seg[j] < v;
+    if (r < M) dst[r] = v;
+  }
+}
+
 __global__ void __launch_bounds__(256) select_kernel(const int64_t* __restrict__ offs, int64_t nmax,
                                                      const pmx_grid g, PillarWs w, int32_t pcap,
                                                      const int32_t* __restrict__ n_pillars, int32_t* pt_idx) {
   __shared__ int buf[8][32];
-  const int b = blockIdx.y;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int p = blockIdx.x * 8 + wid;
-  if (p >= n_pillars[b]) return;
+  const int n_items = *w.ovf_n;
+  for (int item = blockIdx.x * 8 + wid; item < n_items; item += gridDim.x * 8) {
+  const int b = w.ovf[item].x, p = w.ovf[item].y;
   const int M = g.max_points;
   const int64_t q = (int64_t)b * pcap + p;
   const int c = w.fill[q];
@@ -315,6 +349,8 @@ __global__ void __launch_bounds__(256) select_kernel(const int64_t* __restrict__
     rank += u < v;
   }
   if (v != INT_MAX && rank < M) dst[rank] = v;
+  __syncwarp();
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -415,6 +451,7 @@ pmx_status pmx_pillarize(const float* points, const int64_t* frame_offsets, int3
   PMX_CUDA(cudaMemsetAsync(w.first, 0x7f, sizeof(int32_t) * batch * hw, stream));
   PMX_CUDA(cudaMemsetAsync(w.cnt, 0, sizeof(int32_t) * batch * hw, stream));
   PMX_CUDA(cudaMemsetAsync(w.fill, 0, sizeof(int32_t) * batch * pcap, stream));
+  PMX_CUDA(cudaMemsetAsync(w.ovf_n, 0, sizeof(int32_t), stream));
   const int ptx = (int)std::min<int64_t>(ceil_div(nmax, 256), 4096);
   bin_kernel<<<dim3(ptx, batch), 256, 0, stream>>>(reinterpret_cast<const float4*>(points), frame_offsets, nmax, g, w);
   flag_kernel<<<dim3(nb, batch), kPtBlock, 0, stream>>>(frame_offsets, nmax, g, w, nb);
@@ -423,7 +460,9 @@ pmx_status pmx_pillarize(const float* points, const int64_t* frame_offsets, int3
   cellscan_kernel<<<batch, 32, 0, stream>>>(w, cb, n_pillars);
   emit_kernel<<<dim3(cb, batch), 1024, 0, stream>>>(g, w, cb, pcap, coords, counts);
   slot_kernel<<<dim3(ptx, batch), 256, 0, stream>>>(frame_offsets, nmax, g, w, pcap);
-  select_kernel<<<dim3((int)ceil_div(pcap, 8), batch), 256, 0, stream>>>(frame_offsets, nmax, g, w, pcap, n_pillars, pt_idx);
+  select_small_kernel<<<dim3((int)ceil_div(pcap, 256), batch), 256, 0, stream>>>(nmax, g, w, pcap, n_pillars, pt_idx);
+  // overflow pillars (> 32 points): one warp each, grid-stride over the device-side list
+  select_kernel<<<kNumSMs, 256, 0, stream>>>(frame_offsets, nmax, g, w, pcap, n_pillars, pt_idx);
   return check_launch("pmx_pillarize");
 }
 

@@ -162,6 +162,63 @@ __device__ __forceinline__ void store_all(const Outs& outs, int64_t pix, int c, 
     if (i < outs.n) store_one(outs.o[i], pix, c, y);
 }
 
+// 16 f32 values -> 16 exact int8 codes (quantize() semantics), packed.  Common
+// path: q = y * inv rounded by the 1.5*2^23 magic add, whose low byte IS the
+// two's-complement code; one predicate per 16 values sends near-ties (|frac-.5|
+// < 1e-3), |q| >= 127 and NaN to the exact f64 path (quantize_exact).
+__device__ __forceinline__ uint4 quant16(const float (&y)[16], double s, float inv) {
+  // packed f32x2 arithmetic (sm_100): q = y*inv, t = q + M, d = q - (t - M)
+  const float2 M2 = make_float2(12582912.0f, 12582912.0f), I2 = make_float2(inv, inv);
+  const float2 NEG1 = make_float2(-1.0f, -1.0f);
+  uint32_t tb[16];
+  bool good = true;
+#pragma unroll
+  for (int j = 0; j < 16; j += 2) {
+    const float2 qv = __fmul2_rn(make_float2(y[j], y[j + 1]), I2);
+    const float2 t = __fadd2_rn(qv, M2);
+    const float2 d = __fadd2_rn(qv, __ffma2_rn(t, NEG1, M2));  // q + (M - t), both exact
+    good = good && (fabsf(d.x) < 0.499f) && (fabsf(d.y) < 0.499f) && (fabsf(qv.x) < 127.0f) &&
+           (fabsf(qv.y) < 127.0f);
+    tb[j] = __float_as_uint(t.x);
+    tb[j + 1] = __float_as_uint(t.y);
+  }
+  if (!good) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) tb[j] = (uint32_t)quantize_exact(y[j], s, inv);
+  }
+  return make_uint4(__byte_perm(__byte_perm(tb[0], tb[1], 0x0040), __byte_perm(tb[2], tb[3], 0x0040), 0x5410),
+                    __byte_perm(__byte_perm(tb[4], tb[5], 0x0040), __byte_perm(tb[6], tb[7], 0x0040), 0x5410),
+                    __byte_perm(__byte_perm(tb[8], tb[9], 0x0040), __byte_perm(tb[10], tb[11], 0x0040), 0x5410),
+                    __byte_perm(__byte_perm(tb[12], tb[13], 0x0040), __byte_perm(tb[14], tb[15], 0x0040), 0x5410));
+}
+
+// fp16_roundtrip semantics for a pair: satfinite == clip(+-65504) then RNE; NaN stays NaN
+__device__ __forceinline__ uint32_t f16x2_sat(float lo_v, float hi_v) {
+  uint32_t r;
+  asm("cvt.rn.satfinite.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi_v), "f"(lo_v));
+  return r;
+}
+
+// 16 consecutive channels of one pixel -> one consumer format (vectorised when the
+// run is complete and aligned, element-wise otherwise)
+__device__ __forceinline__ void store16(const OutDev& od, int64_t pix, int c0, const float (&y)[16], int n_live) {
+  const int64_t off = pix * od.c_stride + od.c_offset + c0;
+  if (n_live == 16 && od.dtype == PMX_I8 && (off & 15) == 0) {
+    *reinterpret_cast<uint4*>(reinterpret_cast<int8_t*>(od.ptr) + off) = quant16(y, od.scale, od.inv);
+  } else if (n_live == 16 && od.dtype == PMX_F16 && (off & 7) == 0) {
+    uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__half*>(od.ptr) + off);
+    dst[0] = make_uint4(f16x2_sat(y[0], y[1]), f16x2_sat(y[2], y[3]), f16x2_sat(y[4], y[5]), f16x2_sat(y[6], y[7]));
+    dst[1] = make_uint4(f16x2_sat(y[8], y[9]), f16x2_sat(y[10], y[11]), f16x2_sat(y[12], y[13]),
+                        f16x2_sat(y[14], y[15]));
+  } else if (n_live == 16 && od.dtype == PMX_F32 && (off & 3) == 0) {
+    float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(od.ptr) + off);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) dst[q] = make_float4(y[4 * q], y[4 * q + 1], y[4 * q + 2], y[4 * q + 3]);
+  } else {
+    for (int j = 0; j < n_live; ++j) store_one(od, pix, c0 + j, y[j]);
+  }
+}
+
 __host__ pmx_status validate_outs(const pmx_out* outs, int n, int c_needed);
 
 }  // namespace pmx

@@ -266,7 +266,7 @@ class CompiledGraph:
             v = self.values[name]
             if self.pfn is not None and name in (self.pfn.name, self.graph.layers[1].name):
                 continue
-            if name in self.head_names or name == self.final_name:
+            if name in self.head_names or (name == self.final_name and not self.head_names):
                 v.need[_F32] = None
             for c in cons.get(name, []):
                 if c.is_weight_layer:
