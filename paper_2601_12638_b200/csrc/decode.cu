@@ -3,10 +3,12 @@
 //
 // Candidates are packed into 64-bit keys (order-preserving f32 logit << 32 |
 // ~index) so that "larger key" == "higher logit, then lower index": the ranking
-// is a pure integer sort, bit-reproducible.  Reduction: CTAs bitonic-sort chunks
-// of 2048 keys in shared memory and keep their top k; repeated until one chunk
-// remains (107,136 anchors -> 53 x k -> 3 x k -> k for the KITTI head).  The
-// final CTA decodes the k boxes with the SECOND delta coder in IEEE f32.
+// is a pure integer sort, bit-reproducible.  A per-frame 2048-bin histogram of the
+// top key bits finds the bin holding the k-th largest logit; only keys at or above
+// it are compacted (a few hundred of 107,136 for the KITTI head), then CTAs
+// bitonic-sort 2048-key chunks and keep their top k, repeated until one chunk
+// remains (empty chunks skip the sort).  The final kernel decodes the k boxes with
+// the SECOND delta coder in IEEE f32.
 #include "pmx_common.cuh"
 
 namespace pmx {
@@ -34,41 +36,113 @@ __device__ __forceinline__ void bitonic_sort_desc(unsigned long long* s) {
   __syncthreads();
 }
 
-// round 0: keys from the cls head map
-__global__ void __launch_bounds__(kThreads) topk_first(const float* __restrict__ heads, int c_stride, int cls_off,
-                                                       int n_anchors, int64_t ncand, int k,
-                                                       unsigned long long* out, int nchunks) {
-  __shared__ unsigned long long s[kChunk];
-  const int b = blockIdx.y;
-  const int64_t base = (int64_t)blockIdx.x * kChunk;
-  for (int t = threadIdx.x; t < kChunk; t += blockDim.x) {
-    const int64_t i = base + t;
-    unsigned long long key = 0ull;
-    if (i < ncand) {
-      const int64_t pix = i / n_anchors;
-      const int a = (int)(i % n_anchors);
-      const float logit = heads[((int64_t)b * (ncand / n_anchors) + pix) * c_stride + cls_off + a];
-      key = ((unsigned long long)f2key(logit) << 32) | (unsigned long long)(0xffffffffu - (uint32_t)i);
-    }
-    s[t] = key;
-  }
-  bitonic_sort_desc(s);
-  unsigned long long* dst = out + ((int64_t)b * nchunks + blockIdx.x) * k;
-  for (int t = threadIdx.x; t < k; t += blockDim.x) dst[t] = s[t];
+// ---- threshold pre-filter: a per-frame histogram of the top 11 key bits (a quarter
+// octave of the logit) locates the bin holding the k-th largest logit; only keys at
+// or above that bin (typically a few hundred of 107k) enter the sorting rounds.
+constexpr int kBins = 2048;
+
+__device__ __forceinline__ unsigned long long cand_key(const float* __restrict__ heads, int c_stride, int cls_off,
+                                                       int n_anchors, int64_t ncand, int b, int64_t i) {
+  const int64_t pix = i / n_anchors;
+  const int a = (int)(i % n_anchors);
+  const float logit = heads[((int64_t)b * (ncand / n_anchors) + pix) * c_stride + cls_off + a];
+  return ((unsigned long long)f2key(logit) << 32) | (unsigned long long)(0xffffffffu - (uint32_t)i);
 }
 
-// later rounds: top-k of chunks of an existing key array [B, n]
-__global__ void __launch_bounds__(kThreads) topk_merge(const unsigned long long* __restrict__ in, int64_t n, int k,
-                                                       unsigned long long* out, int nchunks) {
-  __shared__ unsigned long long s[kChunk];
+__global__ void __launch_bounds__(256) topk_hist(const float* __restrict__ heads, int c_stride, int cls_off,
+                                                 int n_anchors, int64_t ncand, int* hist) {
+  __shared__ int h[kBins];
   const int b = blockIdx.y;
+  for (int t = threadIdx.x; t < kBins; t += blockDim.x) h[t] = 0;
+  __syncthreads();
   const int64_t base = (int64_t)blockIdx.x * kChunk;
   for (int t = threadIdx.x; t < kChunk; t += blockDim.x) {
     const int64_t i = base + t;
-    s[t] = i < n ? in[(int64_t)b * n + i] : 0ull;
+    if (i < ncand) atomicAdd(&h[(int)(cand_key(heads, c_stride, cls_off, n_anchors, ncand, b, i) >> 53)], 1);
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < kBins; t += blockDim.x)
+    if (h[t]) atomicAdd(hist + (int64_t)b * kBins + t, h[t]);
+}
+
+__global__ void __launch_bounds__(kBins / 2) topk_thresh(const int* __restrict__ hist, int k, uint32_t* thresh) {
+  __shared__ int sh[32];
+  const int b = blockIdx.x;
+  // thread t owns bins (from the top) 2t, 2t+1; inclusive scan of counts from the top
+  const int* hb = hist + (int64_t)b * kBins;
+  const int t = threadIdx.x;
+  const int c0 = hb[kBins - 1 - 2 * t], c1 = hb[kBins - 2 - 2 * t];
+  int v = c0 + c1;
+  const int lane = t & 31, wid = t >> 5;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int u = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += u;
+  }
+  if (lane == 31) sh[wid] = v;
+  __syncthreads();
+  if (wid == 0) {
+    int s = sh[lane];
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(0xffffffffu, s, o);
+      if (lane >= o) s += u;
+    }
+    sh[lane] = s;
+  }
+  __syncthreads();
+  const int incl = v + (wid > 0 ? sh[wid - 1] : 0);
+  const int excl = incl - c0 - c1;
+  // the first bin (from the top) whose inclusive count reaches k
+  if (excl < k && excl + c0 >= k) thresh[b] = (uint32_t)(kBins - 1 - 2 * t) << 21;
+  else if (excl + c0 < k && incl >= k) thresh[b] = (uint32_t)(kBins - 2 - 2 * t) << 21;
+  if (t == blockDim.x - 1 && incl < k) thresh[b] = 0u;  // fewer candidates than k: keep all
+}
+
+__global__ void __launch_bounds__(256) topk_compact(const float* __restrict__ heads, int c_stride, int cls_off,
+                                                    int n_anchors, int64_t ncand, const uint32_t* __restrict__ thresh,
+                                                    unsigned long long* buf, int* cnt) {
+  const int b = blockIdx.y;
+  const uint32_t T = thresh[b];
+  const int lane = threadIdx.x & 31;
+  const int64_t base = (int64_t)blockIdx.x * kChunk;
+  for (int t0 = 0; t0 < kChunk; t0 += blockDim.x) {
+    const int64_t i = base + t0 + threadIdx.x;
+    unsigned long long key = 0ull;
+    bool keep = false;
+    if (i < ncand) {
+      key = cand_key(heads, c_stride, cls_off, n_anchors, ncand, b, i);
+      keep = (uint32_t)(key >> 32) >= T;
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, keep);
+    if (!m) continue;
+    int slot = 0;
+    if (lane == 0) slot = atomicAdd(cnt + b, __popc(m));
+    slot = __shfl_sync(0xffffffffu, slot, 0);
+    if (keep) buf[(int64_t)b * ncand + slot + __popc(m & ((1u << lane) - 1u))] = key;
+  }
+}
+
+// sorting rounds: top-k of each 2048-key chunk of a key array [B, n]; entries past
+// the per-frame device count (n_dev) are empty, and all-empty chunks skip the sort
+__global__ void __launch_bounds__(kThreads) topk_merge(const unsigned long long* __restrict__ in, int64_t n,
+                                                       const int* __restrict__ n_dev, int k, unsigned long long* out,
+                                                       int nchunks) {
+  __shared__ unsigned long long s[kChunk];
+  const int b = blockIdx.y;
+  const int64_t base = (int64_t)blockIdx.x * kChunk;
+  const int64_t nb = n_dev ? (int64_t)n_dev[b] : n;
+  unsigned long long* dst = out + ((int64_t)b * nchunks + blockIdx.x) * k;
+  int any = 0;
+  for (int t = threadIdx.x; t < kChunk; t += blockDim.x) {
+    const int64_t i = base + t;
+    const unsigned long long v = (i < nb && i < n) ? in[(int64_t)b * n + i] : 0ull;
+    s[t] = v;
+    any |= v != 0ull;
+  }
+  if (!__syncthreads_or(any)) {
+    for (int t = threadIdx.x; t < k; t += blockDim.x) dst[t] = 0ull;
+    return;
   }
   bitonic_sort_desc(s);
-  unsigned long long* dst = out + ((int64_t)b * nchunks + blockIdx.x) * k;
   for (int t = threadIdx.x; t < k; t += blockDim.x) dst[t] = s[t];
 }
 
@@ -123,11 +197,37 @@ __global__ void decode_kernel(const pmx_anchor_desc d, const unsigned long long*
   dir_label[o] = label;
 }
 
-int64_t rounds_bytes(int32_t batch, int64_t ncand, int k) {
-  // two ping-pong key buffers sized for the first round's output
-  int64_t n1 = ceil_div(ncand, kChunk) * k;
-  return 2 * (int64_t)batch * n1 * 8 + 512;
+struct DecodeWs {
+  unsigned long long *buf0, *buf1, *cand;
+  int* hist;
+  int* cnt;
+  uint32_t* thresh;
+  size_t bytes;
+};
+
+DecodeWs carve_ws(void* base, int32_t batch, int64_t ncand, int k) {
+  // two ping-pong key buffers sized for the first round's output, the compacted
+  // candidate buffer, the per-frame histograms / counts / thresholds
+  const int64_t n1 = ceil_div(ncand, kChunk) * k;
+  char* p = static_cast<char*>(base);
+  DecodeWs w{};
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    void* r = p ? p + off : nullptr;
+    off += (bytes + 255) & ~size_t(255);
+    return r;
+  };
+  w.buf0 = (unsigned long long*)take(sizeof(unsigned long long) * batch * n1);
+  w.buf1 = (unsigned long long*)take(sizeof(unsigned long long) * batch * n1);
+  w.cand = (unsigned long long*)take(sizeof(unsigned long long) * batch * ncand);
+  w.hist = (int*)take(sizeof(int) * batch * kBins);
+  w.cnt = (int*)take(sizeof(int) * batch);
+  w.thresh = (uint32_t*)take(sizeof(uint32_t) * batch);
+  w.bytes = off;
+  return w;
 }
+
+int64_t rounds_bytes(int32_t batch, int64_t ncand, int k) { return (int64_t)carve_ws(nullptr, batch, ncand, k).bytes; }
 
 }  // namespace
 }  // namespace pmx
@@ -158,18 +258,22 @@ pmx_status pmx_decode_topk(const pmx_anchor_desc* desc, int32_t batch, int32_t o
   PMX_REQUIRE(ncand < 0x7fffffff, "too many anchors");
   const size_t need = (size_t)rounds_bytes(batch, ncand, d.k);
   PMX_REQUIRE(ws && ws_bytes >= need, "decode workspace too small");
-  const int64_t n1 = ceil_div(ncand, kChunk) * d.k;
-  unsigned long long* buf0 = static_cast<unsigned long long*>(ws);
-  unsigned long long* buf1 = buf0 + (int64_t)batch * n1;
+  DecodeWs w = carve_ws(ws, batch, ncand, d.k);
+  PMX_CUDA(cudaMemsetAsync(w.hist, 0, sizeof(int) * batch * kBins, stream));
+  PMX_CUDA(cudaMemsetAsync(w.cnt, 0, sizeof(int) * batch, stream));
   int nch = (int)ceil_div(ncand, kChunk);
-  topk_first<<<dim3(nch, batch), kThreads, 0, stream>>>(heads, head_c_stride, cls_off, d.n_anchors, ncand, d.k, buf0,
-                                                        nch);
+  topk_hist<<<dim3(nch, batch), 256, 0, stream>>>(heads, head_c_stride, cls_off, d.n_anchors, ncand, w.hist);
+  topk_thresh<<<batch, kBins / 2, 0, stream>>>(w.hist, d.k, w.thresh);
+  topk_compact<<<dim3(nch, batch), 256, 0, stream>>>(heads, head_c_stride, cls_off, d.n_anchors, ncand, w.thresh,
+                                                     w.cand, w.cnt);
+  // round 1 over the compacted candidates (per-frame count on the device)
+  topk_merge<<<dim3(nch, batch), kThreads, 0, stream>>>(w.cand, ncand, w.cnt, d.k, w.buf0, nch);
   int64_t n = (int64_t)nch * d.k;
-  unsigned long long* cur = buf0;
-  unsigned long long* nxt = buf1;
+  unsigned long long* cur = w.buf0;
+  unsigned long long* nxt = w.buf1;
   while (nch > 1) {
     int nn = (int)ceil_div(n, kChunk);
-    topk_merge<<<dim3(nn, batch), kThreads, 0, stream>>>(cur, n, d.k, nxt, nn);
+    topk_merge<<<dim3(nn, batch), kThreads, 0, stream>>>(cur, n, nullptr, d.k, nxt, nn);
     n = (int64_t)nn * d.k;
     nch = nn;
     unsigned long long* t = cur;

@@ -692,7 +692,7 @@ class CompiledGraph:
                 while chunks > 1:
                     chunks = -(-(chunks * a.k) // 2048)
                     rounds += 1
-                n += rounds + 1
+                n += 3 + rounds + 1  # hist, thresh, compact, sorting rounds, decode
             else:
                 n += 1
         return n
