@@ -263,6 +263,15 @@ pmx_status pmx_decode_topk(const pmx_anchor_desc* desc, int32_t batch, int32_t o
                            float* topk_logit, float* boxes, int32_t* dir_label, void* ws,
                            size_t ws_bytes, pmx_stream_t stream);
 
+/* ------------------------------------------------------------------------
+ * K12 sensitivity-sweep error (BASELINE config 5; SPEC.md:364-372 sweep with the
+ * head-output error as the score): out2[0] += sum((a - b)^2), out2[1] += sum(b^2)
+ * over n f32 values, accumulated in f64 in a fixed order (deterministic:
+ * per-block partials, then one ordered reduction).  ws: >= 2 * 1184 doubles.
+ * ---------------------------------------------------------------------- */
+pmx_status pmx_sq_err(const float* a, const float* b, int64_t n, double* out2, double* ws,
+                      pmx_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -87,6 +87,7 @@ SIGNATURES = {
     "pmx_decode_topk": (I32, [C.POINTER(AnchorDesc), I32, I32, I32, P, I32, I32, I32, I32, P, P, P, P, P, SZ,
                               P]),
     "pmx_zero": (I32, [P, SZ, P]),
+    "pmx_sq_err": (I32, [P, P, I64, P, P, P]),
 }
 
 _LIB = None

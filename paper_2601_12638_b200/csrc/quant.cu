@@ -181,6 +181,49 @@ __global__ void __launch_bounds__(256) cast_out_kernel(const float* __restrict__
   if (keys) block_minmax_commit<256>(lo, hi, keys);
 }
 
+constexpr int kErrBlocks = 8 * kNumSMs;
+
+__global__ void __launch_bounds__(256) sq_err_partial(const float* __restrict__ a, const float* __restrict__ b,
+                                                      int64_t n, double* part) {
+  __shared__ double sh[2][8];
+  double e = 0.0, r = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double d = (double)a[i] - (double)b[i];
+    e += d * d;
+    r += (double)b[i] * (double)b[i];
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    e += __shfl_xor_sync(0xffffffffu, e, o);
+    r += __shfl_xor_sync(0xffffffffu, r, o);
+  }
+  const int wid = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    sh[0][wid] = e;
+    sh[1][wid] = r;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double se = 0.0, sr = 0.0;
+    for (int w = 0; w < 8; ++w) {
+      se += sh[0][w];
+      sr += sh[1][w];
+    }
+    part[2 * blockIdx.x] = se;
+    part[2 * blockIdx.x + 1] = sr;
+  }
+}
+
+__global__ void sq_err_final(const double* __restrict__ part, int nparts, double* out2) {
+  if (threadIdx.x != 0) return;
+  double e = 0.0, r = 0.0;
+  for (int i = 0; i < nparts; ++i) {
+    e += part[2 * i];
+    r += part[2 * i + 1];
+  }
+  out2[0] += e;
+  out2[1] += r;
+}
+
 template <typename T>
 __global__ void upsample2x_kernel(const T* __restrict__ x, int32_t b, int32_t h, int32_t w, int32_t c,
                                   T* __restrict__ out) {
@@ -285,6 +328,15 @@ pmx_status pmx_minmax(const void* x, int64_t n, int32_t dtype, uint32_t* keys, p
   else
     return fail(PMX_ERR_INVALID, "bad dtype");
   return check_launch("pmx_minmax");
+}
+
+pmx_status pmx_sq_err(const float* a, const float* b, int64_t n, double* out2, double* ws, pmx_stream_t stream) {
+  PMX_REQUIRE(n >= 0, "negative length");
+  PMX_REQUIRE(a && b && out2 && ws, "NULL operand");
+  if (n == 0) return PMX_OK;
+  sq_err_partial<<<kErrBlocks, 256, 0, stream>>>(a, b, n, ws);
+  sq_err_final<<<1, 32, 0, stream>>>(ws, kErrBlocks, out2);
+  return check_launch("pmx_sq_err");
 }
 
 pmx_status pmx_cast_out(const float* x, int64_t pixels, int32_t c, const pmx_out* outs, int32_t n_outs,

@@ -55,3 +55,39 @@ def test_two_rank_gather_and_sharding():
     assert t0 == t1 == 2.5
     assert sc0 == sc1 == [[0.0, 0.0], [1.0, 2.0]]
     assert pl0 == [0, 2, 4, 6] and pl1 == [1, 3, 5]
+
+
+def _sweep_worker(rank, world, port, q):
+    from paper_2601_12638_b200.sweep import sharded_plan_sums
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world),
+                      LOCAL_RANK=str(rank))
+    r, w, _ = D.init_from_env("gloo")
+    seen = []
+
+    def run_plans(js):  # plan j -> (err, ref) = (j + 1, 10 * (j + 1)); records which rank ran it
+        seen.extend(js)
+        return np.array([[j + 1.0, 10.0 * (j + 1)] for j in js])
+
+    tot = sharded_plan_sums(23, r, w, None, run_plans)
+    q.put((r, seen, tot.tolist()))
+    torch.distributed.destroy_process_group()
+
+
+def test_two_rank_sweep_sharding():
+    """Config-5 sweep plumbing: 23 single-INT8 plans round-robin over 2 ranks, each plan
+    run exactly once, the gathered (err, ref) sums identical on both ranks."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_sweep_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    (_, s0, t0), (_, s1, t1) = res
+    assert s0 == list(range(0, 23, 2)) and s1 == list(range(1, 23, 2))
+    want = [[j + 1.0, 10.0 * (j + 1)] for j in range(23)]
+    assert t0 == t1 == want

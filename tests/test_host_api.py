@@ -171,3 +171,23 @@ def test_pointpillars_graph_shape():
     cfg = PointPillarsConfig()
     assert cfg.out_grid == (248, 216)
     assert abs(cfg.out_stride[0] - 0.32) < 1e-9
+
+
+def test_sweep_ranking_and_greedy_plans():
+    """Config-5 host logic: most sensitive first, ties to the lower
+    index; greedy candidates are FP16 on the top-i layers over an INT8 base."""
+    from paper_2601_12638_b200.sweep import greedy_candidates, head_error, records, select_topk
+
+    errs = {1: 0.5, 2: 0.9, 3: 0.1, 4: 0.9, 5: 0.7}
+    assert select_topk(errs, 5) == [2, 4, 5, 1, 3]
+    assert select_topk(errs, 2) == [2, 4]
+    with pytest.raises(ValueError):
+        select_topk(errs, 0)
+    with pytest.raises(ValueError):
+        select_topk(errs, 6)
+    cands = greedy_candidates([2, 4, 5], 3)
+    assert [c.label() for c in cands] == ["FP16: 2", "FP16: 2,4", "FP16: 2,4,5"]
+    assert cands[2].resolve(4) is DType.FP16 and cands[2].resolve(1) is DType.INT8
+    assert head_error([4.0, 16.0]) == 0.5 and head_error([1.0, 0.0]) == float("inf")
+    recs = records({"layer_errors": errs, "ranking": select_topk(errs, 5)})
+    assert [(r.layer_index, r.rank) for r in recs] == [(1, 4), (2, 1), (3, 5), (4, 2), (5, 3)]

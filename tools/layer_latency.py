@@ -1,0 +1,87 @@
+"""Per-layer B200 latency table (the analogue of the paper's Table II):
+each engine op of a batch-1, 120k-point frame captured in its own CUDA graph and
+replayed, for the all-FP32, all-FP16 and all-INT8 plans.
+
+    python tools/layer_latency.py [--points 120000] [--reps 200] > profiles/r1_layer_latency.md
+"""
+
+import argparse
+import json
+import sys
+from pathlib import Path
+
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+import paper_2601_12638_b200 as pm  # noqa: E402
+from paper_2601_12638_b200 import _native as N  # noqa: E402
+
+
+def op_times(eng, reps):
+    cg = eng.cg
+    out = {}
+    s = torch.cuda.Stream()
+    for name, fn in cg.ops:
+        with torch.cuda.stream(s):
+            fn(N.stream_ptr(s))
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            fn(N.stream_ptr(s))
+        for _ in range(10):
+            g.replay()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(reps):
+            g.replay()
+        b.record()
+        torch.cuda.synchronize()
+        out[name] = 1e3 * a.elapsed_time(b) / reps
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--points", type=int, default=120000)
+    ap.add_argument("--reps", type=int, default=200)
+    ap.add_argument("--json", action="store_true")
+    args = ap.parse_args()
+    cfg = pm.PointPillarsConfig(max_pillars=16000)
+    graph = pm.build_pointpillars(cfg, seed=0)
+    frame = pm.make_frame(args.points, 5, cfg)
+    stats = pm.calibrate_frames(graph, [pm.make_frame(args.points, 900 + i, cfg, 0.01) for i in range(2)], cfg)
+    names = {l.name: l.index for l in graph.weight_layers}
+    table = {}
+    for label in ("FP32", "FP16", "INT8"):
+        eng = pm.PointPillarsEngine(graph, label, stats if label == "INT8" else None, cfg, batch=1,
+                                    max_points_per_frame=args.points)
+        eng.load_points([frame])
+        eng.run()
+        table[label] = op_times(eng, args.reps)
+    rows = []
+    for op in table["FP32"]:
+        if op.startswith("conv "):
+            lname = op[5:]
+            idx = names.get(lname, "21-23" if "heads" in lname else "")
+        elif op == "pfn":
+            lname, idx = "voxel_encoder.pfn_layers.0.linear (+maxpool+scatter)", 1
+        else:
+            lname, idx = op, ""
+        rows.append((idx, lname, *(table[p].get(op, float("nan")) for p in ("FP32", "FP16", "INT8"))))
+    if args.json:
+        print(json.dumps({"points": args.points, "rows": rows}))
+        return
+    print(f"B200 per-op latency, batch 1, {args.points} points, 16000 pillars (us, CUDA-graph replay of one op)\n")
+    print("| index | layer | FP32 | FP16 | INT8 |")
+    print("|---|---|---|---|---|")
+    tot = [0.0, 0.0, 0.0]
+    for r in rows:
+        print(f"| {r[0]} | {r[1]} | {r[2]:.1f} | {r[3]:.1f} | {r[4]:.1f} |")
+        for i in range(3):
+            tot[i] += r[2 + i]
+    print(f"| | **sum** | **{tot[0]:.1f}** | **{tot[1]:.1f}** | **{tot[2]:.1f}** |")
+
+
+if __name__ == "__main__":
+    main()
