@@ -222,7 +222,8 @@ pmx_status pmx_conv(const pmx_conv_desc* desc, const void* x, const void* w, con
  * 2 = tcgen05 without the halo variant. */
 void pmx_set_conv_backend(int32_t mode);
 /* Debug: when non-NULL, tcgen05 conv launches record per-role clock64 stamps of
- * CTA 0 into buf[8][64] (producer/MMA/epilogue hand-offs). */
+ * CTA 0 into buf[9][64]: rows 0-7 producer/MMA/epilogue hand-offs per tile, row 8
+ * = kernel entry, setup done, resident weights landed, teardown. */
 void pmx_debug_trace(unsigned long long* buf);
 
 /* Stage an f32 [pixels, c] tensor into every consumer format (the precision

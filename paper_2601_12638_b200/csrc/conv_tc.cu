@@ -1,20 +1,22 @@
 // tcgen05 implicit-GEMM conv / deconv / 1x1 for sm_100a (K6, K7, K9, K10).
 //
-// One CTA = one 128 x BN output tile.  Warp-specialised, mbarrier-pipelined:
+// Persistent (grid <= 148, one CTA per SM), warp-specialised, mbarrier-pipelined;
+// every role walks the same static tile sequence (tile = 128 output pixels x BN):
 //   warp 0 (1 thread)  TMA producer: per K-block, one box of the A operand (the
-//                      input, shifted per 3x3 tap -- implicit im2col, padding by TMA
-//                      out-of-bounds zero fill) and one box of B (weights) into a
-//                      swizzled smem stage;
-//   warp 1 (1 thread)  MMA issuer: tcgen05.mma kind::i8 (int8 x int8 -> s32) or
-//                      kind::f16 (f16 x f16 -> f32) into a TMEM accumulator;
-//                      tcgen05.commit frees the stage / signals the epilogue;
-//   warp 2             TMEM allocator;
-//   warps 0-3          epilogue: tcgen05.ld (thread = output pixel row), scale +
-//                      bias (+ unfolded BN) + ReLU, exact requantisation to every
-//                      consumer format, vectorised NHWC stores (concat slices,
-//                      deconv pixel shuffle).
+//                      input shifted per 3x3 tap -- implicit im2col, padding by TMA
+//                      out-of-bounds zero fill) and one box of B (weights); in HALO
+//                      mode one halo box per tile and resident weights instead;
+//   warp 1 (1 thread)  TMEM allocator + MMA issuer: tcgen05.mma kind::i8 (s8 x s8 ->
+//                      s32) or kind::f16 (f16 x f16 -> f32) into one of two TMEM
+//                      accumulators; tcgen05.commit frees the stage / signals the
+//                      epilogue;
+//   warps 2-17         epilogue (4 per TMEM lane quarter): tcgen05.ld (thread =
+//                      output pixel row), scale + bias (+ unfolded BN) + ReLU, exact
+//                      requantisation to every consumer format, vectorised NHWC
+//                      stores (concat slices, deconv pixel shuffle).
 // Stride-2 3x3 convs read the input through four parity-split tensor maps
-// (x[2i+p] -> map p at i), so every tap is a plain tiled box.
+// (x[2i+p] -> map p at i), so every tap is a plain tiled box.  Launched with
+// programmatic dependent launch: the prologue overlaps the previous layer's tail.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -43,20 +45,22 @@ __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
 }
 
-__device__ __forceinline__ bool mbar_try(uint32_t bar, uint32_t parity) {
+// try_wait with a suspend-time hint: a waiting warp sleeps (NANOSLEEP.SYNCS, woken by
+// the barrier's phase flip) instead of spinning on issue slots the epilogue needs
+__device__ __forceinline__ bool mbar_try_sleep(uint32_t bar, uint32_t parity) {
   uint32_t ok;
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
       "selp.u32 %0, 1, 0, p;\n\t}"
       : "=r"(ok)
-      : "r"(bar), "r"(parity)
+      : "r"(bar), "r"(parity), "r"(1000000u)
       : "memory");
   return ok != 0;
 }
 
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-  while (!mbar_try(bar, parity)) {
+  while (!mbar_try_sleep(bar, parity)) {
   }
 }
 
@@ -150,6 +154,8 @@ struct TcParams {
   int tw, th;      // conv output tile (tw * th = 128)
   int tiles_x, tiles_y;
   int m_tiles, n_tiles;  // tile grid (tile t -> m = t / n_tiles, n = t % n_tiles)
+  int tw_shift;          // log2(tw)
+  FastDiv fd_nt, fd_tx, fd_ty, fd_iw, fd_ih, fd_oc, fd_na;  // / n_tiles, tiles_x, tiles_y, in_w, in_h, out_c, nacc
   int oc_shift;          // log2(out_c) when a power of two, else -1 (deconv tap split)
   int st_shift;          // log2(stride) (deconv stride is a power of two)
   int64_t m_total;  // GEMM mode: number of rows (input pixels)
@@ -163,6 +169,7 @@ struct TcParams {
   uint32_t sbo, layout;       // smem descriptor params (same for A and B)
   uint32_t idesc;
   uint32_t tmem_cols;
+  int nacc;  // TMEM accumulator buffers (MMA runs up to nacc tiles ahead of the slowest epilogue warp)
   // HALO mode
   uint32_t halo_tx;     // halo bytes per tile (TMA transaction size)
   uint32_t hp, hw;      // halo pixels, halo row width (pixels)
@@ -208,23 +215,24 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
   const uint32_t b_smem = base + p.stages * p.a_bytes;
   const uint32_t bres = b_smem + p.stages * p.b_bytes;  // HALO: resident weights (1024-aligned)
   const uint32_t bar_base = bres + p.bres_bytes;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + (bar_base - base) + 8 * (2 * p.stages + 5));
-  const uint32_t bfull = bar_base + 8u * (2 * p.stages + 4);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + (bar_base - base) + 8 * (2 * p.stages + 2 * p.nacc + 1));
+  const uint32_t bfull = bar_base + 8u * (2 * p.stages + 2 * p.nacc);
   auto full = [&](int s) { return bar_base + 8u * s; };
   auto empty = [&](int s) { return bar_base + 8u * (p.stages + s); };
   auto tfull = [&](int a) { return bar_base + 8u * (2 * p.stages + a); };
-  auto tempty = [&](int a) { return bar_base + 8u * (2 * p.stages + 2 + a); };
+  auto tempty = [&](int a) { return bar_base + 8u * (2 * p.stages + p.nacc + a); };
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int total = p.m_tiles * p.n_tiles;
   const int nk = p.taps * p.cblocks;
 
   if (threadIdx.x == 0) {
+    PMX_TRACE(8, 0);
     for (int s = 0; s < p.stages; ++s) {
       mbar_init(full(s), 1);
       mbar_init(empty(s), 1);
     }
-    for (int a = 0; a < 2; ++a) {
+    for (int a = 0; a < p.nacc; ++a) {
       mbar_init(tfull(a), 1);
       mbar_init(tempty(a), kEpiWarps);
     }
@@ -241,22 +249,38 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0) PMX_TRACE(8, 1);
+  // Programmatic dependent launch: everything above, the resident-weight TMA and the
+  // epilogue's parameter prefetch only touch data no earlier kernel writes, so they
+  // overlap the previous layer's tail; the activations are read (and the outputs
+  // written) only after griddepcontrol.wait.  The next layer may start launching now.
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (p.mode == MODE_HALO && warp == 0 && lane == 0) {
+    mbar_expect_tx(bfull, p.bres_bytes);
+    for (int kb = 0; kb < nk; ++kb) {
+      const int tap = kb / p.cblocks, cb = kb % p.cblocks;
+      tma_load_2d(bres + kb * p.bblk_bytes, &maps.b, tap * (p.cblocks * p.kc) + cb * p.kc, 0, bfull);
+    }
+  }
+  if (warp >= 2) {
+    const int n0 = (blockIdx.x % p.n_tiles) * p.bn;
+    for (int c = (warp - 2) >> 2; c < p.bn / 16; c += 4) {
+      const int co = n0 + 16 * c < p.out_c ? n0 + 16 * c : 0;
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(p.bias + co));
+      if (p.alpha) asm volatile("prefetch.global.L1 [%0];" ::"l"(p.alpha + co));
+    }
+  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 
   if (warp == 0) {
     if (lane == 0) {
       // ---------------- TMA producer
       uint32_t it = 0;
       if (p.mode == MODE_HALO) {
-        mbar_expect_tx(bfull, p.bres_bytes);
-        for (int kb = 0; kb < nk; ++kb) {
-          const int tap = kb / p.cblocks, cb = kb % p.cblocks;
-          tma_load_2d(bres + kb * p.bblk_bytes, &maps.b, tap * (p.cblocks * p.kc) + cb * p.kc, 0, bfull);
-        }
         for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
-          int r = t;
-          const int tx = r % p.tiles_x;
-          r /= p.tiles_x;
-          const int oy0 = (r % p.tiles_y) * p.th, tb = r / p.tiles_y, ox0 = tx * p.tw;
+          const int tq = (int)fdiv((uint32_t)t, p.fd_tx), tx = t - tq * p.tiles_x;
+          const int tb = (int)fdiv((uint32_t)tq, p.fd_ty);
+          const int oy0 = (tq - tb * p.tiles_y) * p.th, ox0 = tx * p.tw;
           const int s = it % p.stages;
           const uint32_t ph = (it / p.stages) & 1;
           PMX_TRACE(0, it);
@@ -279,15 +303,13 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
         }
       }
       for (int t = blockIdx.x; t < total && p.mode != MODE_HALO; t += gridDim.x) {
-        const int mt = t / p.n_tiles, nt = t % p.n_tiles;
+        const int mt = (int)fdiv((uint32_t)t, p.fd_nt), nt = t - mt * p.n_tiles;
         const int n0 = nt * p.bn;
         int tb = 0, oy0 = 0, ox0 = 0, m0 = 0;
         if (p.mode == MODE_CONV3) {
-          int r = mt;
-          const int tx = r % p.tiles_x;
-          r /= p.tiles_x;
-          oy0 = (r % p.tiles_y) * p.th;
-          tb = r / p.tiles_y;
+          const int tq = (int)fdiv((uint32_t)mt, p.fd_tx), tx = mt - tq * p.tiles_x;
+          tb = (int)fdiv((uint32_t)tq, p.fd_ty);
+          oy0 = (tq - tb * p.tiles_y) * p.th;
           ox0 = tx * p.tw;
         } else {
           m0 = mt * 128;
@@ -331,8 +353,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
         const uint32_t bblk = p.bblk_bytes;
         mbar_wait(bfull, 0);
         tc_fence_after();
+        PMX_TRACE(8, 2);
         for (int t = blockIdx.x; t < total; t += gridDim.x, ++i, ++it) {
-          const uint32_t acc = i & 1, aph = (i >> 1) & 1;
+          const uint32_t aq = fdiv(i, p.fd_na), acc = i - aq * (uint32_t)p.nacc, aph = aq & 1;
           mbar_wait(tempty(acc), aph ^ 1);
           tc_fence_after();
           const uint32_t d = tmem + acc * bn;
@@ -369,7 +392,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
         }
       } else {
         for (int t = blockIdx.x; t < total; t += gridDim.x, ++i) {
-          const uint32_t acc = i & 1, aph = (i >> 1) & 1;
+          const uint32_t aq = fdiv(i, p.fd_na), acc = i - aq * (uint32_t)p.nacc, aph = aq & 1;
           mbar_wait(tempty(acc), aph ^ 1);
           tc_fence_after();
           const uint32_t d = tmem + acc * bn;
@@ -405,35 +428,34 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
     float lo = __int_as_float(0x7f800000), hi = -lo;
     uint32_t i = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x, ++i) {
-      const uint32_t acc = i & 1, aph = (i >> 1) & 1;
-      const int mt = t / p.n_tiles, nt = t % p.n_tiles;
-      const int n0 = nt * p.bn;
+      const uint32_t aq = fdiv(i, p.fd_na), acc = i - aq * (uint32_t)p.nacc, aph = aq & 1;
+      const uint32_t mt = fdiv((uint32_t)t, p.fd_nt), nt = (uint32_t)t - mt * (uint32_t)p.n_tiles;
+      const int n0 = (int)nt * p.bn;
       bool valid;
       uint32_t pix_in;  // < 2^31 (checked on the host)
       uint32_t iy = 0, ix = 0, ib = 0;
       if (p.mode != MODE_GEMM) {
-        uint32_t r = (uint32_t)mt;
-        const uint32_t tx = r % (uint32_t)p.tiles_x;
-        r /= (uint32_t)p.tiles_x;
-        const uint32_t oy = (r % (uint32_t)p.tiles_y) * p.th + row / p.tw;
-        const uint32_t tb = r / (uint32_t)p.tiles_y;
-        const uint32_t ox = tx * p.tw + row % p.tw;
+        const uint32_t tq = fdiv(mt, p.fd_tx), tx = mt - tq * (uint32_t)p.tiles_x;
+        const uint32_t tb = fdiv(tq, p.fd_ty), ty = tq - tb * (uint32_t)p.tiles_y;
+        const uint32_t oy = ty * p.th + ((uint32_t)row >> p.tw_shift);
+        const uint32_t ox = tx * p.tw + ((uint32_t)row & (uint32_t)(p.tw - 1));
         valid = oy < (uint32_t)p.out_h && ox < (uint32_t)p.out_w;
         pix_in = (tb * p.out_h + oy) * p.out_w + ox;
       } else {
-        pix_in = (uint32_t)mt * 128u + row;
+        pix_in = mt * 128u + row;
         valid = pix_in < (uint32_t)p.m_total;
         if (p.deconv) {
-          ix = pix_in % (uint32_t)p.in_w;
-          const uint32_t tt = pix_in / (uint32_t)p.in_w;
-          iy = tt % (uint32_t)p.in_h;
-          ib = tt / (uint32_t)p.in_h;
+          const uint32_t tt = fdiv(pix_in, p.fd_iw);
+          ix = pix_in - tt * (uint32_t)p.in_w;
+          ib = fdiv(tt, p.fd_ih);
+          iy = tt - ib * (uint32_t)p.in_h;
         }
       }
       if (warp == 2 && lane == 0) PMX_TRACE(5, i);
       mbar_wait(tfull(acc), aph);
       tc_fence_after();
       if (warp == 2 && lane == 0) PMX_TRACE(6, i);
+      if (lane == 0 && i == 6) PMX_TRACE(8, 8 + 2 * (warp - 2));  // per-warp view of one steady-state tile
       const uint32_t trow = tmem + acc * (uint32_t)p.bn + ((uint32_t)(q * 32) << 16);
       for (int c = g; c < nchunks; c += 4) {
         uint32_t v[16];
@@ -449,7 +471,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
             tap = nbase >> p.oc_shift;
             cobase = nbase & (p.out_c - 1);
           } else {
-            tap = nbase / p.out_c;
+            tap = (int)fdiv((uint32_t)nbase, p.fd_oc);
             cobase = nbase - tap * p.out_c;
           }
           const uint32_t ddy = (uint32_t)tap >> p.st_shift, ddx = (uint32_t)tap & (uint32_t)(p.stride - 1);
@@ -488,6 +510,16 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
               if constexpr (DT == PMX_I8) y[j] = __fmaf_rn((float)(int)v[j], p.alpha[co], p.bias[co]);
               else y[j] = __fadd_rn(__uint_as_float(v[j]), p.bias[co]);
             }
+          }
+        }
+        if constexpr (OUTK == 1) {
+          // single int8 consumer, 16-byte aligned rows (checked on the host); the
+          // ReLU folds into the quantizer's lower clamp
+          if (full16 && !p.bn_post && !p.keys) {
+            const OutDev& od = outs.o[0];
+            *reinterpret_cast<uint4*>(reinterpret_cast<int8_t*>(od.ptr) + (size_t)pix * od.c_stride + od.c_offset +
+                                      cobase) = quant16(y, od.scale, od.inv, p.relu ? 0.0f : -128.0f);
+            continue;
           }
         }
         if (p.bn_post) {
@@ -552,11 +584,13 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
       __syncwarp();
       if (lane == 0) mbar_arrive(tempty(acc));
       if (warp == 2 && lane == 0) PMX_TRACE(7, i);
+      if (lane == 0 && i == 6) PMX_TRACE(8, 9 + 2 * (warp - 2));
     }
     if (p.keys) block_minmax_commit<kThreads>(lo, hi, p.keys);
   }
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) PMX_TRACE(8, 3);
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(p.tmem_cols) : "memory");
@@ -564,6 +598,15 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
 }
 
 // ------------------------------------------------------------------ host side
+
+// programmatic dependent launch on the tcgen05 convs (PMX_PDL=0 turns it off for A/B runs)
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("PMX_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 std::once_flag g_encode_once;
@@ -660,6 +703,9 @@ Plan plan_for(const pmx_conv_desc& d) {
   // N tile: the whole GEMM N up to 256 (the A tile is then read once); TMEM holds two
   int bn = (int)(ceil_div(p.n_gemm, 16) * 16);
   if (bn > 256) bn = 256;
+  // small M (batch-1 blocks.2: 27 M tiles): split N while the tile count still fits
+  // one wave -- each CTA then streams a quarter of the weights and issues N=64 MMAs
+  while (bn > 64 && bn % 32 == 0 && (int64_t)p.m_tiles * ceil_div(p.n_gemm, bn / 2) <= kNumSMs) bn /= 2;
   p.bn = bn;
   p.n_tiles = (int)ceil_div(p.n_gemm, bn);
   const int64_t tiles = (int64_t)p.m_tiles * p.n_tiles;
@@ -703,14 +749,25 @@ Plan plan_for(const pmx_conv_desc& d) {
       p.bres_bytes = bres_total;
     }
   }
-  const int cols = 2 * bn;  // double-buffered accumulator
+  p.tw_shift = p.tw > 0 ? __builtin_ctz((unsigned)p.tw) : 0;
+  p.fd_nt = make_fastdiv((uint32_t)p.n_tiles);
+  p.fd_tx = make_fastdiv((uint32_t)(p.tiles_x > 0 ? p.tiles_x : 1));
+  p.fd_ty = make_fastdiv((uint32_t)(p.tiles_y > 0 ? p.tiles_y : 1));
+  p.fd_iw = make_fastdiv((uint32_t)d.in_w);
+  p.fd_ih = make_fastdiv((uint32_t)d.in_h);
+  p.fd_oc = make_fastdiv((uint32_t)d.out_c);
+  // as many TMEM accumulators as fit (2..8): the MMA warp runs ahead of a slow epilogue warp
+  p.nacc = 512 / bn < 8 ? 512 / bn : 8;
+  if (p.nacc < 2) p.nacc = 2;
+  p.fd_na = make_fastdiv((uint32_t)p.nacc);
+  const int cols = p.nacc * bn;
   p.tmem_cols = cols <= 32 ? 32 : (cols <= 64 ? 64 : (cols <= 128 ? 128 : (cols <= 256 ? 256 : 512)));
   const uint32_t m_enc = 128u >> 4, n_enc = (uint32_t)bn >> 3;
   if (d.in_dtype == PMX_I8)
     p.idesc = (2u << 4) | (1u << 7) | (1u << 10) | (n_enc << 17) | (m_enc << 24);
   else
     p.idesc = (1u << 4) | (0u << 7) | (0u << 10) | (n_enc << 17) | (m_enc << 24);
-  pl.smem = 1024 + (size_t)p.stages * (p.a_bytes + p.b_bytes) + p.bres_bytes + (2 * p.stages + 5) * 8 + 16;
+  pl.smem = 1024 + (size_t)p.stages * (p.a_bytes + p.b_bytes) + p.bres_bytes + (2 * p.stages + 2 * p.nacc + 1) * 8 + 16;
   pl.ok = true;
   return pl;
 }
@@ -812,7 +869,17 @@ pmx_status conv_tc_try(const pmx_conv_desc& d, const void* x, const void* w, con
                       outs.o[0].c_offset % 16 == 0 && (reinterpret_cast<uintptr_t>(outs.o[0].ptr) & 15) == 0;
   auto launch = [&](auto kern) -> pmx_status {
     PMX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
-    kern<<<grid, kThreads, pl.smem, st>>>(maps, pl.p, outs);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = pl.smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    PMX_CUDA(cudaLaunchKernelEx(&cfg, kern, maps, pl.p, outs));
     return PMX_OK;
   };
   const int kcb = (int)(pl.p.sbo / 8);  // K-block bytes (64 or 128)

@@ -3,25 +3,32 @@
 //
 // Candidates are packed into 64-bit keys (order-preserving f32 logit << 32 |
 // ~index) so that "larger key" == "higher logit, then lower index": the ranking
-// is a pure integer sort, bit-reproducible.  A per-frame 2048-bin histogram of the
-// top key bits finds the bin holding the k-th largest logit; only keys at or above
-// it are compacted (a few hundred of 107,136 for the KITTI head), then CTAs
-// bitonic-sort 2048-key chunks and keep their top k, repeated until one chunk
-// remains (empty chunks skip the sort).  The final kernel decodes the k boxes with
-// the SECOND delta coder in IEEE f32.
+// is a pure integer sort, bit-reproducible.  Two kernels per call:
+//   1. topk_hist: per-frame 2048-bin histogram of the top 11 key bits (a quarter
+//      octave of the logit); the last CTA of each frame (arrival counter) scans it
+//      and stores the bin holding the k-th largest key;
+//   2. topk_select: keys at or above that bin (typically a few hundred of 107,136
+//      for the KITTI head) are appended to a candidate list; the last CTA of each
+//      frame bitonic-sorts the candidates in shared memory (or, when more than
+//      kCap survive, finds the exact k-th key by an 8-pass MSD radix select over
+//      the list first) and decodes the top k boxes with the SECOND delta coder in
+//      IEEE f32.
 #include "pmx_common.cuh"
 
 namespace pmx {
 namespace {
 
-constexpr int kChunk = 2048;
+constexpr int kChunk = 2048;  // anchors per CTA
 constexpr int kThreads = 1024;
+constexpr int kCap = 4096;    // candidates sorted in shared memory
 
-__device__ __forceinline__ void bitonic_sort_desc(unsigned long long* s) {
-  for (int size = 2; size <= kChunk; size <<= 1) {
+template <int N>
+__device__ __forceinline__ void bitonic_sort_desc(unsigned long long* s, int n) {
+  // n: power of two <= N
+  for (int size = 2; size <= n; size <<= 1) {
     for (int stride = size >> 1; stride > 0; stride >>= 1) {
       __syncthreads();
-      for (int t = threadIdx.x; t < kChunk / 2; t += blockDim.x) {
+      for (int t = threadIdx.x; t < n / 2; t += blockDim.x) {
         const int lo = 2 * t - (t & (stride - 1));
         const int hi = lo + stride;
         const bool desc = ((lo & size) == 0);
@@ -36,9 +43,6 @@ __device__ __forceinline__ void bitonic_sort_desc(unsigned long long* s) {
   __syncthreads();
 }
 
-// ---- threshold pre-filter: a per-frame histogram of the top 11 key bits (a quarter
-// octave of the logit) locates the bin holding the k-th largest logit; only keys at
-// or above that bin (typically a few hundred of 107k) enter the sorting rounds.
 constexpr int kBins = 2048;
 
 __device__ __forceinline__ unsigned long long cand_key(const float* __restrict__ heads, int c_stride, int cls_off,
@@ -49,9 +53,22 @@ __device__ __forceinline__ unsigned long long cand_key(const float* __restrict__
   return ((unsigned long long)f2key(logit) << 32) | (unsigned long long)(0xffffffffu - (uint32_t)i);
 }
 
-__global__ void __launch_bounds__(256) topk_hist(const float* __restrict__ heads, int c_stride, int cls_off,
-                                                 int n_anchors, int64_t ncand, int* hist) {
+// last CTA of frame b to arrive on counter *ctr (all its global writes fenced)
+__device__ __forceinline__ bool last_arrival(int* ctr, int n_ctas) {
+  __shared__ int last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(ctr, 1) == n_ctas - 1;
+  __syncthreads();
+  if (last) __threadfence();
+  return last;
+}
+
+__global__ void __launch_bounds__(kThreads) topk_hist(const float* __restrict__ heads, int c_stride, int cls_off,
+                                                      int n_anchors, int64_t ncand, int k, int* hist, int* arrive,
+                                                      uint32_t* thresh) {
   __shared__ int h[kBins];
+  __shared__ int sh[32];
   const int b = blockIdx.y;
   for (int t = threadIdx.x; t < kBins; t += blockDim.x) h[t] = 0;
   __syncthreads();
@@ -61,17 +78,13 @@ __global__ void __launch_bounds__(256) topk_hist(const float* __restrict__ heads
     if (i < ncand) atomicAdd(&h[(int)(cand_key(heads, c_stride, cls_off, n_anchors, ncand, b, i) >> 53)], 1);
   }
   __syncthreads();
+  int* hb = hist + (int64_t)b * kBins;
   for (int t = threadIdx.x; t < kBins; t += blockDim.x)
-    if (h[t]) atomicAdd(hist + (int64_t)b * kBins + t, h[t]);
-}
-
-__global__ void __launch_bounds__(kBins / 2) topk_thresh(const int* __restrict__ hist, int k, uint32_t* thresh) {
-  __shared__ int sh[32];
-  const int b = blockIdx.x;
+    if (h[t]) atomicAdd(hb + t, h[t]);
+  if (!last_arrival(arrive + b, gridDim.x)) return;
   // thread t owns bins (from the top) 2t, 2t+1; inclusive scan of counts from the top
-  const int* hb = hist + (int64_t)b * kBins;
   const int t = threadIdx.x;
-  const int c0 = hb[kBins - 1 - 2 * t], c1 = hb[kBins - 2 - 2 * t];
+  const int c0 = __ldcg(hb + kBins - 1 - 2 * t), c1 = __ldcg(hb + kBins - 2 - 2 * t);
   int v = c0 + c1;
   const int lane = t & 31, wid = t >> 5;
   for (int o = 1; o < 32; o <<= 1) {
@@ -97,62 +110,9 @@ __global__ void __launch_bounds__(kBins / 2) topk_thresh(const int* __restrict__
   if (t == blockDim.x - 1 && incl < k) thresh[b] = 0u;  // fewer candidates than k: keep all
 }
 
-__global__ void __launch_bounds__(256) topk_compact(const float* __restrict__ heads, int c_stride, int cls_off,
-                                                    int n_anchors, int64_t ncand, const uint32_t* __restrict__ thresh,
-                                                    unsigned long long* buf, int* cnt) {
-  const int b = blockIdx.y;
-  const uint32_t T = thresh[b];
-  const int lane = threadIdx.x & 31;
-  const int64_t base = (int64_t)blockIdx.x * kChunk;
-  for (int t0 = 0; t0 < kChunk; t0 += blockDim.x) {
-    const int64_t i = base + t0 + threadIdx.x;
-    unsigned long long key = 0ull;
-    bool keep = false;
-    if (i < ncand) {
-      key = cand_key(heads, c_stride, cls_off, n_anchors, ncand, b, i);
-      keep = (uint32_t)(key >> 32) >= T;
-    }
-    const unsigned m = __ballot_sync(0xffffffffu, keep);
-    if (!m) continue;
-    int slot = 0;
-    if (lane == 0) slot = atomicAdd(cnt + b, __popc(m));
-    slot = __shfl_sync(0xffffffffu, slot, 0);
-    if (keep) buf[(int64_t)b * ncand + slot + __popc(m & ((1u << lane) - 1u))] = key;
-  }
-}
-
-// sorting rounds: top-k of each 2048-key chunk of a key array [B, n]; entries past
-// the per-frame device count (n_dev) are empty, and all-empty chunks skip the sort
-__global__ void __launch_bounds__(kThreads) topk_merge(const unsigned long long* __restrict__ in, int64_t n,
-                                                       const int* __restrict__ n_dev, int k, unsigned long long* out,
-                                                       int nchunks) {
-  __shared__ unsigned long long s[kChunk];
-  const int b = blockIdx.y;
-  const int64_t base = (int64_t)blockIdx.x * kChunk;
-  const int64_t nb = n_dev ? (int64_t)n_dev[b] : n;
-  unsigned long long* dst = out + ((int64_t)b * nchunks + blockIdx.x) * k;
-  int any = 0;
-  for (int t = threadIdx.x; t < kChunk; t += blockDim.x) {
-    const int64_t i = base + t;
-    const unsigned long long v = (i < nb && i < n) ? in[(int64_t)b * n + i] : 0ull;
-    s[t] = v;
-    any |= v != 0ull;
-  }
-  if (!__syncthreads_or(any)) {
-    for (int t = threadIdx.x; t < k; t += blockDim.x) dst[t] = 0ull;
-    return;
-  }
-  bitonic_sort_desc(s);
-  for (int t = threadIdx.x; t < k; t += blockDim.x) dst[t] = s[t];
-}
-
-__global__ void decode_kernel(const pmx_anchor_desc d, const unsigned long long* __restrict__ keys, int64_t n_in,
-                              int out_h, int out_w, const float* __restrict__ heads, int c_stride, int box_off,
-                              int dir_off, int32_t* topk_idx, float* topk_logit, float* boxes, int32_t* dir_label) {
-  const int b = blockIdx.y;
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= d.k) return;
-  const unsigned long long key = keys[(int64_t)b * n_in + r];
+__device__ void decode_one(const pmx_anchor_desc& d, unsigned long long key, int b, int r, int out_h, int out_w,
+                           const float* __restrict__ heads, int c_stride, int box_off, int dir_off, int32_t* topk_idx,
+                           float* topk_logit, float* boxes, int32_t* dir_label) {
   const int64_t o = (int64_t)b * d.k + r;
   const int64_t ncand = (int64_t)out_h * out_w * d.n_anchors;
   const uint32_t idx = 0xffffffffu - (uint32_t)(key & 0xffffffffull);
@@ -197,18 +157,101 @@ __global__ void decode_kernel(const pmx_anchor_desc d, const unsigned long long*
   dir_label[o] = label;
 }
 
+__global__ void __launch_bounds__(kThreads) topk_select(
+    const pmx_anchor_desc d, const float* __restrict__ heads, int c_stride, int cls_off, int box_off, int dir_off,
+    int out_h, int out_w, const uint32_t* __restrict__ thresh, unsigned long long* cand, int* cnt, int* arrive,
+    int32_t* topk_idx, float* topk_logit, float* boxes, int32_t* dir_label) {
+  __shared__ unsigned long long s[kCap];
+  __shared__ int sh_hist[256];
+  __shared__ int sh_n, sh_sel[2];
+  const int b = blockIdx.y;
+  const int n_anchors = d.n_anchors;
+  const int64_t ncand = (int64_t)out_h * out_w * n_anchors;
+  const uint32_t T = thresh[b];
+  const int lane = threadIdx.x & 31;
+  unsigned long long* cb = cand + (int64_t)b * ncand;
+  const int64_t base = (int64_t)blockIdx.x * kChunk;
+  for (int t0 = 0; t0 < kChunk; t0 += blockDim.x) {
+    const int64_t i = base + t0 + threadIdx.x;
+    unsigned long long key = 0ull;
+    bool keep = false;
+    if (i < ncand) {
+      key = cand_key(heads, c_stride, cls_off, n_anchors, ncand, b, i);
+      keep = (uint32_t)(key >> 32) >= T;
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, keep);
+    if (!m) continue;
+    int slot = 0;
+    if (lane == 0) slot = atomicAdd(cnt + b, __popc(m));
+    slot = __shfl_sync(0xffffffffu, slot, 0);
+    if (keep) cb[slot + __popc(m & ((1u << lane) - 1u))] = key;
+  }
+  if (!last_arrival(arrive + b, gridDim.x)) return;
+
+  // ---- last CTA of the frame: rank the n candidates, decode the top k
+  const int n = __ldcg(cnt + b);
+  const int k = d.k;
+  if (n <= kCap) {
+    int np = 2;
+    while (np < n || np < k) np <<= 1;
+    for (int t = threadIdx.x; t < np; t += blockDim.x) s[t] = t < n ? __ldcg(cb + t) : 0ull;
+    bitonic_sort_desc<kCap>(s, np);
+  } else {
+    // exact k-th largest key by MSD radix select (8 bits per pass); keys are unique
+    unsigned long long prefix = 0ull, mask = 0ull;
+    int kk = k;
+    for (int shift = 56; shift >= 0; shift -= 8) {
+      for (int t = threadIdx.x; t < 256; t += blockDim.x) sh_hist[t] = 0;
+      __syncthreads();
+      for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const unsigned long long key = __ldcg(cb + i);
+        if ((key & mask) == prefix) atomicAdd(&sh_hist[(int)(key >> shift) & 255], 1);
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        int above = 0, bin = 255;
+        for (; bin > 0; --bin) {
+          if (above + sh_hist[bin] >= kk) break;
+          above += sh_hist[bin];
+        }
+        sh_sel[0] = above;
+        sh_sel[1] = bin;
+      }
+      __syncthreads();
+      kk -= sh_sel[0];
+      prefix |= (unsigned long long)sh_sel[1] << shift;
+      mask |= 255ull << shift;
+      __syncthreads();
+    }
+    // prefix == the k-th largest key: gather the k keys >= it, then sort them
+    if (threadIdx.x == 0) sh_n = 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const unsigned long long key = __ldcg(cb + i);
+      if (key >= prefix) s[atomicAdd(&sh_n, 1)] = key;
+    }
+    __syncthreads();
+    int np = 2;
+    while (np < k) np <<= 1;
+    for (int t = k + threadIdx.x; t < np; t += blockDim.x) s[t] = 0ull;
+    bitonic_sort_desc<kCap>(s, np);
+  }
+  for (int r = threadIdx.x; r < k; r += blockDim.x)
+    decode_one(d, s[r], b, r, out_h, out_w, heads, c_stride, box_off, dir_off, topk_idx, topk_logit, boxes,
+               dir_label);
+}
+
 struct DecodeWs {
-  unsigned long long *buf0, *buf1, *cand;
-  int* hist;
-  int* cnt;
+  unsigned long long* cand;
+  int* hist;     // [B, kBins]
+  int* cnt;      // [B]
+  int* arrive;   // [2, B]
   uint32_t* thresh;
+  size_t zero_bytes;  // hist .. arrive are contiguous and zeroed per call
   size_t bytes;
 };
 
-DecodeWs carve_ws(void* base, int32_t batch, int64_t ncand, int k) {
-  // two ping-pong key buffers sized for the first round's output, the compacted
-  // candidate buffer, the per-frame histograms / counts / thresholds
-  const int64_t n1 = ceil_div(ncand, kChunk) * k;
+DecodeWs carve_ws(void* base, int32_t batch, int64_t ncand) {
   char* p = static_cast<char*>(base);
   DecodeWs w{};
   size_t off = 0;
@@ -217,17 +260,16 @@ DecodeWs carve_ws(void* base, int32_t batch, int64_t ncand, int k) {
     off += (bytes + 255) & ~size_t(255);
     return r;
   };
-  w.buf0 = (unsigned long long*)take(sizeof(unsigned long long) * batch * n1);
-  w.buf1 = (unsigned long long*)take(sizeof(unsigned long long) * batch * n1);
   w.cand = (unsigned long long*)take(sizeof(unsigned long long) * batch * ncand);
+  const size_t z0 = off;
   w.hist = (int*)take(sizeof(int) * batch * kBins);
   w.cnt = (int*)take(sizeof(int) * batch);
+  w.arrive = (int*)take(sizeof(int) * 2 * batch);
+  w.zero_bytes = off - z0;
   w.thresh = (uint32_t*)take(sizeof(uint32_t) * batch);
   w.bytes = off;
   return w;
 }
-
-int64_t rounds_bytes(int32_t batch, int64_t ncand, int k) { return (int64_t)carve_ws(nullptr, batch, ncand, k).bytes; }
 
 }  // namespace
 }  // namespace pmx
@@ -238,7 +280,7 @@ extern "C" {
 
 size_t pmx_decode_workspace(const pmx_anchor_desc* desc, int32_t batch, int32_t out_h, int32_t out_w) {
   if (!desc) return 0;
-  return (size_t)rounds_bytes(batch, (int64_t)out_h * out_w * desc->n_anchors, desc->k);
+  return carve_ws(nullptr, batch, (int64_t)out_h * out_w * desc->n_anchors).bytes;
 }
 
 pmx_status pmx_decode_topk(const pmx_anchor_desc* desc, int32_t batch, int32_t out_h, int32_t out_w,
@@ -256,32 +298,15 @@ pmx_status pmx_decode_topk(const pmx_anchor_desc* desc, int32_t batch, int32_t o
   if (batch == 0) return PMX_OK;
   const int64_t ncand = (int64_t)out_h * out_w * d.n_anchors;
   PMX_REQUIRE(ncand < 0x7fffffff, "too many anchors");
-  const size_t need = (size_t)rounds_bytes(batch, ncand, d.k);
-  PMX_REQUIRE(ws && ws_bytes >= need, "decode workspace too small");
-  DecodeWs w = carve_ws(ws, batch, ncand, d.k);
-  PMX_CUDA(cudaMemsetAsync(w.hist, 0, sizeof(int) * batch * kBins, stream));
-  PMX_CUDA(cudaMemsetAsync(w.cnt, 0, sizeof(int) * batch, stream));
-  int nch = (int)ceil_div(ncand, kChunk);
-  topk_hist<<<dim3(nch, batch), 256, 0, stream>>>(heads, head_c_stride, cls_off, d.n_anchors, ncand, w.hist);
-  topk_thresh<<<batch, kBins / 2, 0, stream>>>(w.hist, d.k, w.thresh);
-  topk_compact<<<dim3(nch, batch), 256, 0, stream>>>(heads, head_c_stride, cls_off, d.n_anchors, ncand, w.thresh,
-                                                     w.cand, w.cnt);
-  // round 1 over the compacted candidates (per-frame count on the device)
-  topk_merge<<<dim3(nch, batch), kThreads, 0, stream>>>(w.cand, ncand, w.cnt, d.k, w.buf0, nch);
-  int64_t n = (int64_t)nch * d.k;
-  unsigned long long* cur = w.buf0;
-  unsigned long long* nxt = w.buf1;
-  while (nch > 1) {
-    int nn = (int)ceil_div(n, kChunk);
-    topk_merge<<<dim3(nn, batch), kThreads, 0, stream>>>(cur, n, nullptr, d.k, nxt, nn);
-    n = (int64_t)nn * d.k;
-    nch = nn;
-    unsigned long long* t = cur;
-    cur = nxt;
-    nxt = t;
-  }
-  decode_kernel<<<dim3((unsigned)ceil_div(d.k, 128), batch), 128, 0, stream>>>(
-      d, cur, n, out_h, out_w, heads, head_c_stride, box_off, dir_off, topk_idx, topk_logit, boxes, dir_label);
+  DecodeWs w = carve_ws(ws, batch, ncand);
+  PMX_REQUIRE(ws && ws_bytes >= w.bytes, "decode workspace too small");
+  PMX_CUDA(cudaMemsetAsync(w.hist, 0, w.zero_bytes, stream));
+  const int nch = (int)ceil_div(ncand, kChunk);
+  topk_hist<<<dim3(nch, batch), kThreads, 0, stream>>>(heads, head_c_stride, cls_off, d.n_anchors, ncand, d.k,
+                                                        w.hist, w.arrive, w.thresh);
+  topk_select<<<dim3(nch, batch), kThreads, 0, stream>>>(d, heads, head_c_stride, cls_off, box_off, dir_off, out_h,
+                                                          out_w, w.thresh, w.cand, w.cnt, w.arrive + batch, topk_idx,
+                                                          topk_logit, boxes, dir_label);
   return check_launch("pmx_decode_topk");
 }
 

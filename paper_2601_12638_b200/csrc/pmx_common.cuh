@@ -40,7 +40,7 @@ constexpr int kNumSMs = 148;
 // exact quantize: clip(rint(f64(x) / scale), -128, 127)   (pm/quant.py:98-103)
 //
 // q = x * inv (f32) has relative error < 2^-22, i.e. absolute error < 4e-5 for
-// |q| < 129, so rint(q) equals rint(x / scale) unless q lies within 1e-3 of a
+// |q| < 129, so rint(q) equals rint(x / scale) unless q lies within 1e-4 of a
 // half-integer; there the IEEE f64 divide decides (the reference's own op).
 
 struct QScale {
@@ -59,7 +59,7 @@ __device__ __forceinline__ int quantize_exact(float x, double s, float inv) {
   }
   float r = rintf(q);
   float d = fabsf(__fsub_rn(q, r));
-  if (fabsf(d - 0.5f) < 1e-3f) {
+  if (fabsf(d - 0.5f) < 1e-4f) {
     double e = __ddiv_rn((double)x, s);
     r = (float)rint(e);
   }
@@ -67,15 +67,53 @@ __device__ __forceinline__ int quantize_exact(float x, double s, float inv) {
   return c < -128 ? -128 : (c > 127 ? 127 : c);
 }
 
-// Same result as quantize_exact with a short common path: away from ties
-// (|frac - .5| >= 1e-3) and inside |q| < 127 the f32 estimate is already exact and
-// needs no clamp; everything else (ties, saturation, NaN) takes the exact path.
+// |frac(q) - .5| guard band.  q = RN(x * RN(1/s)) is within 2^-23 relative of x / s,
+// i.e. within 1.6e-5 absolute for |q| < 128, so outside a 1e-4 band around the .5
+// ties RN(q) already equals rint(x / s) and only values inside the band need the
+// f64 divide of quantize_exact (pm/quant.py:100).
+constexpr float kTieBand = 0.4999f;
+
+// Same result as quantize_exact with a short common path: away from ties and inside
+// |q| < 127 the f32 estimate is already exact and needs no clamp; everything else
+// (ties, saturation, NaN) takes the exact path.
 __device__ __forceinline__ int quantize_fast(float x, double s, float inv) {
   const float q = __fmul_rn(x, inv);
   const float r = rintf(q);
-  if (fabsf(__fsub_rn(q, r)) < 0.499f && fabsf(q) < 127.0f) return (int)r;
+  if (fabsf(__fsub_rn(q, r)) < kTieBand && fabsf(q) < 127.0f) return (int)r;
   return quantize_exact(x, s, inv);
 }
+
+// NaN-propagating min / max (PTX max.NaN: FMNMX.NAN; the 3-input form is FMNMX3)
+__device__ __forceinline__ float fmax_nan(float a, float b) {
+  float r;
+  asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float fmin_nan(float a, float b) {
+  float r;
+  asm("min.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float fmax3_nan(float a, float b, float c) {
+  float r;
+  asm("max.NaN.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+
+// unsigned division by a runtime constant for numerators < 2^31:
+// q = (umulhi(n, m) + n) >> s with s = ceil(log2 d), m = 2^32 (2^s - d) / d + 1
+struct FastDiv {
+  uint32_t d, m, s;
+};
+
+__host__ inline FastDiv make_fastdiv(uint32_t d) {
+  uint32_t s = 0;
+  while ((1ull << s) < d) ++s;
+  const uint64_t m = ((1ull << 32) * ((1ull << s) - d)) / d + 1;
+  return FastDiv{d, (uint32_t)m, s};
+}
+
+__device__ __forceinline__ uint32_t fdiv(uint32_t n, const FastDiv& f) { return (__umulhi(n, f.m) + n) >> f.s; }
 
 // fp16_roundtrip (pm/quant.py:144-147): saturate at +-65504, then RNE.
 __device__ __forceinline__ __half f16_sat(float x) {
@@ -163,28 +201,35 @@ __device__ __forceinline__ void store_all(const Outs& outs, int64_t pix, int c, 
 }
 
 // 16 f32 values -> 16 exact int8 codes (quantize() semantics), packed.  Common
-// path: q = y * inv rounded by the 1.5*2^23 magic add, whose low byte IS the
-// two's-complement code; one predicate per 16 values sends near-ties (|frac-.5|
-// < 1e-3), |q| >= 127 and NaN to the exact f64 path (quantize_exact).
-__device__ __forceinline__ uint4 quant16(const float (&y)[16], double s, float inv) {
+// path: q = y * inv clamped to [lo, 127] with NaN-propagating min/max (exact: clip
+// commutes with rint there, and the .5 ties at 127.5 / -128.5 land on the same code
+// either way; lo = 0 fuses a preceding ReLU since inv > 0), rounded by the 1.5*2^23
+// magic add whose low byte IS the two's-complement code.  One max-reduction of
+// |q - rint(q)| flags the rare tie-band value or NaN; then every value is redone on
+// the exact f64 path.
+__device__ __forceinline__ uint4 quant16(const float (&y)[16], double s, float inv, float lo = -128.0f) {
   // packed f32x2 arithmetic (sm_100): q = y*inv, t = q + M, d = q - (t - M)
   const float2 M2 = make_float2(12582912.0f, 12582912.0f), I2 = make_float2(inv, inv);
   const float2 NEG1 = make_float2(-1.0f, -1.0f);
   uint32_t tb[16];
-  bool good = true;
+  float dmax = 0.0f;
 #pragma unroll
   for (int j = 0; j < 16; j += 2) {
-    const float2 qv = __fmul2_rn(make_float2(y[j], y[j + 1]), I2);
+    float2 qv = __fmul2_rn(make_float2(y[j], y[j + 1]), I2);
+    qv.x = fmin_nan(fmax_nan(qv.x, lo), 127.0f);
+    qv.y = fmin_nan(fmax_nan(qv.y, lo), 127.0f);
     const float2 t = __fadd2_rn(qv, M2);
     const float2 d = __fadd2_rn(qv, __ffma2_rn(t, NEG1, M2));  // q + (M - t), both exact
-    good = good && (fabsf(d.x) < 0.499f) && (fabsf(d.y) < 0.499f) && (fabsf(qv.x) < 127.0f) &&
-           (fabsf(qv.y) < 127.0f);
+    dmax = fmax3_nan(dmax, fabsf(d.x), fabsf(d.y));
     tb[j] = __float_as_uint(t.x);
     tb[j + 1] = __float_as_uint(t.y);
   }
-  if (!good) {
+  if (!(dmax < kTieBand)) {
 #pragma unroll
-    for (int j = 0; j < 16; ++j) tb[j] = (uint32_t)quantize_exact(y[j], s, inv);
+    for (int j = 0; j < 16; ++j) {
+      const float yj = lo == 0.0f ? fmaxf(y[j], 0.0f) : y[j];
+      tb[j] = (uint32_t)quantize_exact(yj, s, inv);
+    }
   }
   return make_uint4(__byte_perm(__byte_perm(tb[0], tb[1], 0x0040), __byte_perm(tb[2], tb[3], 0x0040), 0x5410),
                     __byte_perm(__byte_perm(tb[4], tb[5], 0x0040), __byte_perm(tb[6], tb[7], 0x0040), 0x5410),

@@ -332,8 +332,8 @@ pmx_status pmx_minmax(const void* x, int64_t n, int32_t dtype, uint32_t* keys, p
 
 pmx_status pmx_sq_err(const float* a, const float* b, int64_t n, double* out2, double* ws, pmx_stream_t stream) {
   PMX_REQUIRE(n >= 0, "negative length");
-  PMX_REQUIRE(a && b && out2 && ws, "NULL operand");
   if (n == 0) return PMX_OK;
+  PMX_REQUIRE(a && b && out2 && ws, "NULL operand");
   sq_err_partial<<<kErrBlocks, 256, 0, stream>>>(a, b, n, ws);
   sq_err_final<<<1, 32, 0, stream>>>(ws, kErrBlocks, out2);
   return check_launch("pmx_sq_err");

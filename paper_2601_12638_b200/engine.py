@@ -682,17 +682,9 @@ class CompiledGraph:
         n = 0
         for name, _ in self.ops:
             if name == "pillarize":
-                n += 8
+                n += 9  # bin, flag, thresh, cellcount, cellscan, emit, slot, select_small, select
             elif name == "decode":
-                a = self.anchors
-                B, H, W, _ = self.heads_cat.shape
-                ncand = H * W * len(a.rotations)
-                chunks = -(-ncand // 2048)
-                rounds = 1
-                while chunks > 1:
-                    chunks = -(-(chunks * a.k) // 2048)
-                    rounds += 1
-                n += 3 + rounds + 1  # hist, thresh, compact, sorting rounds, decode
+                n += 2  # topk_hist (+ threshold), topk_select (+ sort, decode)
             else:
                 n += 1
         return n

@@ -27,6 +27,9 @@ CASES = [  # kind, cin, cout, k, stride, (h, w), batch
     ("conv", 384, 2, 1, 1, (11, 13), 1),     # conv_cls
     ("conv", 384, 20, 1, 1, (248, 216), 1),  # fused heads, full size
     ("conv", 64, 64, 3, 2, (496, 432), 1),   # blocks.0.0 full size
+    ("conv", 128, 128, 3, 1, (124, 108), 1), # blocks.1.x full size, batch 1
+    ("conv", 256, 256, 3, 1, (62, 54), 1),   # blocks.2.x full size, batch 1 (N split to 4 x 64)
+    ("deconv", 256, 128, 4, 4, (62, 54), 1), # deblocks.2 full size, batch 1
 ]
 
 

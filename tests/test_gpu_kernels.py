@@ -211,14 +211,21 @@ class _Geom:
         self.dir_offset = spec.dir_offset
 
 
-@pytest.mark.parametrize("H,W,k,ties", [(248, 216, 100, False), (32, 24, 100, True), (8, 6, 200, False)])
+@pytest.mark.parametrize("H,W,k,ties", [(248, 216, 100, False), (32, 24, 100, True), (8, 6, 200, False),
+                                        (248, 216, 512, "const"), (248, 216, 100, "coarse"), (1, 1, 5, False)])
 def test_decode_topk_exact_index_set(pm, H, W, k, ties):
+    """Exact top-k: the shared-memory sort (few survivors of the histogram threshold)
+    and the radix-select path (all 107k logits equal, or > 4096 in the k-th bin)."""
     spec = pm.PointPillarsConfig(topk=k).anchor_spec()
     rng = np.random.default_rng(H * W)
     A = len(spec.rotations)
     cls = rng.normal(size=(A, H, W)).astype(np.float32)
-    if ties:
+    if ties is True:
         cls = np.round(cls * 2) / 2  # many equal logits: ties resolve to the lower index
+    elif ties == "const":
+        cls[:] = 0.25
+    elif ties == "coarse":
+        cls = (3.0 + np.round(cls) / 64).astype(np.float32)  # thousands of keys share the k-th bin
     box = (0.1 * rng.normal(size=(7 * A, H, W))).astype(np.float32)
     dr = rng.normal(size=(2 * A, H, W)).astype(np.float32)
     out = pm.decode_topk(cls, box, dr, spec)

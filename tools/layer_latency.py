@@ -46,21 +46,24 @@ def main():
     ap.add_argument("--points", type=int, default=120000)
     ap.add_argument("--reps", type=int, default=200)
     ap.add_argument("--json", action="store_true")
+    ap.add_argument("--batch", type=int, default=1)
+    ap.add_argument("--plans", default="FP32;FP16;INT8")
     args = ap.parse_args()
     cfg = pm.PointPillarsConfig(max_pillars=16000)
     graph = pm.build_pointpillars(cfg, seed=0)
-    frame = pm.make_frame(args.points, 5, cfg)
+    frames = [pm.make_frame(args.points, 5 + i, cfg) for i in range(args.batch)]
     stats = pm.calibrate_frames(graph, [pm.make_frame(args.points, 900 + i, cfg, 0.01) for i in range(2)], cfg)
     names = {l.name: l.index for l in graph.weight_layers}
     table = {}
-    for label in ("FP32", "FP16", "INT8"):
-        eng = pm.PointPillarsEngine(graph, label, stats if label == "INT8" else None, cfg, batch=1,
-                                    max_points_per_frame=args.points)
-        eng.load_points([frame])
+    plans = args.plans.split(";")
+    for label in plans:
+        eng = pm.PointPillarsEngine(graph, label, stats if label != "FP32" and label != "FP16" else None, cfg,
+                                    batch=args.batch, max_points_per_frame=args.points)
+        eng.load_points(frames)
         eng.run()
         table[label] = op_times(eng, args.reps)
     rows = []
-    for op in table["FP32"]:
+    for op in table[plans[0]]:
         if op.startswith("conv "):
             lname = op[5:]
             idx = names.get(lname, "21-23" if "heads" in lname else "")
@@ -68,19 +71,20 @@ def main():
             lname, idx = "voxel_encoder.pfn_layers.0.linear (+maxpool+scatter)", 1
         else:
             lname, idx = op, ""
-        rows.append((idx, lname, *(table[p].get(op, float("nan")) for p in ("FP32", "FP16", "INT8"))))
+        rows.append((idx, lname, *(table[p].get(op, float("nan")) for p in plans)))
     if args.json:
         print(json.dumps({"points": args.points, "rows": rows}))
         return
-    print(f"B200 per-op latency, batch 1, {args.points} points, 16000 pillars (us, CUDA-graph replay of one op)\n")
-    print("| index | layer | FP32 | FP16 | INT8 |")
-    print("|---|---|---|---|---|")
-    tot = [0.0, 0.0, 0.0]
+    print(f"B200 per-op latency, batch {args.batch}, {args.points} points/frame, 16000 pillars "
+          "(us, CUDA-graph replay of one op)\n")
+    print("| index | layer | " + " | ".join(plans) + " |")
+    print("|---|---|" + "---|" * len(plans))
+    tot = [0.0] * len(plans)
     for r in rows:
-        print(f"| {r[0]} | {r[1]} | {r[2]:.1f} | {r[3]:.1f} | {r[4]:.1f} |")
-        for i in range(3):
+        print(f"| {r[0]} | {r[1]} | " + " | ".join(f"{v:.1f}" for v in r[2:]) + " |")
+        for i in range(len(plans)):
             tot[i] += r[2 + i]
-    print(f"| | **sum** | **{tot[0]:.1f}** | **{tot[1]:.1f}** | **{tot[2]:.1f}** |")
+    print("| | **sum** | " + " | ".join(f"**{t:.1f}**" for t in tot) + " |")
 
 
 if __name__ == "__main__":
