@@ -59,6 +59,21 @@ __device__ __forceinline__ bool mbar_try_sleep(uint32_t bar, uint32_t parity) {
   return ok != 0;
 }
 
+// plain try_wait loop (no suspend-time hint) for the MMA issuer: it must resume the
+// moment an operand stage or accumulator frees up
+__device__ __forceinline__ void mbar_spin(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   while (!mbar_try_sleep(bar, parity)) {
   }
@@ -114,13 +129,34 @@ __device__ __forceinline__ void tc_commit(uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
 }
 
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+// tcgen05.ld of 16 accumulator columns (thread = TMEM lane) WITHOUT waiting; the
+// matching tmem_ld_wait names the destination registers as in/out operands so the
+// compiler cannot read them before the wait
+__device__ __forceinline__ void tmem_ld16_issue(uint32_t taddr, uint32_t (&v)[16]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
       : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
         "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
       : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ void tmem_ld_wait(uint32_t (&v)[16]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]), "+r"(v[6]), "+r"(v[7]),
+                 "+r"(v[8]), "+r"(v[9]), "+r"(v[10]), "+r"(v[11]), "+r"(v[12]), "+r"(v[13]), "+r"(v[14]), "+r"(v[15])
+               :
+               : "memory");
+}
+
+// one lane of a converged warp (the lowest active one)
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(pred)
+      :
+      : "memory");
+  return pred != 0;
 }
 
 // K-major smem operand descriptor (tcgen05 format: version 1 at bit 46, layout at 61).
@@ -155,7 +191,7 @@ struct TcParams {
   int tiles_x, tiles_y;
   int m_tiles, n_tiles;  // tile grid (tile t -> m = t / n_tiles, n = t % n_tiles)
   int tw_shift;          // log2(tw)
-  FastDiv fd_nt, fd_tx, fd_ty, fd_iw, fd_ih, fd_oc, fd_na;  // / n_tiles, tiles_x, tiles_y, in_w, in_h, out_c, nacc
+  FastDiv fd_nt, fd_tx, fd_ty, fd_iw, fd_ih, fd_oc;  // / n_tiles, tiles_x, tiles_y, in_w, in_h, out_c
   int oc_shift;          // log2(out_c) when a power of two, else -1 (deconv tap split)
   int st_shift;          // log2(stride) (deconv stride is a power of two)
   int64_t m_total;  // GEMM mode: number of rows (input pixels)
@@ -169,7 +205,9 @@ struct TcParams {
   uint32_t sbo, layout;       // smem descriptor params (same for A and B)
   uint32_t idesc;
   uint32_t tmem_cols;
-  int nacc;  // TMEM accumulator buffers (MMA runs up to nacc tiles ahead of the slowest epilogue warp)
+  int nacc;        // TMEM accumulator buffers (power of two; MMA runs up to nacc tiles ahead)
+  int nacc_shift;  // log2(nacc)
+  int egroups;     // epilogue tile slots (1, 2 or 4)
   // HALO mode
   uint32_t halo_tx;     // halo bytes per tile (TMA transaction size)
   uint32_t hp, hw;      // halo pixels, halo row width (pixels)
@@ -197,6 +235,114 @@ struct TcMaps {
 constexpr int kEpiWarps = 16;                  // warps 2..17: four per TMEM lane quarter
 constexpr int kThreads = 32 * (2 + kEpiWarps);  // + TMA producer warp + MMA warp
 
+// One chunk (16 accumulator columns of one pixel row): y = acc * alpha + bias (int8)
+// or acc + bias (f16), optional unfolded BN and ReLU, observer min/max, then every
+// consumer format.  alpha / bias come from the shared-memory copies.
+template <int DT, int OUTK>
+__device__ __forceinline__ void epi_chunk(const TcParams& p, const Outs& outs, const uint32_t (&v)[16], uint32_t pix,
+                                          int nbase, int cobase, const float* s_alpha, const float* s_bias, float qlo,
+                                          float& lo, float& hi) {
+  const bool full16 = (nbase + 16) <= p.n_gemm;
+  float y[16];
+  if (full16) {
+    const float4* b4p = reinterpret_cast<const float4*>(s_bias + cobase);
+    const float4* a4p = reinterpret_cast<const float4*>(s_alpha + cobase);
+#pragma unroll
+    for (int j4 = 0; j4 < 4; ++j4) {
+      const float4 b4 = b4p[j4];
+      float2 r0, r1;
+      if constexpr (DT == PMX_I8) {
+        const float4 a4 = a4p[j4];
+        r0 = __ffma2_rn(make_float2((float)(int)v[4 * j4], (float)(int)v[4 * j4 + 1]), make_float2(a4.x, a4.y),
+                        make_float2(b4.x, b4.y));
+        r1 = __ffma2_rn(make_float2((float)(int)v[4 * j4 + 2], (float)(int)v[4 * j4 + 3]), make_float2(a4.z, a4.w),
+                        make_float2(b4.z, b4.w));
+      } else {
+        r0 = __fadd2_rn(make_float2(__uint_as_float(v[4 * j4]), __uint_as_float(v[4 * j4 + 1])),
+                        make_float2(b4.x, b4.y));
+        r1 = __fadd2_rn(make_float2(__uint_as_float(v[4 * j4 + 2]), __uint_as_float(v[4 * j4 + 3])),
+                        make_float2(b4.z, b4.w));
+      }
+      y[4 * j4] = r0.x;
+      y[4 * j4 + 1] = r0.y;
+      y[4 * j4 + 2] = r1.x;
+      y[4 * j4 + 3] = r1.y;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int co = cobase + j;
+      y[j] = 0.f;
+      if ((nbase + j) < p.n_gemm) {
+        if constexpr (DT == PMX_I8) y[j] = __fmaf_rn((float)(int)v[j], s_alpha[co], s_bias[co]);
+        else y[j] = __fadd_rn(__uint_as_float(v[j]), s_bias[co]);
+      }
+    }
+  }
+  if constexpr (OUTK == 1) {
+    // single int8 consumer, 16-byte aligned rows (checked on the host); the ReLU folds
+    // into the quantizer's lower clamp
+    if (full16 && !p.bn_post && !p.keys) {
+      const OutDev& od = outs.o[0];
+      *reinterpret_cast<uint4*>(reinterpret_cast<int8_t*>(od.ptr) + (size_t)pix * od.c_stride + od.c_offset + cobase) =
+          quant16(y, od.scale, od.inv, qlo);
+      return;
+    }
+  }
+  if (p.bn_post) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int co = cobase + j;
+      if ((nbase + j) < p.n_gemm)
+        y[j] = __fadd_rn(__fmul_rn(__fsub_rn(y[j], p.bn_post[co]), p.bn_post[p.out_c + co]), p.bn_post[2 * p.out_c + co]);
+    }
+  }
+  if (p.relu) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) y[j] = fmaxf(y[j], 0.f);
+  }
+  if (p.keys) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+      if ((nbase + j) < p.n_gemm) {
+        lo = nmin(lo, y[j]);
+        hi = nmax(hi, y[j]);
+      }
+  }
+  if constexpr (OUTK == 1) {
+    const OutDev& od = outs.o[0];
+    if (full16) {
+      *reinterpret_cast<uint4*>(reinterpret_cast<int8_t*>(od.ptr) + (size_t)pix * od.c_stride + od.c_offset + cobase) =
+          quant16(y, od.scale, od.inv);
+    } else {
+      for (int j = 0; j < 16; ++j)
+        if (nbase + j < p.n_gemm) store_one(od, pix, cobase + j, y[j]);
+    }
+  } else {
+#pragma unroll
+    for (int o = 0; o < PMX_MAX_OUTS; ++o) {
+      if (o >= outs.n) break;
+      const OutDev& od = outs.o[o];
+      const int64_t off = (int64_t)pix * od.c_stride + od.c_offset + cobase;
+      if (full16 && od.dtype == PMX_I8 && (off & 15) == 0) {
+        *reinterpret_cast<uint4*>(reinterpret_cast<int8_t*>(od.ptr) + off) = quant16(y, od.scale, od.inv);
+      } else if (full16 && od.dtype == PMX_F16 && (off & 7) == 0) {
+        uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__half*>(od.ptr) + off);
+        dst[0] = make_uint4(f16x2_sat(y[0], y[1]), f16x2_sat(y[2], y[3]), f16x2_sat(y[4], y[5]), f16x2_sat(y[6], y[7]));
+        dst[1] = make_uint4(f16x2_sat(y[8], y[9]), f16x2_sat(y[10], y[11]), f16x2_sat(y[12], y[13]),
+                            f16x2_sat(y[14], y[15]));
+      } else if (full16 && od.dtype == PMX_F32 && (off & 3) == 0) {
+        float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(od.ptr) + off);
+#pragma unroll
+        for (int qq = 0; qq < 4; ++qq) dst[qq] = make_float4(y[4 * qq], y[4 * qq + 1], y[4 * qq + 2], y[4 * qq + 3]);
+      } else {
+        for (int j = 0; j < 16; ++j)
+          if (nbase + j < p.n_gemm) store_one(od, pix, cobase + j, y[j]);
+      }
+    }
+  }
+}
+
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
@@ -217,6 +363,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
   const uint32_t bar_base = bres + p.bres_bytes;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + (bar_base - base) + 8 * (2 * p.stages + 2 * p.nacc + 1));
   const uint32_t bfull = bar_base + 8u * (2 * p.stages + 2 * p.nacc);
+  // per-channel alpha / bias copies (16-byte aligned, after the barriers + TMEM slot)
+  float* s_alpha = reinterpret_cast<float*>(gbase + (((bar_base - base) + 8 * (2 * p.stages + 2 * p.nacc + 1) + 4 + 15) & ~15u));
+  float* s_bias = s_alpha + ((p.out_c + 3) & ~3);
   auto full = [&](int s) { return bar_base + 8u * s; };
   auto empty = [&](int s) { return bar_base + 8u * (p.stages + s); };
   auto tfull = [&](int a) { return bar_base + 8u * (2 * p.stages + a); };
@@ -234,7 +383,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
     }
     for (int a = 0; a < p.nacc; ++a) {
       mbar_init(tfull(a), 1);
-      mbar_init(tempty(a), kEpiWarps);
+      mbar_init(tempty(a), 4 * (4 / p.egroups));  // the warps draining one tile
     }
     mbar_init(bfull, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -275,14 +424,12 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
   if (warp == 0) {
     if (lane == 0) {
       // ---------------- TMA producer
-      uint32_t it = 0;
+      uint32_t it = 0, s = 0, ph = 0;  // ring position, slot, phase
       if (p.mode == MODE_HALO) {
         for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
           const int tq = (int)fdiv((uint32_t)t, p.fd_tx), tx = t - tq * p.tiles_x;
           const int tb = (int)fdiv((uint32_t)tq, p.fd_ty);
           const int oy0 = (tq - tb * p.tiles_y) * p.th, ox0 = tx * p.tw;
-          const int s = it % p.stages;
-          const uint32_t ph = (it / p.stages) & 1;
           PMX_TRACE(0, it);
           mbar_wait(empty(s), ph ^ 1);
           mbar_expect_tx(full(s), p.halo_tx);
@@ -300,6 +447,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
             }
           }
           PMX_TRACE(1, it);
+          if (++s == (uint32_t)p.stages) s = 0, ph ^= 1;
         }
       }
       for (int t = blockIdx.x; t < total && p.mode != MODE_HALO; t += gridDim.x) {
@@ -315,8 +463,6 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
           m0 = mt * 128;
         }
         for (int kb = 0; kb < nk; ++kb, ++it) {
-          const int s = it % p.stages;
-          const uint32_t ph = (it / p.stages) & 1;
           mbar_wait(empty(s), ph ^ 1);
           mbar_expect_tx(full(s), p.a_bytes + p.b_bytes);
           const int tap = kb / p.cblocks, cb = kb % p.cblocks;
@@ -335,54 +481,59 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
             tma_load_2d(adst, &maps.a[0], c0, m0, full(s));
           }
           tma_load_2d(bdst, &maps.b, tap * (p.cblocks * p.kc) + c0, n0, full(s));
+          if (++s == (uint32_t)p.stages) s = 0, ph ^= 1;
         }
       }
     }
     __syncwarp();
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ---------------- MMA issuer (descriptor high words hoisted; only the start
-      // address changes per instruction -- the issue path is ~50 cycles/MMA)
-      constexpr int ksteps = KCB / 32;  // 32 bytes of K per instruction
-      const uint32_t idesc = p.idesc;
-      const uint32_t bn = (uint32_t)p.bn;
-      const uint64_t dsw = sdesc(0, p.sbo, p.layout);  // swizzled operands (address field 0)
-      uint32_t it = 0, i = 0;
-      if constexpr (CINB > 0) {
-        constexpr int CB = CINB / KCB;
-        const uint32_t bblk = p.bblk_bytes;
-        mbar_wait(bfull, 0);
+    // ---------------- MMA issuer.  The whole warp walks the loop (barrier waits are
+    // warp-wide, so the descriptors stay in uniform registers) and one elected lane
+    // issues.  Descriptor words: hi = SBO | version | layout (constant), lo = LBO << 16
+    // | (address >> 4); the address is always < 256 KB, so every operand's lo word is
+    // one uniform add of a compile-time constant to the stage base -- the issue path
+    // is ~2 instructions per MMA and never starves behind the epilogue warps.
+    const uint32_t idesc = p.idesc;
+    const uint32_t bn = (uint32_t)p.bn;
+    uint32_t i = 0;
+    if constexpr (CINB > 0) {
+      constexpr int CB = CINB / KCB;
+      const uint32_t bblk = p.bblk_bytes;
+      const uint32_t b_hi = (uint32_t)(sdesc(0, p.sbo, p.layout) >> 32), b_lo0 = (uint32_t)sdesc(bres, p.sbo, p.layout);
+      mbar_wait(bfull, 0);
+      tc_fence_after();
+      if (lane == 0) PMX_TRACE(8, 2);
+      uint32_t s = 0, ph = 0, acc = 0, aph = 0;  // smem stage / accumulator and their phases
+      for (int t = blockIdx.x; t < total; t += gridDim.x, ++i) {
+        if (lane == 0) PMX_TRACE(9, i);
+        mbar_spin(tempty(acc), aph ^ 1);
         tc_fence_after();
-        PMX_TRACE(8, 2);
-        for (int t = blockIdx.x; t < total; t += gridDim.x, ++i, ++it) {
-          const uint32_t aq = fdiv(i, p.fd_na), acc = i - aq * (uint32_t)p.nacc, aph = aq & 1;
-          mbar_wait(tempty(acc), aph ^ 1);
-          tc_fence_after();
-          const uint32_t d = tmem + acc * bn;
-          const int s = it % p.stages;
-          PMX_TRACE(2, i);
-          mbar_wait(full(s), (it / p.stages) & 1);
-          tc_fence_after();
+        const uint32_t d = tmem + acc * bn;
+        if (lane == 0) PMX_TRACE(2, i);
+        mbar_spin(full(s), ph);
+        tc_fence_after();
+        if (elect_one()) {
           PMX_TRACE(3, i);
-          const uint32_t abase = a_smem + s * p.a_bytes;
+          const uint32_t alo = (a_smem + s * p.a_bytes) >> 4;
 #pragma unroll
           for (int tap = 0; tap < 9; ++tap) {
             // A operand of this tap inside the halo: plane base, pixel offset, row width
             const int dy = tap / 3 - 1, dx = tap % 3 - 1;
             const int py = HS == 2 ? (dy != 0) : 0, px = HS == 2 ? (dx != 0) : 0;
-            const int HW = HS == 2 ? 8 + px : 10;              // halo row width (pixels)
-            const int HPX = HS == 2 ? (16 + py) * HW : 180;    // pixels in this plane
+            const int HW = HS == 2 ? 8 + px : 10;            // halo row width (pixels)
+            const int HPX = HS == 2 ? (16 + py) * HW : 180;  // pixels in this plane
             const int q = py * 2 + px;
             const int plane_px = HS == 2 ? (q == 0 ? 0 : (q == 1 ? 128 : (q == 2 ? 272 : 408))) : 0;
             const int pix0 = HS == 2 ? (dy == 1) * HW + (dx == 1) : (dy + 1) * HW + (dx + 1);
-            const uint64_t dhalo = sdesc(0, HW * 16u, 0u, HPX * 16u);
+            const uint32_t a_hi = (uint32_t)(HW * 16) >> 4 | (1u << 14);  // SBO | version (layout 0)
+            const uint32_t a_lbo = (uint32_t)(HPX * 16) >> 4;
 #pragma unroll
             for (int k = 0; k < CINB / 32; ++k) {
               // two 16-byte channel groups per instruction (core matrices at +LBO)
               const uint32_t aoff = (uint32_t)(plane_px * CINB + ((2 * k) * HPX + pix0) * 16);
               const uint32_t boff = (uint32_t)((tap * CB + (k * 32) / KCB)) * bblk + (uint32_t)((k * 32) % KCB);
-              const uint64_t ad = dhalo | (uint64_t)(((abase + aoff) & 0x3FFFFu) >> 4);
-              const uint64_t bd = dsw | (uint64_t)(((bres + boff) & 0x3FFFFu) >> 4);
+              const uint64_t ad = ((uint64_t)a_hi << 32) | (alo + ((a_lbo << 16) + (aoff >> 4)));
+              const uint64_t bd = ((uint64_t)b_hi << 32) | (b_lo0 + (boff >> 4));
               tc_mma<DT>(d, ad, bd, idesc, (tap | k) != 0);
             }
           }
@@ -390,46 +541,74 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
           tc_commit(tfull(acc));
           PMX_TRACE(4, i);
         }
-      } else {
-        for (int t = blockIdx.x; t < total; t += gridDim.x, ++i) {
-          const uint32_t aq = fdiv(i, p.fd_na), acc = i - aq * (uint32_t)p.nacc, aph = aq & 1;
-          mbar_wait(tempty(acc), aph ^ 1);
+        __syncwarp();
+        if (++s == (uint32_t)p.stages) s = 0, ph ^= 1;
+        if (++acc == (uint32_t)p.nacc) acc = 0, aph ^= 1;
+      }
+    } else {
+      constexpr int ksteps = KCB / 32;  // 32 bytes of K per instruction
+      const uint32_t hi = (uint32_t)(sdesc(0, p.sbo, p.layout) >> 32), lo0 = (uint32_t)sdesc(0, p.sbo, p.layout);
+      uint32_t s = 0, ph = 0, acc = 0, aph = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x, ++i) {
+        if (lane == 0) PMX_TRACE(9, i);
+        mbar_spin(tempty(acc), aph ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + acc * bn;
+        if (lane == 0) PMX_TRACE(2, i);
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_spin(full(s), ph);
           tc_fence_after();
-          const uint32_t d = tmem + acc * bn;
-          PMX_TRACE(2, i);
-          for (int kb = 0; kb < nk; ++kb, ++it) {
-            const int s = it % p.stages;
-            const uint32_t ph = (it / p.stages) & 1;
-            mbar_wait(full(s), ph);
-            tc_fence_after();
+          if (elect_one()) {
             if (kb == 0) PMX_TRACE(3, i);
-            const uint32_t abase = a_smem + s * p.a_bytes, bbase = b_smem + s * p.b_bytes;
+            const uint32_t alo = lo0 + ((a_smem + s * p.a_bytes) >> 4), blo = lo0 + ((b_smem + s * p.b_bytes) >> 4);
 #pragma unroll
             for (int k = 0; k < ksteps; ++k) {
-              const uint64_t ad = dsw | (uint64_t)(((abase + 32u * k) & 0x3FFFFu) >> 4);
-              const uint64_t bd = dsw | (uint64_t)(((bbase + 32u * k) & 0x3FFFFu) >> 4);
+              const uint64_t ad = ((uint64_t)hi << 32) | (alo + 2u * k);
+              const uint64_t bd = ((uint64_t)hi << 32) | (blo + 2u * k);
               tc_mma<DT>(d, ad, bd, idesc, (kb | k) != 0);
             }
             tc_commit(empty(s));
           }
+          __syncwarp();
+          if (++s == (uint32_t)p.stages) s = 0, ph ^= 1;
+        }
+        if (elect_one()) {
           tc_commit(tfull(acc));
           PMX_TRACE(4, i);
         }
+        __syncwarp();
+        if (++acc == (uint32_t)p.nacc) acc = 0, aph ^= 1;
       }
     }
-    __syncwarp();
   } else {
-    // ---------------- epilogue warps: thread = accumulator row (TMEM lane); four
-    // column groups per lane quarter, chunks of 16 accumulator columns round-robin
-    const int q = warp & 3;          // TMEM lane quarter this warp may access
-    const int g = (warp - 2) >> 2;   // column group 0..3
+    // ---------------- epilogue warps: thread = accumulator row (TMEM lane).  The 16
+    // warps form `egroups` tile slots (consecutive tiles are drained concurrently by
+    // different slots) x 4 / egroups column ranges per tile; a warp owns a contiguous
+    // range of up to 4 chunks of 16 accumulator columns and double-buffers its TMEM
+    // loads.  Per-channel alpha / bias are staged once in shared memory.
+    const int q = warp & 3;         // TMEM lane quarter this warp may access
+    const int e = (warp - 2) >> 2;  // 0..3
+    const int egn = p.egroups, colsplit = 4 / egn;
+    const int eg = e / colsplit, cg = e - eg * colsplit;
     const int row = q * 32 + lane;
     const int nchunks = p.bn / 16;
+    const int cpw = (nchunks + colsplit - 1) / colsplit;
+    const int c_begin = cg * cpw, c_end = min(nchunks, c_begin + cpw);
+    {
+      const int et = threadIdx.x - 64;
+      for (int j = et; j < p.out_c; j += 32 * kEpiWarps) {
+        s_alpha[j] = p.alpha ? p.alpha[j] : 0.0f;
+        s_bias[j] = p.bias[j];
+      }
+      asm volatile("bar.sync 1, %0;" ::"r"(32 * kEpiWarps) : "memory");
+    }
     float lo = __int_as_float(0x7f800000), hi = -lo;
-    uint32_t i = 0;
-    for (int t = blockIdx.x; t < total; t += gridDim.x, ++i) {
-      const uint32_t aq = fdiv(i, p.fd_na), acc = i - aq * (uint32_t)p.nacc, aph = aq & 1;
-      const uint32_t mt = fdiv((uint32_t)t, p.fd_nt), nt = (uint32_t)t - mt * (uint32_t)p.n_tiles;
+    const float qlo = p.relu ? 0.0f : -128.0f;
+    for (uint32_t i = (uint32_t)eg;; i += (uint32_t)egn) {
+      const uint32_t t = blockIdx.x + i * gridDim.x;
+      if (t >= (uint32_t)total) break;
+      const uint32_t acc = i & (uint32_t)(p.nacc - 1), aph = (i >> p.nacc_shift) & 1;
+      const uint32_t mt = fdiv(t, p.fd_nt), nt = t - mt * (uint32_t)p.n_tiles;
       const int n0 = (int)nt * p.bn;
       bool valid;
       uint32_t pix_in;  // < 2^31 (checked on the host)
@@ -457,9 +636,13 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
       if (warp == 2 && lane == 0) PMX_TRACE(6, i);
       if (lane == 0 && i == 6) PMX_TRACE(8, 8 + 2 * (warp - 2));  // per-warp view of one steady-state tile
       const uint32_t trow = tmem + acc * (uint32_t)p.bn + ((uint32_t)(q * 32) << 16);
-      for (int c = g; c < nchunks; c += 4) {
+#pragma unroll 1
+      for (int c = c_begin; c < c_end; ++c) {
+        // 5 warps share one SM sub-partition: 96 registers per thread leave no room
+        // to double-buffer the TMEM loads; the other tile slots hide the latency
         uint32_t v[16];
-        tmem_ld16(trow + 16 * c, v);
+        tmem_ld16_issue(trow + 16 * c, v);
+        tmem_ld_wait(v);
         const int nbase = n0 + 16 * c;
         if (!valid || nbase >= p.n_gemm) continue;
         // deconv: 16 consecutive GEMM columns share one tap (Cout % 16 == 0)
@@ -477,107 +660,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
           const uint32_t ddy = (uint32_t)tap >> p.st_shift, ddx = (uint32_t)tap & (uint32_t)(p.stride - 1);
           pix = (ib * p.out_h + iy * p.stride + ddy) * p.out_w + ix * p.stride + ddx;
         }
-        const bool full16 = (nbase + 16) <= p.n_gemm;
-        float y[16];
-        if (full16) {
-#pragma unroll
-          for (int j4 = 0; j4 < 4; ++j4) {
-            const float4 b4 = __ldg(reinterpret_cast<const float4*>(p.bias + cobase) + j4);
-            float2 r0, r1;
-            if constexpr (DT == PMX_I8) {
-              const float4 a4 = __ldg(reinterpret_cast<const float4*>(p.alpha + cobase) + j4);
-              r0 = __ffma2_rn(make_float2((float)(int)v[4 * j4], (float)(int)v[4 * j4 + 1]), make_float2(a4.x, a4.y),
-                              make_float2(b4.x, b4.y));
-              r1 = __ffma2_rn(make_float2((float)(int)v[4 * j4 + 2], (float)(int)v[4 * j4 + 3]),
-                              make_float2(a4.z, a4.w), make_float2(b4.z, b4.w));
-            } else {
-              r0 = __fadd2_rn(make_float2(__uint_as_float(v[4 * j4]), __uint_as_float(v[4 * j4 + 1])),
-                              make_float2(b4.x, b4.y));
-              r1 = __fadd2_rn(make_float2(__uint_as_float(v[4 * j4 + 2]), __uint_as_float(v[4 * j4 + 3])),
-                              make_float2(b4.z, b4.w));
-            }
-            y[4 * j4] = r0.x;
-            y[4 * j4 + 1] = r0.y;
-            y[4 * j4 + 2] = r1.x;
-            y[4 * j4 + 3] = r1.y;
-          }
-        } else {
-#pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const int co = cobase + j;
-            y[j] = 0.f;
-            if ((nbase + j) < p.n_gemm) {
-              if constexpr (DT == PMX_I8) y[j] = __fmaf_rn((float)(int)v[j], p.alpha[co], p.bias[co]);
-              else y[j] = __fadd_rn(__uint_as_float(v[j]), p.bias[co]);
-            }
-          }
-        }
-        if constexpr (OUTK == 1) {
-          // single int8 consumer, 16-byte aligned rows (checked on the host); the
-          // ReLU folds into the quantizer's lower clamp
-          if (full16 && !p.bn_post && !p.keys) {
-            const OutDev& od = outs.o[0];
-            *reinterpret_cast<uint4*>(reinterpret_cast<int8_t*>(od.ptr) + (size_t)pix * od.c_stride + od.c_offset +
-                                      cobase) = quant16(y, od.scale, od.inv, p.relu ? 0.0f : -128.0f);
-            continue;
-          }
-        }
-        if (p.bn_post) {
-#pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const int co = cobase + j;
-            if ((nbase + j) < p.n_gemm)
-              y[j] = __fadd_rn(__fmul_rn(__fsub_rn(y[j], p.bn_post[co]), p.bn_post[p.out_c + co]),
-                               p.bn_post[2 * p.out_c + co]);
-          }
-        }
-        if (p.relu) {
-#pragma unroll
-          for (int j = 0; j < 16; ++j) y[j] = fmaxf(y[j], 0.f);
-        }
-        if (p.keys) {
-#pragma unroll
-          for (int j = 0; j < 16; ++j)
-            if ((nbase + j) < p.n_gemm) {
-              lo = nmin(lo, y[j]);
-              hi = nmax(hi, y[j]);
-            }
-        }
-        if constexpr (OUTK == 1) {
-          // single int8 consumer, 16-byte aligned rows (checked on the host)
-          const OutDev& od = outs.o[0];
-          if (full16) {
-            *reinterpret_cast<uint4*>(reinterpret_cast<int8_t*>(od.ptr) + (size_t)pix * od.c_stride + od.c_offset +
-                                      cobase) = quant16(y, od.scale, od.inv);
-          } else {
-            for (int j = 0; j < 16; ++j)
-              if (nbase + j < p.n_gemm) store_one(od, pix, cobase + j, y[j]);
-          }
-        } else {
-#pragma unroll
-          for (int o = 0; o < PMX_MAX_OUTS; ++o) {
-            if (o >= outs.n) break;
-            const OutDev& od = outs.o[o];
-            const int64_t off = (int64_t)pix * od.c_stride + od.c_offset + cobase;
-            if (full16 && od.dtype == PMX_I8 && (off & 15) == 0) {
-              *reinterpret_cast<uint4*>(reinterpret_cast<int8_t*>(od.ptr) + off) = quant16(y, od.scale, od.inv);
-            } else if (full16 && od.dtype == PMX_F16 && (off & 7) == 0) {
-              uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__half*>(od.ptr) + off);
-              dst[0] = make_uint4(f16x2_sat(y[0], y[1]), f16x2_sat(y[2], y[3]), f16x2_sat(y[4], y[5]),
-                                  f16x2_sat(y[6], y[7]));
-              dst[1] = make_uint4(f16x2_sat(y[8], y[9]), f16x2_sat(y[10], y[11]), f16x2_sat(y[12], y[13]),
-                                  f16x2_sat(y[14], y[15]));
-            } else if (full16 && od.dtype == PMX_F32 && (off & 3) == 0) {
-              float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(od.ptr) + off);
-#pragma unroll
-              for (int qq = 0; qq < 4; ++qq)
-                dst[qq] = make_float4(y[4 * qq], y[4 * qq + 1], y[4 * qq + 2], y[4 * qq + 3]);
-            } else {
-              for (int j = 0; j < 16; ++j)
-                if (nbase + j < p.n_gemm) store_one(od, pix, cobase + j, y[j]);
-            }
-          }
-        }
+        epi_chunk<DT, OUTK>(p, outs, v, pix, nbase, cobase, s_alpha, s_bias, qlo, lo, hi);
       }
       // release this accumulator buffer to the MMA warp
       tc_fence_before();
@@ -714,7 +797,7 @@ Plan plan_for(const pmx_conv_desc& d) {
   p.a_bytes = 128u * kc_bytes;
   p.b_bytes = (uint32_t)bn * kc_bytes;
   const uint32_t stage = p.a_bytes + p.b_bytes;
-  int stages = (int)((200u * 1024u) / stage);  // one persistent CTA per SM
+  int stages = (int)((200u * 1024u - 8u * (uint32_t)d.out_c) / stage);  // one persistent CTA per SM
   if (stages > 12) stages = 12;
   if (stages < 2) stages = 2;
   p.stages = stages;
@@ -727,7 +810,8 @@ Plan plan_for(const pmx_conv_desc& d) {
     const uint32_t halo_al = (halo + 1023u) & ~1023u;
     const uint32_t bblk = (uint32_t)bn * kc_bytes;
     const uint32_t bres_total = 9u * p.cblocks * bblk;
-    const uint32_t budget = 227u * 1024u - 2048u;  // dynamic smem minus alignment + barriers
+    // dynamic smem minus alignment, barriers and the alpha / bias copies
+    const uint32_t budget = 227u * 1024u - 2048u - 8u * (uint32_t)((d.out_c + 3) & ~3);
     if (bres_total + 2 * halo_al <= budget) {
       p.mode = MODE_HALO;
       p.tw = 8;
@@ -756,10 +840,13 @@ Plan plan_for(const pmx_conv_desc& d) {
   p.fd_iw = make_fastdiv((uint32_t)d.in_w);
   p.fd_ih = make_fastdiv((uint32_t)d.in_h);
   p.fd_oc = make_fastdiv((uint32_t)d.out_c);
-  // as many TMEM accumulators as fit (2..8): the MMA warp runs ahead of a slow epilogue warp
-  p.nacc = 512 / bn < 8 ? 512 / bn : 8;
-  if (p.nacc < 2) p.nacc = 2;
-  p.fd_na = make_fastdiv((uint32_t)p.nacc);
+  // as many TMEM accumulators as fit (a power of two, 2..8): the MMA warp runs ahead
+  // of the epilogue; the epilogue drains up to 4 tiles at once (tile slots)
+  p.nacc = 2;
+  while (p.nacc < 8 && 2 * p.nacc * bn <= 512) p.nacc *= 2;
+  p.nacc_shift = __builtin_ctz((unsigned)p.nacc);
+  p.egroups = bn <= 64 ? 4 : (bn <= 128 ? 2 : 1);
+  if (p.egroups > p.nacc) p.egroups = p.nacc;
   const int cols = p.nacc * bn;
   p.tmem_cols = cols <= 32 ? 32 : (cols <= 64 ? 64 : (cols <= 128 ? 128 : (cols <= 256 ? 256 : 512)));
   const uint32_t m_enc = 128u >> 4, n_enc = (uint32_t)bn >> 3;
@@ -767,7 +854,8 @@ Plan plan_for(const pmx_conv_desc& d) {
     p.idesc = (2u << 4) | (1u << 7) | (1u << 10) | (n_enc << 17) | (m_enc << 24);
   else
     p.idesc = (1u << 4) | (0u << 7) | (0u << 10) | (n_enc << 17) | (m_enc << 24);
-  pl.smem = 1024 + (size_t)p.stages * (p.a_bytes + p.b_bytes) + p.bres_bytes + (2 * p.stages + 2 * p.nacc + 1) * 8 + 16;
+  pl.smem = 1024 + (size_t)p.stages * (p.a_bytes + p.b_bytes) + p.bres_bytes + (2 * p.stages + 2 * p.nacc + 1) * 8 + 32 +
+            8 * (size_t)((d.out_c + 3) & ~3);
   pl.ok = true;
   return pl;
 }

@@ -677,6 +677,36 @@ class CompiledGraph:
                 acc[name] += a.elapsed_time(b)
         return {k: v / reps for k, v in acc.items()}
 
+    def timed_ops(self, reps: int = 10) -> dict:
+        """Device time of every op: each op is captured `reps` times back to back into its
+        own CUDA graph, replayed once to warm up, then replayed between CUDA events on
+        the capturing stream -> mean ms per op (no host launch gaps inside the range)."""
+        torch = self.torch
+        st = torch.cuda.Stream()
+        st.wait_stream(torch.cuda.current_stream())
+        out = {}
+        with torch.cuda.stream(st):
+            sp = N.stream_ptr()
+            for _, fn in self.ops:  # warm-up (lazy module loads, tensor-map encodes)
+                fn(sp)
+        torch.cuda.synchronize()
+        for name, fn in self.ops:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=st):
+                sp = N.stream_ptr()
+                for _ in range(reps):
+                    fn(sp)
+            with torch.cuda.stream(st):
+                g.replay()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(st)
+                g.replay()
+                b.record(st)
+            torch.cuda.synchronize()
+            out[name] = a.elapsed_time(b) / reps
+            del g
+        return out
+
     def kernels_per_launch(self) -> int:
         """Number of libpmx kernels one launch() issues (memsets excluded)."""
         n = 0

@@ -30,7 +30,7 @@ def main():
                       in_c_stride=cin, in_c_offset=0, out_c=cout, k_h=3, k_w=3, stride_h=st, stride_w=st, pad_h=1,
                       pad_w=1, out_h=oh, out_w=ow, relu=1)
     arr, n = N.outs_array([N.Out(ptr=y.data_ptr(), scale=0.05, dtype=N.PMX_I8, c_stride=cout, c_offset=0)])
-    tr = torch.zeros(9 * 64, dtype=torch.int64, device="cuda")
+    tr = torch.zeros(10 * 64, dtype=torch.int64, device="cuda")
 
     def call():
         N.check(lib.pmx_conv(ctypes.byref(desc), x.data_ptr(), wt.data_ptr(), alpha.data_ptr(), bias.data_ptr(),
@@ -50,17 +50,17 @@ def main():
     call()
     torch.cuda.synchronize()
     lib.pmx_debug_trace(None)
-    t = tr.cpu().numpy().reshape(9, 64).astype(np.int64)
+    t = tr.cpu().numpy().reshape(10, 64).astype(np.int64)
     t0 = t[8, 0]
     print("prologue: setup %d, weights landed %d, teardown %d (cycles from entry)" %
           tuple((t[8, i] - t0) if t[8, i] else -1 for i in (1, 2, 3)))
     names = ["P.wait_empty", "P.issued", "M.wait_full", "M.full_ok", "M.committed", "E.wait_tfull", "E.tfull_ok",
-             "E.released"]
-    print("tile " + " ".join(f"{n:>12}" for n in names))
+             "E.released", "", "M.loop_top"]
+    print("tile " + " ".join(f"{names[e]:>12}" for e in (0, 1, 9, 2, 3, 4, 5, 6, 7)))
     for i in range(24):
-        if not t[:8, i].any():
+        if not t[:8, i].any() and not t[9, i]:
             break
-        print(f"{i:4d} " + " ".join(f"{(t[e, i] - t0) if t[e, i] else -1:12d}" for e in range(8)))
+        print(f"{i:4d} " + " ".join(f"{(t[e, i] - t0) if t[e, i] else -1:12d}" for e in (0, 1, 9, 2, 3, 4, 5, 6, 7)))
 
 
 if __name__ == "__main__":

@@ -39,16 +39,25 @@ __global__ void mma_bench(int n_mma, uint32_t idesc, uint32_t layout, uint32_t s
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = tslot;
   if (threadIdx.x == 0) {
+    const uint32_t step = vary == 1 ? 32u : (vary == 2 ? 16u : (vary == 3 ? 512u : 1024u));
+    uint64_t ad[9], bd[9];
+#pragma unroll
+    for (int j = 0; j < 9; ++j) {
+      const uint32_t off = vary ? (uint32_t)j * step : 0u;
+      ad[j] = sdesc(base + off, sbo, layout, lbo);
+      bd[j] = sdesc(base + 32768 + (off & ~1023u), sbo, layout, lbo);
+    }
     long long t0 = clock64();
-    for (int i = 0; i < n_mma; ++i) {
-      const uint32_t off = vary ? (uint32_t)((i % 9) * (vary == 1 ? 32 : 16)) : 0u;
-      const uint64_t ad = sdesc(base + off, sbo, layout, lbo), bd = sdesc(base + 32768 + (off & ~1023u), sbo, layout, lbo);
+    for (int i = 0; i < n_mma; i += 9) {
+#pragma unroll
+      for (int j = 0; j < 9; ++j) {
       if (KIND == 0)
         asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\ttcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}"
-                     ::"r"(tmem), "l"(ad), "l"(bd), "r"(idesc), "r"(i));
+                     ::"r"(tmem), "l"(ad[j]), "l"(bd[j]), "r"(idesc), "r"(i + j));
       else
         asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\ttcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}"
-                     ::"r"(tmem), "l"(ad), "l"(bd), "r"(idesc), "r"(i));
+                     ::"r"(tmem), "l"(ad[j]), "l"(bd[j]), "r"(idesc), "r"(i + j));
+      }
     }
     long long t1 = clock64();
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&bar)));
@@ -67,13 +76,14 @@ __global__ void mma_bench(int n_mma, uint32_t idesc, uint32_t layout, uint32_t s
 int main() {
   long long* d;
   cudaMalloc(&d, 16);
-  const int n = 512;
+  const int n = 504;
   cudaFuncSetAttribute(mma_bench<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
   cudaFuncSetAttribute(mma_bench<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
   struct Cfg { int lay; uint32_t sbo, lbo; int vary; const char* name; };
   Cfg cfgs[] = {{2, 1024, 16, 0, "SW128 fixed"}, {2, 1024, 16, 1, "SW128 vary+32B"}, {4, 512, 16, 0, "SW64 fixed"},
                 {0, 128, 2048, 0, "NONE sbo128"}, {0, 160, 2880, 0, "NONE sbo160 lbo2880"},
-                {0, 160, 2880, 2, "NONE sbo160 vary+16B"}};
+                {0, 160, 2880, 2, "NONE sbo160 vary+16B"},
+                {4, 512, 16, 3, "SW64 vary+512B"}, {2, 1024, 16, 4, "SW128 vary+1024B"}, {0, 128, 1024, 3, "NONE sbo128 vary+512B"}};
   for (int kind = 0; kind < 2; ++kind)
     for (int N : {64, 128, 256})
       for (const Cfg& c : cfgs) {

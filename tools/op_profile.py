@@ -50,24 +50,24 @@ def main():
         import numpy as np
 
         lib = N.load()
-        tr = torch.zeros(9 * 64, dtype=torch.int64, device="cuda")
+        tr = torch.zeros(10 * 64, dtype=torch.int64, device="cuda")
         lib.pmx_debug_trace(tr.data_ptr())
         fn(N.stream_ptr())
         torch.cuda.synchronize()
         lib.pmx_debug_trace(None)
-        t = tr.cpu().numpy().reshape(9, 64).astype(np.int64)
+        t = tr.cpu().numpy().reshape(10, 64).astype(np.int64)
         t0 = t[8, 0]
         print("prologue: setup %d, weights landed %d, teardown %d (cycles from entry)" %
               tuple((t[8, i] - t0) if t[8, i] else -1 for i in (1, 2, 3)))
         names = ["P.wait_empty", "P.issued", "M.wait_full", "M.full_ok", "M.committed", "E.wait_tfull",
-                 "E.tfull_ok", "E.released"]
-        print("tile " + " ".join(f"{n:>12}" for n in names))
+                 "E.tfull_ok", "E.released", "", "M.loop_top"]
+        print("tile " + " ".join(f"{names[e]:>12}" for e in (0, 1, 9, 2, 3, 4, 5, 6, 7)))
         print("tile 6 per epilogue warp (tfull_ok, released): " +
               " ".join(f"w{w + 2}:{t[8, 8 + 2 * w] - t0}/{t[8, 9 + 2 * w] - t0}" for w in range(16)))
         for i in range(32):
-            if not t[:8, i].any():
+            if not t[:8, i].any() and not t[9, i]:
                 break
-            print(f"{i:4d} " + " ".join(f"{(t[e, i] - t0) if t[e, i] else -1:12d}" for e in range(8)))
+            print(f"{i:4d} " + " ".join(f"{(t[e, i] - t0) if t[e, i] else -1:12d}" for e in (0, 1, 9, 2, 3, 4, 5, 6, 7)))
         return
     torch.cuda.profiler.start()
     fn(N.stream_ptr())
