@@ -44,7 +44,7 @@ typedef enum {
 
 typedef enum { PMX_F32 = 0, PMX_F16 = 1, PMX_I8 = 2, PMX_F64 = 3 } pmx_dtype;
 
-#define PMX_ABI_VERSION 1
+#define PMX_ABI_VERSION 2
 
 const char* pmx_last_error(void);
 int32_t pmx_abi_version(void);
@@ -122,6 +122,13 @@ pmx_status pmx_pillarize(const float* points, const int64_t* frame_offsets, int3
                          int32_t* coords, int32_t* counts, int32_t* pt_idx, int32_t* n_pillars,
                          void* ws, size_t ws_bytes, pmx_stream_t stream);
 
+/* The cell -> pillar-slot map pmx_pillarize leaves in `ws`: device int32
+ * [B, grid_h, grid_w], the kept pillar's slot + 1 in that cell, 0 if empty
+ * (every cell is written on every call; valid until `ws` is reused).  Input of
+ * pmx_conv_gather.  Returns NULL on bad arguments. */
+const int32_t* pmx_pillarize_cell_map(const pmx_grid* grid, int32_t batch, int64_t max_points_per_frame,
+                                      const void* ws);
+
 /* Materialise padded per-pillar features [B, Pcap, M, F] f32 (zero padded) and
  * the mask [B, Pcap, M] u8 -- the PillarSample of pm/tensor_ops.py:60-77.
  * n_features = 5: (x, y, i, x-mx, y-my), pm/scenes.py:186-192 (points' third
@@ -183,6 +190,19 @@ pmx_status pmx_pfn_scatter(const pmx_pfn_desc* desc, const pmx_grid* grid, int32
                            int32_t n_outs, uint32_t* in_keys, uint32_t* out_keys,
                            pmx_stream_t stream);
 
+/* Same computation as pmx_pfn_scatter, but the pooled pillar features are written
+ * densely per pillar slot -- outs[o] row b * pcap + p, rows >= n_pillars[b]
+ * untouched -- instead of onto a canvas (scatter_pillars pm/tensor_ops.py:138-160
+ * then happens virtually inside pmx_conv_gather: no canvas memset or write). */
+pmx_status pmx_pfn_pillars(const pmx_pfn_desc* desc, const pmx_grid* grid, int32_t batch,
+                           int32_t pcap, const float* points, const int64_t* frame_offsets,
+                           const float* features, const uint8_t* mask, const int32_t* coords,
+                           const int32_t* counts, const int32_t* pt_idx,
+                           const int32_t* n_pillars, const void* weight, const float* alpha,
+                           const float* bias, const float* bn_post, const pmx_out* outs,
+                           int32_t n_outs, uint32_t* in_keys, uint32_t* out_keys,
+                           pmx_stream_t stream);
+
 /* ------------------------------------------------------------------------
  * K6-K10 implicit-GEMM layer kernel -- replaces conv2d pm/tensor_ops.py:109-131
  * / linear :80-91 under the precision dispatch of pm/model.py:271-307, plus the
@@ -218,12 +238,25 @@ pmx_status pmx_conv(const pmx_conv_desc* desc, const void* x, const void* w, con
                     const float* bias, const float* bn_post, const pmx_out* outs, int32_t n_outs,
                     uint32_t* out_keys, void* ws, size_t ws_bytes, pmx_stream_t stream);
 
+/* pmx_conv on the pillar canvas without materialising it (the first backbone
+ * conv): x[b, y, x, c] = feats[(b * pcap + cell_map[b, y, x] - 1) * in_c_stride +
+ * in_c_offset + c], or 0 where cell_map == 0.  desc describes the canvas (in_h /
+ * in_w = grid, in_c_stride = channels per pillar row).  Bit-identical to pmx_conv
+ * on the scattered canvas.  Only the tcgen05 halo shapes (3x3, stride 1/2, 64 or
+ * 128 bytes of channels, int8/f16): PMX_ERR_UNSUPPORTED otherwise -- the caller
+ * then scatters a canvas and calls pmx_conv. */
+int32_t pmx_conv_gather_supported(const pmx_conv_desc* desc); /* 1 if pmx_conv_gather runs desc */
+pmx_status pmx_conv_gather(const pmx_conv_desc* desc, const void* feats, const int32_t* cell_map,
+                           int32_t pcap, const void* w, const float* alpha, const float* bias,
+                           const float* bn_post, const pmx_out* outs, int32_t n_outs,
+                           uint32_t* out_keys, pmx_stream_t stream);
+
 /* Force a backend for testing: 0 = automatic, 1 = SIMT reference kernel only,
  * 2 = tcgen05 without the halo variant. */
 void pmx_set_conv_backend(int32_t mode);
 /* Debug: when non-NULL, tcgen05 conv launches record per-role clock64 stamps of
- * CTA 0 into buf[9][64]: rows 0-7 producer/MMA/epilogue hand-offs per tile, row 8
- * = kernel entry, setup done, resident weights landed, teardown. */
+ * CTA 0 into buf[10][64]: rows 0-7 producer/MMA/epilogue hand-offs per tile, row 8
+ * = kernel entry, setup done, resident weights landed, teardown; row 9 = MMA loop top. */
 void pmx_debug_trace(unsigned long long* buf);
 
 /* Stage an f32 [pixels, c] tensor into every consumer format (the precision

@@ -77,6 +77,11 @@ SIGNATURES = {
     "pmx_pillar_features": (I32, [P, P, I32, C.POINTER(Grid), I32, I32, P, P, P, P, P, P, P]),
     "pmx_pfn_scatter": (I32, [C.POINTER(PfnDesc), C.POINTER(Grid), I32, I32, P, P, P, P, P, P, P, P, P, P,
                               P, P, C.POINTER(Out), I32, P, P, P]),
+    "pmx_pfn_pillars": (I32, [C.POINTER(PfnDesc), C.POINTER(Grid), I32, I32, P, P, P, P, P, P, P, P, P, P,
+                              P, P, C.POINTER(Out), I32, P, P, P]),
+    "pmx_pillarize_cell_map": (P, [C.POINTER(Grid), I32, I64, P]),
+    "pmx_conv_gather_supported": (I32, [C.POINTER(ConvDesc)]),
+    "pmx_conv_gather": (I32, [C.POINTER(ConvDesc), P, P, I32, P, P, P, P, C.POINTER(Out), I32, P, P]),
     "pmx_conv_workspace": (SZ, [C.POINTER(ConvDesc)]),
     "pmx_conv": (I32, [C.POINTER(ConvDesc), P, P, P, P, P, C.POINTER(Out), I32, P, P, SZ, P]),
     "pmx_set_conv_backend": (None, [I32]),

@@ -13,8 +13,9 @@ namespace pmx {
 // implemented in conv_tc.cu
 pmx_status conv_tc_try(const pmx_conv_desc& d, const void* x, const void* w, const float* alpha, const float* bias,
                        const float* bn_post, const Outs& outs, uint32_t* keys, void* ws, size_t ws_bytes,
-                       cudaStream_t st, bool* launched);
+                       cudaStream_t st, bool* launched, const GatherIn* gin);
 size_t conv_tc_workspace(const pmx_conv_desc& d);
+bool conv_tc_gather_ok(const pmx_conv_desc& d);
 const char* conv_tc_backend(int dtype, int kind);
 
 int g_conv_backend_mode = 0;
@@ -214,7 +215,7 @@ pmx_status pmx_conv(const pmx_conv_desc* desc, const void* x, const void* w, con
   Outs o = make_outs(outs, n_outs);
   if (g_conv_backend_mode == 0) {
     bool launched = false;
-    st = conv_tc_try(d, x, w, alpha, bias, bn_post, o, out_keys, ws, ws_bytes, stream, &launched);
+    st = conv_tc_try(d, x, w, alpha, bias, bn_post, o, out_keys, ws, ws_bytes, stream, &launched, nullptr);
     if (st != PMX_OK || launched) return st;
   }
   ConvArgs a;
@@ -238,6 +239,40 @@ pmx_status pmx_conv(const pmx_conv_desc* desc, const void* x, const void* w, con
   else if (d.in_dtype == PMX_F16) launch_simt<PMX_F16>(a, o, stream);
   else launch_simt<PMX_F32>(a, o, stream);
   return check_launch("pmx_conv(simt)");
+}
+
+int32_t pmx_conv_gather_supported(const pmx_conv_desc* desc) {
+  if (!desc || validate(*desc) != PMX_OK) return 0;
+  const int esz = elem_size(desc->in_dtype);
+  if (((int64_t)desc->in_c_stride * esz) % 16 != 0 || ((int64_t)desc->in_c_offset * esz) % 16 != 0) return 0;
+  return conv_tc_gather_ok(*desc) ? 1 : 0;
+}
+
+pmx_status pmx_conv_gather(const pmx_conv_desc* desc, const void* feats, const int32_t* cell_map, int32_t pcap,
+                           const void* w, const float* alpha, const float* bias, const float* bn_post,
+                           const pmx_out* outs, int32_t n_outs, uint32_t* out_keys, pmx_stream_t stream) {
+  PMX_REQUIRE(desc != nullptr, "desc is NULL");
+  const pmx_conv_desc d = *desc;
+  pmx_status st = validate(d);
+  if (st != PMX_OK) return st;
+  PMX_REQUIRE(feats && cell_map && w && bias, "NULL conv operand");
+  PMX_REQUIRE(pcap >= 1, "pcap must be positive");
+  PMX_REQUIRE(d.in_dtype != PMX_I8 || alpha, "int8 conv needs alpha");
+  st = validate_outs(outs, n_outs, d.out_c);
+  if (st != PMX_OK) return st;
+  if (d.batch == 0) return PMX_OK;
+  const int esz = elem_size(d.in_dtype);
+  PMX_REQUIRE(((int64_t)d.in_c_stride * esz) % 16 == 0 && ((int64_t)d.in_c_offset * esz) % 16 == 0 &&
+                  (reinterpret_cast<uintptr_t>(feats) & 15) == 0,
+              "gathered pillar rows must be 16-byte aligned");
+  if (g_conv_backend_mode == 1) return fail(PMX_ERR_UNSUPPORTED, "pmx_conv_gather: tcgen05 backend disabled");
+  Outs o = make_outs(outs, n_outs);
+  GatherIn gin{feats, cell_map, pcap};
+  bool launched = false;
+  st = conv_tc_try(d, feats, w, alpha, bias, bn_post, o, out_keys, nullptr, 0, stream, &launched, &gin);
+  if (st != PMX_OK) return st;
+  if (!launched) return fail(PMX_ERR_UNSUPPORTED, "pmx_conv_gather: shape outside the tcgen05 halo kernels");
+  return PMX_OK;
 }
 
 }  // extern "C"

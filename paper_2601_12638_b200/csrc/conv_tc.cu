@@ -87,6 +87,15 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map
       : "memory");
 }
 
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                            uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+          dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
+      : "memory");
+}
+
 __device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
                                             uint32_t bar) {
   asm volatile(
@@ -220,6 +229,11 @@ struct TcParams {
   const float* bn_post;
   uint32_t* keys;
   unsigned long long* trace;  // debug: per-role clock64 stamps of CTA 0 (pmx_debug_trace)
+  // GATHER (first conv on the pillar canvas)
+  const void* g_feats;   // [B * pcap, row] pillar features (+ channel offset)
+  const int32_t* g_map;  // [B, in_h, in_w] pillar slot per cell, -1 empty
+  int g_pcap;
+  int g_row_bytes;
 };
 
 #define PMX_TRACE(ev, idx)                                                              \
@@ -234,6 +248,8 @@ struct TcMaps {
 
 constexpr int kEpiWarps = 16;                  // warps 2..17: four per TMEM lane quarter
 constexpr int kThreads = 32 * (2 + kEpiWarps);  // + TMA producer warp + MMA warp
+constexpr int kGatherWarps = 3;                 // GATHER: warp 0 + warps 18, 19 build the halo tiles
+constexpr int kThreadsGather = kThreads + 32 * (kGatherWarps - 1);
 
 // One chunk (16 accumulator columns of one pixel row): y = acc * alpha + bias (int8)
 // or acc + bias (f16), optional unfolded BN and ReLU, observer min/max, then every
@@ -347,12 +363,137 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
 
+// GATHER producer (first conv on the pillar canvas, never materialised): the halo
+// tile of the (virtual) canvas x[b, y, x, :] = feats[b * pcap + map[b, y, x] - 1, :]
+// (0 where map == 0 or outside the grid) is built in shared memory by 96 threads in
+// exactly the layout the TMA halo path produces -- per parity plane, [channel
+// group][plane pixel][16 B].  Every thread owns up to kPixPerThr fixed halo pixels;
+// per tile:
+//   A  its pixels' cell-map entries (loaded during the previous tile) -> compact
+//      list of occupied halo pixels (~7% at KITTI density); the next tile's map
+//      entries are loaded right away so that round trip overlaps this tile;
+//   B2 the 16-byte feature loads of the listed pixels (one round trip per tile);
+//   B1 zero-fill the stage, barrier, then B2's stores overwrite the occupied pixels;
+//      a proxy fence publishes the generic-proxy stores to the tensor core.
+// Replaces the canvas write of pm/tensor_ops.py:138-160 + the conv's canvas read.
+template <int HS>
+struct GatherGeom {
+  static constexpr int NPL = HS == 2 ? 4 : 1;
+  static constexpr int HPX_TOTAL = HS == 2 ? 561 : 180;
+};
+
+constexpr int kPixPerThr = 6;  // ceil(561 / 96)
+
+__host__ __device__ constexpr int plane_w(int hs, int q) { return hs == 2 ? 8 + (q & 1) : 10; }
+__host__ __device__ constexpr int plane_hpx(int hs, int q) { return hs == 2 ? (16 + (q >> 1)) * (8 + (q & 1)) : 180; }
+__host__ __device__ constexpr int plane_p0(int hs, int q) {
+  return hs == 2 ? (q == 0 ? 0 : (q == 1 ? 128 : (q == 2 ? 272 : 408))) : 0;
+}
+
+template <int CINB, int HS, typename FullF, typename EmptyF>
+__device__ __forceinline__ void gather_producer(const TcParams& p, uint32_t a_smem, int gt, int lane, int total,
+                                                int32_t* s_list, int32_t* s_cnt, FullF full, EmptyF empty) {
+  using Geo = GatherGeom<HS>;
+  constexpr int G = CINB / 16;  // 16-byte channel groups per pixel
+  constexpr int NT = 32 * kGatherWarps;
+  static_assert(NT * kPixPerThr >= Geo::HPX_TOTAL, "halo pixels per thread");
+  const char* feats = reinterpret_cast<const char*>(p.g_feats);
+  // my halo pixels: offset from the tile's input origin and the list code (plane << 10 | pixel)
+  int ry[kPixPerThr], rx[kPixPerThr], code[kPixPerThr];
+#pragma unroll
+  for (int j = 0; j < kPixPerThr; ++j) {
+    const int hp = gt + NT * j;
+    int q = 0;
+    if (HS == 2) q = (hp >= 128) + (hp >= 272) + (hp >= 408);
+    const int pp = hp - plane_p0(HS, q);
+    const int W = plane_w(HS, q);
+    const int r = pp / W, c = pp - (pp / W) * W;
+    const int py = q >> 1, px = q & 1;
+    ry[j] = HS == 2 ? 2 * (r - py) + py : r - 1;  // iy = stride * oy0 + ry
+    rx[j] = HS == 2 ? 2 * (c - px) + px : c - 1;
+    code[j] = hp < Geo::HPX_TOTAL ? (pp | (q << 10)) : -1;
+  }
+  auto load_map = [&](int t, int (&m)[kPixPerThr]) {
+    const int tq = (int)fdiv((uint32_t)t, p.fd_tx), tx = t - tq * p.tiles_x;
+    const int tb = (int)fdiv((uint32_t)tq, p.fd_ty);
+    const int oy0 = (tq - tb * p.tiles_y) * p.th, ox0 = tx * p.tw;
+    const int32_t* map = p.g_map + (int64_t)tb * p.in_h * p.in_w;
+#pragma unroll
+    for (int j = 0; j < kPixPerThr; ++j) {
+      const int iy = HS * oy0 + ry[j], ix = HS * ox0 + rx[j];
+      m[j] = 0;
+      if (code[j] >= 0 && (unsigned)iy < (unsigned)p.in_h && (unsigned)ix < (unsigned)p.in_w)
+        m[j] = __ldg(map + iy * p.in_w + ix);
+    }
+  };
+  int mcur[kPixPerThr];
+  if (blockIdx.x < total) load_map(blockIdx.x, mcur);
+  uint32_t s = 0, ph = 0;
+  int i = 0;
+  for (int t = blockIdx.x; t < total; t += gridDim.x, ++i) {
+    const int tb = (int)fdiv(fdiv((uint32_t)t, p.fd_tx), p.fd_ty);
+    const char* fb = feats + (int64_t)tb * p.g_pcap * p.g_row_bytes;
+    int32_t* cnt = s_cnt + (i & 1);
+    // A: occupied pixels -> s_list (code | (slot << 12))
+#pragma unroll
+    for (int j = 0; j < kPixPerThr; ++j)
+      if (mcur[j] != 0) s_list[atomicAdd(cnt, 1)] = code[j] | ((mcur[j] - 1) << 12);
+    const int tn = t + gridDim.x;
+    if (tn < total) load_map(tn, mcur);  // next tile's map: in flight during B
+    asm volatile("bar.sync 2, %0;" ::"r"(NT) : "memory");
+    if (gt == 0) s_cnt[(i + 1) & 1] = 0;
+    const int n_items = *cnt * G;
+    // B2 (first batch): feature loads of the occupied pixels
+    uint4 v[4];
+    uint32_t dst[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int it = gt + u * NT;
+      dst[u] = 0;
+      if (it < n_items) {
+        const uint32_t e = (uint32_t)s_list[it / G];
+        const int g = it % G, pp = e & 1023, q = (e >> 10) & 3;
+        const int m = (int)(e >> 12);
+        v[u] = __ldg(reinterpret_cast<const uint4*>(fb + (int64_t)m * p.g_row_bytes + g * 16));
+        dst[u] = (uint32_t)(plane_p0(HS, q) * G + g * plane_hpx(HS, q) + pp) * 16u;
+      }
+    }
+    // B1: zero-fill the stage
+    mbar_wait(empty(s), ph ^ 1);
+    const uint32_t slot = a_smem + s * p.a_bytes;
+    for (int it = gt; it < Geo::HPX_TOTAL * G; it += NT)
+      asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(slot + 16u * it), "r"(0) : "memory");
+    asm volatile("bar.sync 2, %0;" ::"r"(NT) : "memory");
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (gt + u * NT < n_items)
+        asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(slot + dst[u]), "r"(v[u].x), "r"(v[u].y),
+                     "r"(v[u].z), "r"(v[u].w)
+                     : "memory");
+    // dense tiles (> 4 NT chunks): the rest
+    for (int it = gt + 4 * NT; it < n_items; it += NT) {
+      const uint32_t e = (uint32_t)s_list[it / G];
+      const int g = it % G, pp = e & 1023, q = (e >> 10) & 3;
+      const int m = (int)(e >> 12);
+      const uint4 w4 = __ldg(reinterpret_cast<const uint4*>(fb + (int64_t)m * p.g_row_bytes + g * 16));
+      asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(
+                       slot + (uint32_t)(plane_p0(HS, q) * G + g * plane_hpx(HS, q) + pp) * 16u),
+                   "r"(w4.x), "r"(w4.y), "r"(w4.z), "r"(w4.w)
+                   : "memory");
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    if (lane == 0) mbar_arrive(full(s));
+    if (++s == (uint32_t)p.stages) s = 0, ph ^= 1;
+  }
+}
+
 // Persistent: grid = min(tiles, SMs); every role walks the same static tile sequence.
 // Accumulators are double-buffered in TMEM so the epilogue of tile i overlaps the
 // TMA + MMA of tile i+1; the smem ring runs across tile boundaries.
-template <int DT, int OUTK, int KCB, int CINB, int HS>
-__global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_constant__ TcMaps maps, const TcParams p,
-                                                              const Outs outs) {
+template <int DT, int OUTK, int KCB, int CINB, int HS, bool GATHER>
+__global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
+    conv_tc_kernel(const __grid_constant__ TcMaps maps, const TcParams p, const Outs outs) {
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
@@ -378,7 +519,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
   if (threadIdx.x == 0) {
     PMX_TRACE(8, 0);
     for (int s = 0; s < p.stages; ++s) {
-      mbar_init(full(s), 1);
+      mbar_init(full(s), GATHER ? kGatherWarps : 1);  // TMA: expect_tx; gather: one arrive per warp
       mbar_init(empty(s), 1);
     }
     for (int a = 0; a < p.nacc; ++a) {
@@ -386,6 +527,11 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
       mbar_init(tempty(a), 4 * (4 / p.egroups));  // the warps draining one tile
     }
     mbar_init(bfull, 1);
+    if constexpr (GATHER) {
+      int32_t* s_cnt = reinterpret_cast<int32_t*>(s_bias + ((p.out_c + 3) & ~3));
+      s_cnt[0] = 0;
+      s_cnt[1] = 0;
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -421,7 +567,14 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(const __grid_const
   }
   asm volatile("griddepcontrol.wait;" ::: "memory");
 
-  if (warp == 0) {
+  if (GATHER && (warp == 0 || warp >= 2 + kEpiWarps)) {
+    if constexpr (GATHER) {
+      // smem after alpha / bias: two list counters, the occupied-pixel list
+      int32_t* s_cnt = reinterpret_cast<int32_t*>(s_bias + ((p.out_c + 3) & ~3));
+      gather_producer<CINB, HS>(p, a_smem, warp == 0 ? lane : 32 * (warp - 1 - kEpiWarps) + lane, lane, total,
+                                s_cnt + 4, s_cnt, full, empty);
+    }
+  } else if (warp == 0) {
     if (lane == 0) {
       // ---------------- TMA producer
       uint32_t it = 0, s = 0, ph = 0;  // ring position, slot, phase
@@ -724,7 +877,7 @@ struct Plan {
 };
 
 // Can the tensor-core path run this layer?  (shape / alignment rules)
-Plan plan_for(const pmx_conv_desc& d) {
+Plan plan_for(const pmx_conv_desc& d, bool gather = false) {
   Plan pl{};
   pl.ok = false;
   if (d.in_dtype != PMX_I8 && d.in_dtype != PMX_F16) return pl;
@@ -811,7 +964,7 @@ Plan plan_for(const pmx_conv_desc& d) {
     const uint32_t bblk = (uint32_t)bn * kc_bytes;
     const uint32_t bres_total = 9u * p.cblocks * bblk;
     // dynamic smem minus alignment, barriers and the alpha / bias copies
-    const uint32_t budget = 227u * 1024u - 2048u - 8u * (uint32_t)((d.out_c + 3) & ~3);
+    const uint32_t budget = 227u * 1024u - 2048u - 8u * (uint32_t)((d.out_c + 3) & ~3) - (gather ? 2304u : 0u);
     if (bres_total + 2 * halo_al <= budget) {
       p.mode = MODE_HALO;
       p.tw = 8;
@@ -855,7 +1008,7 @@ Plan plan_for(const pmx_conv_desc& d) {
   else
     p.idesc = (1u << 4) | (0u << 7) | (0u << 10) | (n_enc << 17) | (m_enc << 24);
   pl.smem = 1024 + (size_t)p.stages * (p.a_bytes + p.b_bytes) + p.bres_bytes + (2 * p.stages + 2 * p.nacc + 1) * 8 + 32 +
-            8 * (size_t)((d.out_c + 3) & ~3);
+            8 * (size_t)((d.out_c + 3) & ~3) + (gather ? 2304 : 0);
   pl.ok = true;
   return pl;
 }
@@ -868,7 +1021,9 @@ pmx_status build_maps(const pmx_conv_desc& d, const Plan& pl, const void* x, con
   const char* xb = static_cast<const char*>(x) + (size_t)d.in_c_offset * esz;
   const cuuint64_t cs = (cuuint64_t)d.in_c_stride * esz;
   pmx_status st;
-  if (p.mode == MODE_HALO && p.stride == 2) {
+  if (x == nullptr) {
+    // GATHER: the A operand is built in shared memory by the producer warps
+  } else if (p.mode == MODE_HALO && p.stride == 2) {
     // parity plane (py, px) of the input: x[2i + py, 2j + px] -> plane[i, j];
     // [channel group][plane pixel][16 bytes], box (16 + py) x (8 + px)
     const cuuint32_t cpg = 16 / esz;
@@ -933,33 +1088,49 @@ const char* conv_tc_backend(int dtype, int) {
 
 size_t conv_tc_workspace(const pmx_conv_desc&) { return 0; }
 
+bool conv_tc_gather_ok(const pmx_conv_desc& d) {
+  if (g_conv_backend_mode == 1) return false;
+  const Plan pl = plan_for(d, true);
+  return pl.ok && pl.p.mode == MODE_HALO;
+}
+
 pmx_status conv_tc_try(const pmx_conv_desc& d, const void* x, const void* w, const float* alpha, const float* bias,
                        const float* bn_post, const Outs& outs, uint32_t* keys, void*, size_t, cudaStream_t st,
-                       bool* launched) {
+                       bool* launched, const GatherIn* gin) {
   *launched = false;
-  Plan pl = plan_for(d);
+  const bool gather = gin != nullptr;
+  Plan pl = plan_for(d, gather);
   if (!pl.ok) return PMX_OK;
+  if (gather && pl.p.mode != MODE_HALO) return PMX_OK;
   if ((reinterpret_cast<uintptr_t>(x) & 15) || (reinterpret_cast<uintptr_t>(w) & 15)) return PMX_OK;
   pmx_status s = get_encode();
   if (s != PMX_OK) return s;
   TcMaps maps;
   memset(&maps, 0, sizeof(maps));
-  s = build_maps(d, pl, x, w, &maps);
+  if (gather && gin->pcap > (1 << 20)) return PMX_OK;
+  s = build_maps(d, pl, gather ? nullptr : x, w, &maps);
   if (s != PMX_OK) return s;
   pl.p.alpha = alpha;
   pl.p.bias = bias;
   pl.p.bn_post = bn_post;
   pl.p.keys = keys;
   pl.p.trace = g_trace;
+  if (gather) {
+    const int esz = d.in_dtype == PMX_I8 ? 1 : 2;
+    pl.p.g_feats = static_cast<const char*>(gin->feats) + (size_t)d.in_c_offset * esz;
+    pl.p.g_map = gin->map;
+    pl.p.g_pcap = gin->pcap;
+    pl.p.g_row_bytes = d.in_c_stride * esz;
+  }
   dim3 grid(pl.grid_x, pl.grid_y);
   // OUTK 1: the common single int8 consumer with 16-byte aligned pixel rows
   const bool one_i8 = outs.n == 1 && outs.o[0].dtype == PMX_I8 && outs.o[0].c_stride % 16 == 0 &&
                       outs.o[0].c_offset % 16 == 0 && (reinterpret_cast<uintptr_t>(outs.o[0].ptr) & 15) == 0;
-  auto launch = [&](auto kern) -> pmx_status {
+  auto launch = [&](auto kern, int threads) -> pmx_status {
     PMX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = grid;
-    cfg.blockDim = dim3(kThreads);
+    cfg.blockDim = dim3(threads);
     cfg.dynamicSmemBytes = pl.smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
@@ -973,15 +1144,23 @@ pmx_status conv_tc_try(const pmx_conv_desc& d, const void* x, const void* w, con
   const int kcb = (int)(pl.p.sbo / 8);  // K-block bytes (64 or 128)
   const int cinb = pl.p.mode == MODE_HALO ? (int)pl.p.cin_bytes : 0;
   const int hs = pl.p.mode == MODE_HALO ? pl.p.stride : 0;
-#define PMX_TC_LAUNCH(DTV, KB, CB, HSV)                                                                     \
-  s = one_i8 ? launch(conv_tc_kernel<DTV, 1, KB, CB, HSV>) : launch(conv_tc_kernel<DTV, 0, KB, CB, HSV>)
-#define PMX_TC_SHAPES(DTV)                                        \
-  if (cinb == 64 && hs == 1) PMX_TC_LAUNCH(DTV, 64, 64, 1);       \
-  else if (cinb == 64) PMX_TC_LAUNCH(DTV, 64, 64, 2);             \
-  else if (cinb == 128 && hs == 1) PMX_TC_LAUNCH(DTV, 128, 128, 1); \
-  else if (cinb == 128) PMX_TC_LAUNCH(DTV, 128, 128, 2);          \
-  else if (kcb == 64) PMX_TC_LAUNCH(DTV, 64, 0, 0);               \
-  else PMX_TC_LAUNCH(DTV, 128, 0, 0);
+#define PMX_TC_LAUNCH(DTV, KB, CB, HSV)                                                                        \
+  if (gather)                                                                                                  \
+    s = one_i8 ? launch(conv_tc_kernel<DTV, 1, KB, CB, HSV, true>, kThreadsGather)                            \
+               : launch(conv_tc_kernel<DTV, 0, KB, CB, HSV, true>, kThreadsGather);                           \
+  else                                                                                                         \
+    s = one_i8 ? launch(conv_tc_kernel<DTV, 1, KB, CB, HSV, false>, kThreads)                                 \
+               : launch(conv_tc_kernel<DTV, 0, KB, CB, HSV, false>, kThreads)
+#define PMX_TC_LAUNCH_NG(DTV, KB)                                                                              \
+  s = one_i8 ? launch(conv_tc_kernel<DTV, 1, KB, 0, 0, false>, kThreads)                                      \
+             : launch(conv_tc_kernel<DTV, 0, KB, 0, 0, false>, kThreads)
+#define PMX_TC_SHAPES(DTV)                                          \
+  if (cinb == 64 && hs == 1) { PMX_TC_LAUNCH(DTV, 64, 64, 1); }     \
+  else if (cinb == 64) { PMX_TC_LAUNCH(DTV, 64, 64, 2); }           \
+  else if (cinb == 128 && hs == 1) { PMX_TC_LAUNCH(DTV, 128, 128, 1); } \
+  else if (cinb == 128) { PMX_TC_LAUNCH(DTV, 128, 128, 2); }        \
+  else if (kcb == 64) { PMX_TC_LAUNCH_NG(DTV, 64); }                \
+  else { PMX_TC_LAUNCH_NG(DTV, 128); }
   if (d.in_dtype == PMX_I8) {
     PMX_TC_SHAPES(PMX_I8)
   } else {
@@ -989,9 +1168,10 @@ pmx_status conv_tc_try(const pmx_conv_desc& d, const void* x, const void* w, con
   }
 #undef PMX_TC_SHAPES
 #undef PMX_TC_LAUNCH
+#undef PMX_TC_LAUNCH_NG
   if (s != PMX_OK) return s;
   *launched = true;
-  return check_launch("pmx_conv(tcgen05)");
+  return check_launch(gather ? "pmx_conv_gather(tcgen05)" : "pmx_conv(tcgen05)");
 }
 
 }  // namespace pmx

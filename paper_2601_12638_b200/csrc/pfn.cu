@@ -44,6 +44,7 @@ struct PfnArgs {
   float in_inv;
   uint32_t* in_keys;
   uint32_t* out_keys;
+  int dense;  // pmx_pfn_pillars: rows are pillar slots (b * pcap + p), no canvas
 };
 
 template <int DT>
@@ -198,7 +199,8 @@ __global__ void __launch_bounds__(kThreads) pfn_kernel(const PfnArgs a, const Ou
       }
     }
     // scatter the pooled 16-channel run onto the canvas, every consumer format
-    const int64_t pix = ((int64_t)b * a.g.grid_h + a.coords[2 * q]) * a.g.grid_w + a.coords[2 * q + 1];
+    const int64_t pix =
+        a.dense ? q : ((int64_t)b * a.g.grid_h + a.coords[2 * q]) * a.g.grid_w + a.coords[2 * q + 1];
     const int n_live = C - c0 < 16 ? C - c0 : 16;
 #pragma unroll
     for (int o = 0; o < PMX_MAX_OUTS; ++o)
@@ -240,7 +242,7 @@ pmx_status launch_dt(const PfnArgs& a, const Outs& outs, dim3 grid, cudaStream_t
 
 using namespace pmx;
 
-extern "C" pmx_status pmx_pfn_scatter(const pmx_pfn_desc* desc, const pmx_grid* grid, int32_t batch, int32_t pcap,
+static pmx_status pfn_impl(int dense, const pmx_pfn_desc* desc, const pmx_grid* grid, int32_t batch, int32_t pcap,
                                       const float* points, const int64_t* frame_offsets, const float* features,
                                       const uint8_t* mask, const int32_t* coords, const int32_t* counts,
                                       const int32_t* pt_idx, const int32_t* n_pillars, const void* weight,
@@ -284,9 +286,32 @@ extern "C" pmx_status pmx_pfn_scatter(const pmx_pfn_desc* desc, const pmx_grid* 
   a.in_inv = d.in_dtype == PMX_I8 ? (float)(1.0 / d.in_scale) : 1.f;
   a.in_keys = in_keys;
   a.out_keys = out_keys;
+  a.dense = dense;
   Outs o = make_outs(outs, n_outs);
   dim3 g((unsigned)ceil_div(pcap, kPPB), (unsigned)batch);
   if (d.in_dtype == PMX_I8) return launch_dt<PMX_I8>(a, o, g, stream);
   if (d.in_dtype == PMX_F16) return launch_dt<PMX_F16>(a, o, g, stream);
   return launch_dt<PMX_F32>(a, o, g, stream);
+}
+
+extern "C" pmx_status pmx_pfn_scatter(const pmx_pfn_desc* desc, const pmx_grid* grid, int32_t batch, int32_t pcap,
+                                      const float* points, const int64_t* frame_offsets, const float* features,
+                                      const uint8_t* mask, const int32_t* coords, const int32_t* counts,
+                                      const int32_t* pt_idx, const int32_t* n_pillars, const void* weight,
+                                      const float* alpha, const float* bias, const float* bn_post,
+                                      const pmx_out* outs, int32_t n_outs, uint32_t* in_keys, uint32_t* out_keys,
+                                      pmx_stream_t stream) {
+  return pfn_impl(0, desc, grid, batch, pcap, points, frame_offsets, features, mask, coords, counts, pt_idx,
+                  n_pillars, weight, alpha, bias, bn_post, outs, n_outs, in_keys, out_keys, stream);
+}
+
+extern "C" pmx_status pmx_pfn_pillars(const pmx_pfn_desc* desc, const pmx_grid* grid, int32_t batch, int32_t pcap,
+                                      const float* points, const int64_t* frame_offsets, const float* features,
+                                      const uint8_t* mask, const int32_t* coords, const int32_t* counts,
+                                      const int32_t* pt_idx, const int32_t* n_pillars, const void* weight,
+                                      const float* alpha, const float* bias, const float* bn_post,
+                                      const pmx_out* outs, int32_t n_outs, uint32_t* in_keys, uint32_t* out_keys,
+                                      pmx_stream_t stream) {
+  return pfn_impl(1, desc, grid, batch, pcap, points, frame_offsets, features, mask, coords, counts, pt_idx,
+                  n_pillars, weight, alpha, bias, bn_post, outs, n_outs, in_keys, out_keys, stream);
 }

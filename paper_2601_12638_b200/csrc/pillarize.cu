@@ -26,7 +26,7 @@ constexpr int kCellBlock = 1024 * kCellPerThr;
 struct PillarWs {
   int32_t* first;   // [B*HW]
   int32_t* cnt;     // [B*HW]
-  int32_t* pid;     // [B*HW]
+  int32_t* pid;     // [B*HW] kept pillar slot + 1, 0 = empty
   int32_t* cell;    // [B*Nmax]
   int32_t* ptblk;   // [B*NB]
   int32_t* thresh;  // [B]
@@ -243,7 +243,7 @@ __global__ void __launch_bounds__(1024) emit_kernel(const pmx_grid g, PillarWs w
     if (c >= hw) break;
     if (keep[j]) {
       int64_t q = (int64_t)b * pcap + a;
-      w.pid[b * hw + c] = a;
+      w.pid[b * hw + c] = a + 1;  // slot + 1 (0 = empty: TMA out-of-bounds fill reads as empty)
       coords[2 * q + 0] = (int)(c / g.grid_w);
       coords[2 * q + 1] = (int)(c % g.grid_w);
       counts[q] = n[j] < g.max_points ? n[j] : g.max_points;
@@ -251,7 +251,7 @@ __global__ void __launch_bounds__(1024) emit_kernel(const pmx_grid g, PillarWs w
       a += 1;
       p += n[j];
     } else {
-      w.pid[b * hw + c] = -1;
+      w.pid[b * hw + c] = 0;
     }
   }
 }
@@ -262,7 +262,7 @@ __global__ void slot_kernel(const int64_t* __restrict__ offs, int64_t nmax, cons
   const int64_t n = offs[b + 1] - offs[b];
   const int64_t hw = (int64_t)g.grid_h * g.grid_w;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    int p = w.pid[b * hw + w.cell[b * nmax + i]];
+    int p = w.pid[b * hw + w.cell[b * nmax + i]] - 1;
     if (p >= 0) {
       int64_t q = (int64_t)b * pcap + p;
       int s = atomicAdd(w.fill + q, 1);
@@ -415,6 +415,15 @@ __global__ void __launch_bounds__(256) features_kernel(const float4* __restrict_
 using namespace pmx;
 
 extern "C" {
+
+const int32_t* pmx_pillarize_cell_map(const pmx_grid* g, int32_t batch, int64_t max_points_per_frame,
+                                      const void* ws) {
+  if (!g || !ws || batch < 0) return nullptr;
+  int32_t pcap = g->max_pillars > 0 ? g->max_pillars : g->grid_h * g->grid_w;
+  PillarWs w;
+  carve(g, batch, max_points_per_frame, pcap, const_cast<void*>(ws), &w);
+  return w.pid;  // emit_kernel writes every cell: kept pillar slot + 1, or 0
+}
 
 size_t pmx_pillarize_workspace(const pmx_grid* g, int32_t batch, int64_t max_points_per_frame) {
   if (!g || batch < 0) return 0;

@@ -266,4 +266,11 @@ __device__ __forceinline__ void store16(const OutDev& od, int64_t pix, int c0, c
 
 __host__ pmx_status validate_outs(const pmx_out* outs, int n, int c_needed);
 
+// first-conv input gathered from pillar rows (pmx_conv_gather)
+struct GatherIn {
+  const void* feats;
+  const int32_t* map;
+  int32_t pcap;
+};
+
 }  // namespace pmx

@@ -150,6 +150,7 @@ class CompiledGraph:
         self._resolve_sources(in_shape, pcap, n_features, max_points_per_frame)
         self._shapes()
         self._needs()
+        self.gather = self._gather_plan()
         self._allocate()
         self._prep_weights()
         self._build_ops()
@@ -305,6 +306,35 @@ class CompiledGraph:
                     for src in self.layer_src[name]:
                         self.values[src].slot = s
 
+    def _first_conv_desc(self, l, src, cs, off, fmt):
+        B, H, W, C = src.shape
+        _, Ho, Wo, Co = self.values[l.name].shape
+        kh, kw = l.weight.shape[2:]
+        (sh, sw), (ph, pw) = l.conv.stride, l.conv.padding
+        return N.ConvDesc(kind=N.PMX_CONV2D, in_dtype=_DT[fmt[0]], batch=B, in_h=H, in_w=W, in_c=C, in_c_stride=cs,
+                          in_c_offset=off, out_c=Co, k_h=kh, k_w=kw, stride_h=sh, stride_w=sw, pad_h=ph, pad_w=pw,
+                          out_h=Ho, out_w=Wo, relu=int(l.relu))
+
+    def _gather_plan(self):
+        """Virtual canvas: when the PFN output feeds exactly one conv in one int8/f16
+        format that the tcgen05 gather kernel covers, the PFN writes pillar rows and
+        that conv reads them through pillarize's cell map (pmx_conv_gather) -- the
+        scatter of pm/tensor_ops.py:138-160 happens in shared memory, never in HBM."""
+        if self.source != "points" or self.pfn is None:
+            return None
+        canvas = self.values[self.graph.layers[2].name]
+        cons = self.cons.get(canvas.name, [])
+        if len(cons) != 1 or cons[0].kind != "conv2d" or len(canvas.need) != 1:
+            return None
+        fmt = next(iter(canvas.need))
+        if fmt[0] not in ("int8", "fp16") or _fmt_of(cons[0], self.stats) != fmt:
+            return None
+        C = canvas.shape[3]
+        d = self._first_conv_desc(cons[0], canvas, C, 0, fmt)
+        if not self.lib.pmx_conv_gather_supported(ctypes.byref(d)):
+            return None
+        return {"layer": cons[0].name, "fmt": fmt}
+
     def _is_concat(self, name):
         for l in self.graph.layers:
             if l.name == name:
@@ -345,6 +375,11 @@ class CompiledGraph:
                 for f in v.need:
                     u.need[f] = None
                 off += u.shape[3]
+        if self.gather:
+            canvas = self.values[self.graph.layers[2].name]
+            fmt = self.gather["fmt"]
+            rows = self._empty((self.B * self.pcap, canvas.shape[3]), fmt)
+            canvas.bufs[fmt] = (rows, canvas.shape[3], 0)
         for name, v in self.values.items():
             if v.logical == "pfn":
                 continue
@@ -567,10 +602,14 @@ class CompiledGraph:
         pt_idx = self.pt_idx.data_ptr() if self.source == "points" else None
         pcap = max(self.pcap, 1)
 
+        fn = lib.pmx_pfn_scatter
+        if self.gather:
+            zero, fn = [], lib.pmx_pfn_pillars  # pillar rows; the consumer gathers them
+
         def run(s):
             for ptr_, nbytes in zero:
                 N.check(lib.pmx_zero(ptr_, nbytes, s), "zero canvas")
-            N.check(lib.pmx_pfn_scatter(
+            N.check(fn(
                 ctypes.byref(d), ctypes.byref(g), self.B, pcap, pts, offs, feats, mask, self.coords.data_ptr(),
                 self.counts.data_ptr(), pt_idx, self.n_pillars.data_ptr(), rec["w"].data_ptr(),
                 N.ptr(rec["alpha"]), rec["bias"].data_ptr(), N.ptr(rec["bn"]), arr, n, in_keys, out_keys, s),
@@ -616,6 +655,18 @@ class CompiledGraph:
         self.op_info[f"conv {l.name}"] = {
             "flops": 2.0 * m * n_gemm * k_gemm, "precision": rec["precision"],
             "bytes": B * H * W * C * esz[rec["precision"]] + n_gemm * k_gemm * esz[rec["precision"]] + out_bytes}
+        if self.gather and self.gather["layer"] == l.name:
+            g = self._keep[0]
+            cmap = lib.pmx_pillarize_cell_map(ctypes.byref(g), self.B, self.nmax, self.pws.data_ptr())
+            if not cmap:
+                raise RuntimeError("pmx_pillarize_cell_map failed")
+            pcap = self.pcap
+            self.op_info[f"conv {l.name}"]["bytes"] += (B * H * W * 4 - B * H * W * C * esz[rec["precision"]]
+                                                        + B * pcap * C * esz[rec["precision"]])
+            self.ops.append((f"conv {l.name}", lambda s: N.check(lib.pmx_conv_gather(
+                ctypes.byref(d), t.data_ptr(), cmap, pcap, rec["w"].data_ptr(), N.ptr(rec["alpha"]),
+                rec["bias"].data_ptr(), N.ptr(rec["bn"]), arr, n, keys, s), f"layer {l.name} (gather)")))
+            return
         ws_bytes = lib.pmx_conv_workspace(ctypes.byref(d))
         ws = self.torch.empty(max(ws_bytes, 1), dtype=self.torch.uint8, device="cuda")
         self._keep.append(ws)
