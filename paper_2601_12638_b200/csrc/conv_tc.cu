@@ -74,10 +74,12 @@ __device__ __forceinline__ void mbar_spin(uint32_t bar, uint32_t parity) {
   } while (!ok);
 }
 
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-  while (!mbar_try_sleep(bar, parity)) {
-  }
-}
+// Every role waits with the plain try_wait (the hardware suspends the warp inside
+// TRYWAIT and resumes it when the phase completes).  The suspend-time-hint form
+// compiles to TRYWAIT + NANOSLEEP.SYNCS, whose wake-up was measured (conv_trace) to
+// lag the barrier by up to ~6000 cycles -- epilogue warps of one tile started
+// thousands of cycles apart.
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) { mbar_spin(bar, parity); }
 
 __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t bar) {
   asm volatile(
@@ -250,6 +252,45 @@ constexpr int kEpiWarps = 16;                  // warps 2..17: four per TMEM lan
 constexpr int kThreads = 32 * (2 + kEpiWarps);  // + TMA producer warp + MMA warp
 constexpr int kGatherWarps = 3;                 // GATHER: warp 0 + warps 18, 19 build the halo tiles
 constexpr int kThreadsGather = kThreads + 32 * (kGatherWarps - 1);
+
+// 16 f32 values -> 16 exact int8 codes WITHOUT clamping: valid (returns true) when
+// every |q| < 127 and no q lies within the tie band of a half-integer -- then
+// rint(q) is already the code (pm/quant.py:98-103 semantics, no clip needed); NaN /
+// Inf / saturation / near-ties return false and the caller takes the exact path.
+// RELU: relu(y) then quantize == max(code, 0): negative bytes are zeroed with a
+// sign-replicating byte permute.  ~4.5 instructions per value.
+template <bool RELU>
+__device__ __forceinline__ bool quant16_noclamp(const float (&y)[16], float inv, uint4& out) {
+  const float2 M2 = make_float2(12582912.0f, 12582912.0f), I2 = make_float2(inv, inv);
+  uint32_t tb[16];
+  float dm = 0.0f, qm = 0.0f;
+#pragma unroll
+  for (int j = 0; j < 16; j += 2) {
+    const float2 q = __fmul2_rn(make_float2(y[j], y[j + 1]), I2);
+    const float2 t = __fadd2_rn(q, M2);                                  // rint(q) in the low bits
+    const float2 r = __fadd2_rn(t, make_float2(-12582912.0f, -12582912.0f));  // rint(q), exact
+    const float2 d = __fadd2_rn(q, make_float2(-r.x, -r.y));             // q - rint(q), exact
+    dm = fmax3_nan(dm, fabsf(d.x), fabsf(d.y));
+    qm = fmax3_nan(qm, fabsf(q.x), fabsf(q.y));
+    tb[j] = __float_as_uint(t.x);
+    tb[j + 1] = __float_as_uint(t.y);
+  }
+  uint32_t w[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    w[k] = __byte_perm(__byte_perm(tb[4 * k], tb[4 * k + 1], 0x0040), __byte_perm(tb[4 * k + 2], tb[4 * k + 3], 0x0040),
+                       0x5410);
+    if (RELU) {
+      // prmt with the sign-replicate bit (nibble msb) set: 0xFF where the byte is
+      // negative (the __byte_perm intrinsic drops that bit)
+      uint32_t sm;
+      asm("prmt.b32 %0, %1, 0, 0xBA98;" : "=r"(sm) : "r"(w[k]));
+      w[k] &= ~sm;
+    }
+  }
+  out = make_uint4(w[0], w[1], w[2], w[3]);
+  return dm < kTieBand && qm < 127.0f;
+}
 
 // One chunk (16 accumulator columns of one pixel row): y = acc * alpha + bias (int8)
 // or acc + bias (f16), optional unfolded BN and ReLU, observer min/max, then every
@@ -757,6 +798,12 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
     }
     float lo = __int_as_float(0x7f800000), hi = -lo;
     const float qlo = p.relu ? 0.0f : -128.0f;
+    // OUTK 1 fast path: consumer parameters in registers, kernel-uniform eligibility
+    int8_t* const o_ptr = reinterpret_cast<int8_t*>(outs.o[0].ptr) + outs.o[0].c_offset;
+    const int64_t o_cs = outs.o[0].c_stride;
+    const double o_scale = outs.o[0].scale;
+    const float o_inv = outs.o[0].inv;
+    const bool fast = OUTK == 1 && !p.bn_post && !p.keys && (p.n_gemm % 16) == 0;
     for (uint32_t i = (uint32_t)eg;; i += (uint32_t)egn) {
       const uint32_t t = blockIdx.x + i * gridDim.x;
       if (t >= (uint32_t)total) break;
@@ -812,6 +859,40 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
           }
           const uint32_t ddy = (uint32_t)tap >> p.st_shift, ddx = (uint32_t)tap & (uint32_t)(p.stride - 1);
           pix = (ib * p.out_h + iy * p.stride + ddy) * p.out_w + ix * p.stride + ddx;
+        }
+        if constexpr (OUTK == 1) {
+          if (fast) {
+            // one aligned int8 consumer, no unfolded BN / observer, full 16-column run
+            float y[16];
+            const float4* b4p = reinterpret_cast<const float4*>(s_bias + cobase);
+            const float4* a4p = reinterpret_cast<const float4*>(s_alpha + cobase);
+#pragma unroll
+            for (int j4 = 0; j4 < 4; ++j4) {
+              const float4 b4 = b4p[j4];
+              float2 r0, r1;
+              if constexpr (DT == PMX_I8) {
+                const float4 a4 = a4p[j4];
+                r0 = __ffma2_rn(make_float2((float)(int)v[4 * j4], (float)(int)v[4 * j4 + 1]),
+                                make_float2(a4.x, a4.y), make_float2(b4.x, b4.y));
+                r1 = __ffma2_rn(make_float2((float)(int)v[4 * j4 + 2], (float)(int)v[4 * j4 + 3]),
+                                make_float2(a4.z, a4.w), make_float2(b4.z, b4.w));
+              } else {
+                r0 = __fadd2_rn(make_float2(__uint_as_float(v[4 * j4]), __uint_as_float(v[4 * j4 + 1])),
+                                make_float2(b4.x, b4.y));
+                r1 = __fadd2_rn(make_float2(__uint_as_float(v[4 * j4 + 2]), __uint_as_float(v[4 * j4 + 3])),
+                                make_float2(b4.z, b4.w));
+              }
+              y[4 * j4] = r0.x;
+              y[4 * j4 + 1] = r0.y;
+              y[4 * j4 + 2] = r1.x;
+              y[4 * j4 + 3] = r1.y;
+            }
+            uint4 code;
+            const bool ok = p.relu ? quant16_noclamp<true>(y, o_inv, code) : quant16_noclamp<false>(y, o_inv, code);
+            if (!ok) code = quant16(y, o_scale, o_inv, qlo);
+            *reinterpret_cast<uint4*>(o_ptr + (size_t)pix * o_cs + cobase) = code;
+            continue;
+          }
         }
         epi_chunk<DT, OUTK>(p, outs, v, pix, nbase, cobase, s_alpha, s_bias, qlo, lo, hi);
       }

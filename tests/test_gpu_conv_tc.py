@@ -101,3 +101,56 @@ def test_tcgen05_matches_simt(case, prec, tc_mode):
         assert float((a - b).norm() / b.norm()) <= 1e-5
         codes = (tc[1].int() - ref[1].int()).abs()
         assert int(codes.max()) <= 1 and float((codes != 0).float().mean()) < 1e-3
+
+
+@pytest.mark.parametrize("case", CASES, ids=lambda c: f"{c[0]}{c[1]}x{c[2]}k{c[3]}s{c[4]}_{c[5][0]}x{c[5][1]}")
+@pytest.mark.parametrize("relu", [1, 0])
+def test_tcgen05_single_int8_consumer(case, relu):
+    """The OUTK=1 epilogue (one 16-byte aligned int8 consumer: the clamp-free fast
+    quantizer with the byte-permute ReLU, and its exact fallback) vs the SIMT kernel,
+    bit for bit, with scales chosen so that codes saturate and hit exact .5 ties."""
+    import torch
+
+    from paper_2601_12638_b200 import _native as N
+
+    lib = N.load()
+    kind, cin, cout, k, s, (h, w), batch = case
+    if cout % 16:
+        pytest.skip("OUTK=1 needs 16-byte aligned rows")
+    rng = np.random.default_rng(cin * 11 + cout + k + s + h + relu)
+    deconv = kind == "deconv"
+    if deconv:
+        oh, ow, wshape = h * s, w * s, (k * k * cout, cin)
+    else:
+        pad = 1 if k == 3 else 0
+        oh, ow, wshape = (h + 2 * pad - k) // s + 1, (w + 2 * pad - k) // s + 1, (cout, k * k * cin)
+    desc = N.ConvDesc(kind=N.PMX_DECONV2D if deconv else N.PMX_CONV2D, in_dtype=N.PMX_I8, batch=batch, in_h=h,
+                      in_w=w, in_c=cin, in_c_stride=cin, in_c_offset=0, out_c=cout, k_h=k, k_w=k, stride_h=s,
+                      stride_w=s, pad_h=0 if deconv or k == 1 else 1, pad_w=0 if deconv or k == 1 else 1,
+                      out_h=oh, out_w=ow, relu=relu)
+    x = torch.from_numpy(rng.integers(-128, 128, size=(batch, h, w, cin), dtype=np.int8)).cuda()
+    wt = torch.from_numpy(rng.integers(-128, 128, size=wshape, dtype=np.int8)).cuda()
+    # alpha = 2^-12: y = acc / 4096 + bias, with bias multiples of 1/8 and scale 1/2
+    # many y/s land exactly on .5 ties; the wide accumulator range saturates codes
+    kdim = wshape[1]
+    alpha = torch.full((cout,), 2.0 ** (-9 if kdim <= 128 else -12), dtype=torch.float32, device="cuda")
+    bias = torch.from_numpy((rng.integers(-8, 8, cout) / 8.0).astype(np.float32)).cuda()
+    outs = []
+    for mode in (0, 1):
+        y = torch.full((batch, oh, ow, cout), 99, dtype=torch.int8, device="cuda")
+        arr, n = N.outs_array([N.Out(ptr=y.data_ptr(), scale=0.5, dtype=N.PMX_I8, c_stride=cout, c_offset=0)])
+        lib.pmx_set_conv_backend(mode)
+        try:
+            N.check(lib.pmx_conv(ctypes.byref(desc), x.data_ptr(), wt.data_ptr(), alpha.data_ptr(), bias.data_ptr(),
+                                 None, arr, n, None, None, 0, N.stream_ptr()), "conv")
+            torch.cuda.synchronize()
+        finally:
+            lib.pmx_set_conv_backend(0)
+        outs.append(y)
+    assert torch.equal(outs[0], outs[1]), (outs[0].int() - outs[1].int()).abs().max()
+    c = outs[0].int()
+    assert int((c == 127).sum()) > 0 and int((c != 0).sum()) > 0
+    if relu:
+        assert int(c.min()) == 0
+    else:
+        assert int(c.min()) < 0
