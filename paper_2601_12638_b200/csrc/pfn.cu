@@ -13,6 +13,8 @@
 // pm/tensor_ops.py:80-91, relu :134, max_over_points :163-173, scatter :138-160.
 // INT8: features and weights are integer codes; the 9-term dot product of codes
 // (|sum| < 2^18) is exact in f32 FMA, then y = fma(acc, s_x * s_w[c], bias[c]).
+#include <type_traits>
+
 #include "pmx_common.cuh"
 
 namespace pmx {
@@ -217,10 +219,268 @@ __global__ void __launch_bounds__(kThreads) pfn_kernel(const PfnArgs a, const Ou
   }
 }
 
+// POINTS9 path.  A warp takes 32 pillars.
+//  Phase A (lane = pillar): counts, coords, the first kSlots points (independent
+//   gathers in flight together), the cluster mean as the sequential f32 sum in slot
+//   order (numpy's chunk.mean, bit for bit), the 9 features (observer), layer 1's
+//   transform -> shared memory.
+//  Phase B (lane = output channel pair 2l, 2l+1; weights in registers): for each of the
+//   32 pillars, the FMA chain over the features (broadcast shared-memory reads) and the
+//   max over points; epilogue once per pillar; 128-byte coalesced row stores.
+// Points beyond kSlots (dense clusters, M up to 32) are rebuilt in phase B.
+constexpr int kSlots = 8;
+// one point record = the 9 transformed features in layer 1's storage type, padded to
+// whole 16-byte rows: int8 codes 16 B, binary16 32 B, f32 48 B
+template <int DT>
+struct Rec {
+  using T = typename std::conditional<DT == PMX_I8, int8_t, typename std::conditional<DT == PMX_F16, __half, float>::type>::type;
+  static constexpr int N = DT == PMX_I8 ? 16 : (DT == PMX_F16 ? 16 : 12);  // elements per record
+  static constexpr int BYTES = N * (int)sizeof(T);
+};
+template <int DT>
+constexpr size_t pfn_points_smem() {
+  return (size_t)(kThreads / 32) * 32 * kSlots * Rec<DT>::BYTES + (size_t)(kThreads / 32) * 32 * 6 * 4;
+}
+
+__device__ __forceinline__ void store2(const OutDev& o, int64_t pix, int c, float y0, float y1, bool two) {
+  const int64_t off = pix * o.c_stride + o.c_offset + c;
+  if (o.dtype == PMX_F16 && two && (off & 1) == 0) {
+    const __half2 h = __halves2half2(f16_sat(y0), f16_sat(y1));
+    *reinterpret_cast<__half2*>(reinterpret_cast<__half*>(o.ptr) + off) = h;
+  } else if (o.dtype == PMX_I8 && two && (off & 1) == 0) {
+    const int a = quantize_exact(y0, o.scale, o.inv), b = quantize_exact(y1, o.scale, o.inv);
+    *reinterpret_cast<uint16_t*>(reinterpret_cast<int8_t*>(o.ptr) + off) = (uint16_t)((a & 0xff) | ((b & 0xff) << 8));
+  } else if (o.dtype == PMX_F32 && two && (off & 1) == 0) {
+    *reinterpret_cast<float2*>(reinterpret_cast<float*>(o.ptr) + off) = make_float2(y0, y1);
+  } else {
+    store_one(o, pix, c, y0);
+    if (two) store_one(o, pix, c + 1, y1);
+  }
+}
+
+template <int DT>
+__global__ void __launch_bounds__(kThreads) pfn_points_kernel(const PfnArgs a, const Outs outs) {
+  using R = Rec<DT>;
+  using T = typename R::T;
+  extern __shared__ __align__(16) uint8_t pfn_smem[];
+  // [warp][pillar][slot] records, then [warp][pillar][6] slow-path metadata
+  T (*sf)[32][kSlots][R::N] = reinterpret_cast<T (*)[32][kSlots][R::N]>(pfn_smem);
+  float (*smeta)[32][6] =
+      reinterpret_cast<float (*)[32][6]>(pfn_smem + (size_t)(kThreads / 32) * 32 * kSlots * R::BYTES);
+  const int b = blockIdx.y;
+  const int C = a.d.channels;
+  const int M = a.d.max_points;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int P = a.n_pillars[b];
+  const int64_t hw = (int64_t)a.g.grid_h * a.g.grid_w;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    const uint32_t zk = f2key(0.0f);
+    if (a.out_keys && P < hw) {  // empty cells stay 0 on the canvas
+      atomicMin(a.out_keys + 0, zk);
+      atomicMax(a.out_keys + 1, zk);
+    }
+    if (a.in_keys && P == 0) {  // record() of an empty tensor is (0, 0)
+      atomicMin(a.in_keys + 0, zk);
+      atomicMax(a.in_keys + 1, zk);
+    }
+  }
+  const float INF = __int_as_float(0x7f800000);
+  const float4* fp = a.points + a.offs[b];
+  const float xoff = (float)((double)a.g.cell_w * 0.5 + (double)a.g.x_min);
+  const float yoff = (float)((double)a.g.cell_h * 0.5 + (double)a.g.y_min);
+  // ---------------- phase A: lane = pillar
+  const int p = (blockIdx.x * (kThreads / 32) + warp) * 32 + lane;
+  const bool live = p < P;
+  const int64_t q = (int64_t)b * a.pcap + (live ? p : 0);
+  const int k = live ? a.counts[q] : 0;
+  const int32_t* idx = a.pt_idx + q * M;
+  float in_lo = INF, in_hi = -INF;
+  float4 pts[kSlots];
+#pragma unroll
+  for (int s = 0; s < kSlots; ++s) pts[s] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+  for (int s = 0; s < kSlots; ++s)
+    if (s < k) pts[s] = __ldg(fp + __ldg(idx + s));
+  float sx = 0.f, sy = 0.f, sz = 0.f;
+#pragma unroll
+  for (int s = 0; s < kSlots; ++s)
+    if (s < k) {
+      sx = __fadd_rn(sx, pts[s].x);
+      sy = __fadd_rn(sy, pts[s].y);
+      sz = __fadd_rn(sz, pts[s].z);
+    }
+  for (int s = kSlots; s < k; ++s) {  // dense cluster tail, still in slot order
+    const float4 pt = __ldg(fp + __ldg(idx + s));
+    sx = __fadd_rn(sx, pt.x);
+    sy = __fadd_rn(sy, pt.y);
+    sz = __fadd_rn(sz, pt.z);
+  }
+  const float fk = (float)(k > 0 ? k : 1);
+  const float mxm = __fdiv_rn(sx, fk), mym = __fdiv_rn(sy, fk), mzm = __fdiv_rn(sz, fk);
+  float xc = 0.f, yc = 0.f;
+  if (live) {
+    const int2 cc = *reinterpret_cast<const int2*>(a.coords + 2 * q);
+    xc = __fadd_rn(__fmul_rn((float)cc.y, a.g.cell_w), xoff);
+    yc = __fadd_rn(__fmul_rn((float)cc.x, a.g.cell_h), yoff);
+  }
+  if (live && k < M) { in_lo = 0.f; in_hi = 0.f; }  // zero padding rows are part of layer 1's input
+  auto feats = [&](const float4& pt, float (&f)[9]) {
+    f[0] = pt.x; f[1] = pt.y; f[2] = pt.z; f[3] = pt.w;
+    f[4] = __fsub_rn(pt.x, mxm); f[5] = __fsub_rn(pt.y, mym); f[6] = __fsub_rn(pt.z, mzm);
+    f[7] = __fsub_rn(pt.x, xc); f[8] = __fsub_rn(pt.y, yc);
+  };
+#pragma unroll
+  for (int s = 0; s < kSlots; ++s) {
+    if (s < k) {
+      float f[9];
+      feats(pts[s], f);
+      if (a.in_keys) {
+#pragma unroll
+        for (int j = 0; j < 9; ++j) { in_lo = nmin(in_lo, f[j]); in_hi = nmax(in_hi, f[j]); }
+      }
+      T* dst = sf[warp][lane][s];
+#pragma unroll
+      for (int j = 0; j < 9; ++j) {
+        const float v = transform_in<DT>(f[j], a);  // exactly representable in T
+        if constexpr (DT == PMX_I8) dst[j] = (int8_t)(int)v;
+        else if constexpr (DT == PMX_F16) dst[j] = __float2half_rn(v);
+        else dst[j] = v;
+      }
+    }
+  }
+  if (k > kSlots) {
+    smeta[warp][lane][0] = mxm; smeta[warp][lane][1] = mym; smeta[warp][lane][2] = mzm;
+    smeta[warp][lane][3] = xc; smeta[warp][lane][4] = yc;
+    if (a.in_keys) {
+      for (int s = kSlots; s < k; ++s) {
+        float f[9];
+        feats(__ldg(fp + __ldg(idx + s)), f);
+#pragma unroll
+        for (int j = 0; j < 9; ++j) { in_lo = nmin(in_lo, f[j]); in_hi = nmax(in_hi, f[j]); }
+      }
+    }
+  }
+  __syncwarp();
+  // ---------------- phase B: lane = channels (c, c + 1)
+  const int c = 2 * lane;
+  const bool has0 = c < C, has1 = c + 1 < C;
+  float w0[9], w1[9];
+#pragma unroll
+  for (int j = 0; j < 9; ++j) {
+    auto wat = [&](int cc) -> float {
+      if (cc >= C) return 0.f;
+      if constexpr (DT == PMX_I8) return (float)reinterpret_cast<const int8_t*>(a.weight)[cc * 9 + j];
+      else if constexpr (DT == PMX_F16) return __half2float(reinterpret_cast<const __half*>(a.weight)[cc * 9 + j]);
+      else return reinterpret_cast<const float*>(a.weight)[cc * 9 + j];
+    };
+    w0[j] = wat(c);
+    w1[j] = wat(c + 1);
+  }
+  const float al0 = (DT == PMX_I8 && has0) ? a.alpha[c] : 1.f, al1 = (DT == PMX_I8 && has1) ? a.alpha[c + 1] : 1.f;
+  const float bi0 = has0 ? a.bias[c] : 0.f, bi1 = has1 ? a.bias[c + 1] : 0.f;
+  float o_lo = INF, o_hi = -INF;
+  for (int j = 0; j < 32; ++j) {
+    const int kj = __shfl_sync(0xffffffffu, k, j);
+    if (kj == 0) continue;  // warp-uniform
+    const int64_t qj = __shfl_sync(0xffffffffu, q, j);
+    float m0 = -INF, m1 = -INF;
+    auto point = [&](const float (&f)[9]) {
+      float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int t = 0; t < 9; ++t) acc = __ffma2_rn(make_float2(f[t], f[t]), make_float2(w0[t], w1[t]), acc);
+      if (a.bn_post == nullptr) {
+        m0 = nmax(m0, acc.x);
+        m1 = nmax(m1, acc.y);
+      } else {  // unfolded BN may have a negative gamma: finish every point
+        float y0, y1;
+        if constexpr (DT == PMX_I8) {
+          y0 = __fmaf_rn(acc.x, al0, bi0);
+          y1 = __fmaf_rn(acc.y, al1, bi1);
+        } else {
+          y0 = __fadd_rn(acc.x, bi0);
+          y1 = __fadd_rn(acc.y, bi1);
+        }
+        if (has0) y0 = __fadd_rn(__fmul_rn(__fsub_rn(y0, a.bn_post[c]), a.bn_post[C + c]), a.bn_post[2 * C + c]);
+        if (has1)
+          y1 = __fadd_rn(__fmul_rn(__fsub_rn(y1, a.bn_post[c + 1]), a.bn_post[C + c + 1]), a.bn_post[2 * C + c + 1]);
+        if (a.d.relu) { y0 = fmaxf(y0, 0.f); y1 = fmaxf(y1, 0.f); }
+        m0 = nmax(m0, y0);
+        m1 = nmax(m1, y1);
+      }
+    };
+    const int kk = kj < kSlots ? kj : kSlots;
+    for (int s = 0; s < kk; ++s) {
+      float f[9];
+      const uint4* src = reinterpret_cast<const uint4*>(sf[warp][j][s]);  // broadcast reads
+      if constexpr (DT == PMX_I8) {
+        const uint4 r = src[0];
+        const uint32_t w[3] = {r.x, r.y, r.z};
+#pragma unroll
+        for (int t = 0; t < 9; ++t) f[t] = (float)(int8_t)((w[t >> 2] >> (8 * (t & 3))) & 0xff);
+      } else if constexpr (DT == PMX_F16) {
+        const uint4 r0 = src[0], r1 = src[1];
+        const uint32_t w[5] = {r0.x, r0.y, r0.z, r0.w, r1.x};
+#pragma unroll
+        for (int t = 0; t < 9; ++t) f[t] = __half2float(__ushort_as_half((unsigned short)(w[t >> 1] >> (16 * (t & 1)))));
+      } else {
+        const float4 f0 = reinterpret_cast<const float4*>(src)[0], f1 = reinterpret_cast<const float4*>(src)[1],
+                     f2 = reinterpret_cast<const float4*>(src)[2];
+        f[0] = f0.x; f[1] = f0.y; f[2] = f0.z; f[3] = f0.w; f[4] = f1.x; f[5] = f1.y; f[6] = f1.z; f[7] = f1.w;
+        f[8] = f2.x;
+      }
+      point(f);
+    }
+    if (kj > kSlots) {  // dense cluster: rebuild the remaining points (every lane, broadcast loads)
+      const float* mt = smeta[warp][j];
+      const int32_t* idj = a.pt_idx + qj * M;
+      for (int s = kSlots; s < kj; ++s) {
+        const float4 pt = __ldg(fp + __ldg(idj + s));
+        float f[9];
+        f[0] = pt.x; f[1] = pt.y; f[2] = pt.z; f[3] = pt.w;
+        f[4] = __fsub_rn(pt.x, mt[0]); f[5] = __fsub_rn(pt.y, mt[1]); f[6] = __fsub_rn(pt.z, mt[2]);
+        f[7] = __fsub_rn(pt.x, mt[3]); f[8] = __fsub_rn(pt.y, mt[4]);
+#pragma unroll
+        for (int t = 0; t < 9; ++t) f[t] = transform_in<DT>(f[t], a);
+        point(f);
+      }
+    }
+    float y0 = m0, y1 = m1;
+    if (a.bn_post == nullptr) {
+      if constexpr (DT == PMX_I8) {
+        y0 = __fmaf_rn(m0, al0, bi0);
+        y1 = __fmaf_rn(m1, al1, bi1);
+      } else {
+        y0 = __fadd_rn(m0, bi0);
+        y1 = __fadd_rn(m1, bi1);
+      }
+      if (a.d.relu) { y0 = fmaxf(y0, 0.f); y1 = fmaxf(y1, 0.f); }
+    }
+    if (has0) {
+      int64_t pix = qj;
+      if (!a.dense) {
+        const int2 cc = *reinterpret_cast<const int2*>(a.coords + 2 * qj);
+        pix = ((int64_t)b * a.g.grid_h + cc.x) * a.g.grid_w + cc.y;
+      }
+#pragma unroll
+      for (int o = 0; o < PMX_MAX_OUTS; ++o)
+        if (o < outs.n) store2(outs.o[o], pix, c, y0, y1, has1);
+      if (a.out_keys) {
+        o_lo = nmin(o_lo, y0); o_hi = nmax(o_hi, y0);
+        if (has1) { o_lo = nmin(o_lo, y1); o_hi = nmax(o_hi, y1); }
+      }
+    }
+  }
+  if (a.in_keys) block_minmax_commit<kThreads>(in_lo, in_hi, a.in_keys);
+  if (a.out_keys) block_minmax_commit<kThreads>(o_lo, o_hi, a.out_keys);
+}
+
 template <int DT>
 pmx_status launch_dt(const PfnArgs& a, const Outs& outs, dim3 grid, cudaStream_t st) {
   if (a.d.source == PMX_PFN_FROM_POINTS9) {
-    pfn_kernel<DT, 9, true><<<grid, kThreads, 0, st>>>(a, outs);
+    const dim3 g2((unsigned)ceil_div(a.pcap, kThreads), grid.y);  // 32 pillars per warp
+    const size_t sm = pfn_points_smem<DT>();
+    PMX_CUDA(cudaFuncSetAttribute(pfn_points_kernel<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    pfn_points_kernel<DT><<<g2, kThreads, sm, st>>>(a, outs);
   } else {
     switch (a.d.n_features) {
 #define PMX_F_CASE(N) \

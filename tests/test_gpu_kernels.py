@@ -238,3 +238,78 @@ def test_decode_topk_exact_index_set(pm, H, W, k, ties):
     np.testing.assert_allclose(out["boxes"][0].cpu().numpy()[:kk], boxes, rtol=2e-6, atol=2e-6)
     if kk < k:
         assert (out["idx"][0].cpu().numpy()[kk:] == -1).all()
+
+
+# ----------------------------------------------------------------------------- PFN (K4)
+
+
+@pytest.mark.parametrize("prec", ["int8", "fp16", "fp32"])
+@pytest.mark.parametrize("clustered", [False, True])
+def test_pfn_pillar_rows_vs_oracle(pm, prec, clustered):
+    """pmx_pfn_pillars (the 9-feature PFN: transform -> linear -> bias -> ReLU -> max over
+    points, one f32 row per pillar) vs a numpy restatement on the oracle's pillar
+    features; clustered frames put up to 32 points in a pillar (the kernel keeps 8 per
+    pillar in shared memory and rebuilds the rest)."""
+    import ctypes
+
+    import torch
+
+    from paper_2601_12638_b200 import _native as N
+
+    cfg = pm.PointPillarsConfig.small(max_pillars=800)
+    pts = _kitti_case(pm, 4000, 21, cfg, clustered)
+    spec = cfg.grid_spec()
+    want_idx = O.pillar_index(O.bin_points(pts[:, :2], spec.grid, spec.origin, spec.cell), spec.grid, 32, 800)
+    feats, mask = O.pillar_features9(pts, want_idx, spec.origin, spec.cell)
+    P = len(want_idx.coords)
+    assert (want_idx.counts.max() > 8) == clustered
+    rng = np.random.default_rng(3)
+    C = 64
+    w = rng.normal(scale=0.3, size=(C, 9)).astype(np.float32)
+    bias = rng.normal(scale=0.1, size=C).astype(np.float32)
+    in_scale = float(np.abs(feats).max() / 127.0)
+    if prec == "int8":
+        xq = O.quantize(feats, in_scale).astype(np.float64)
+        ws = np.abs(w).max(axis=1) / 127.0
+        wq = np.rint(w.astype(np.float64) / ws[:, None]).clip(-128, 127)
+        acc = np.einsum("pmj,cj->pmc", xq, wq)  # exact integers
+        alpha = (in_scale * ws).astype(np.float32)
+        y = (acc * alpha.astype(np.float64) + bias).astype(np.float32)
+        wdev = torch.from_numpy(wq.astype(np.int8)).cuda()
+        adev = torch.from_numpy(alpha).cuda()
+    else:
+        x = feats if prec == "fp32" else O.fp16_roundtrip(feats)
+        wv = w if prec == "fp32" else O.fp16_roundtrip(w)
+        y = (np.einsum("pmj,cj->pmc", x.astype(np.float64), wv.astype(np.float64)) + bias).astype(np.float32)
+        wdev = torch.from_numpy(wv if prec == "fp32" else wv.astype(np.float16)).cuda()
+        adev = None
+    y = np.maximum(y, 0)
+    y = np.where(mask[:, :, None], y, -np.inf).max(axis=1)  # [P, C]
+    # device pipeline: pillarize -> PFN rows
+    lib = N.load()
+    g = spec_c = pm.engine.GridSpec(grid=spec.grid, origin=spec.origin, cell=spec.cell, max_points=32,
+                                    max_pillars=800).to_c()
+    dpts = torch.from_numpy(pts).cuda()
+    offs = torch.tensor([0, len(pts)], dtype=torch.int64, device="cuda")
+    coords = torch.empty((1, 800, 2), dtype=torch.int32, device="cuda")
+    counts = torch.empty((1, 800), dtype=torch.int32, device="cuda")
+    pt_idx = torch.empty((1, 800, 32), dtype=torch.int32, device="cuda")
+    npil = torch.empty((1,), dtype=torch.int32, device="cuda")
+    wsb = lib.pmx_pillarize_workspace(ctypes.byref(g), 1, len(pts))
+    ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+    N.check(lib.pmx_pillarize(dpts.data_ptr(), offs.data_ptr(), 1, len(pts), ctypes.byref(g), 800, coords.data_ptr(),
+                              counts.data_ptr(), pt_idx.data_ptr(), npil.data_ptr(), ws.data_ptr(), wsb,
+                              N.stream_ptr()), "pillarize")
+    rows = torch.full((800, C), -7.0, dtype=torch.float32, device="cuda")
+    arr, n = N.outs_array([N.Out(ptr=rows.data_ptr(), scale=0.0, dtype=N.PMX_F32, c_stride=C, c_offset=0)])
+    d = N.PfnDesc(source=N.PMX_PFN_FROM_POINTS9, in_dtype=N.DTYPE_CODE[prec], n_features=9, channels=C,
+                  max_points=32, relu=1, in_scale=in_scale if prec == "int8" else 0.0)
+    bdev = torch.from_numpy(bias).cuda()
+    N.check(lib.pmx_pfn_pillars(ctypes.byref(d), ctypes.byref(g), 1, 800, dpts.data_ptr(), offs.data_ptr(), None,
+                                None, coords.data_ptr(), counts.data_ptr(), pt_idx.data_ptr(), npil.data_ptr(),
+                                wdev.data_ptr(), N.ptr(adev), bdev.data_ptr(), None, arr, n, None, None,
+                                N.stream_ptr()), "pfn_pillars")
+    got = rows.cpu().numpy()
+    assert int(npil.item()) == P
+    np.testing.assert_allclose(got[:P], y, rtol=1e-5, atol=1e-5)
+    assert (got[P:] == -7.0).all()  # rows past n_pillars untouched
