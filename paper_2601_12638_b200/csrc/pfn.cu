@@ -259,7 +259,7 @@ __device__ __forceinline__ void store2(const OutDev& o, int64_t pix, int c, floa
 }
 
 template <int DT>
-__global__ void __launch_bounds__(kThreads) pfn_points_kernel(const PfnArgs a, const Outs outs) {
+__global__ void __launch_bounds__(kThreads, 3) pfn_points_kernel(const PfnArgs a, const Outs outs) {
   using R = Rec<DT>;
   using T = typename R::T;
   extern __shared__ __align__(16) uint8_t pfn_smem[];
@@ -361,67 +361,76 @@ __global__ void __launch_bounds__(kThreads) pfn_points_kernel(const PfnArgs a, c
     }
   }
   __syncwarp();
-  // ---------------- phase B: lane = channels (c, c + 1)
-  const int c = 2 * lane;
-  const bool has0 = c < C, has1 = c + 1 < C;
-  float w0[9], w1[9];
+  // ---------------- phase B: two pillars per step; lane = (pillar half, 4 channels)
+  const int half = lane >> 4;
+  const int c = 4 * (lane & 15);
+  float w[4][9];
 #pragma unroll
-  for (int j = 0; j < 9; ++j) {
-    auto wat = [&](int cc) -> float {
-      if (cc >= C) return 0.f;
-      if constexpr (DT == PMX_I8) return (float)reinterpret_cast<const int8_t*>(a.weight)[cc * 9 + j];
-      else if constexpr (DT == PMX_F16) return __half2float(reinterpret_cast<const __half*>(a.weight)[cc * 9 + j]);
-      else return reinterpret_cast<const float*>(a.weight)[cc * 9 + j];
-    };
-    w0[j] = wat(c);
-    w1[j] = wat(c + 1);
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int j = 0; j < 9; ++j) {
+      const int cc = c + u;
+      float v = 0.f;
+      if (cc < C) {
+        if constexpr (DT == PMX_I8) v = (float)reinterpret_cast<const int8_t*>(a.weight)[cc * 9 + j];
+        else if constexpr (DT == PMX_F16) v = __half2float(reinterpret_cast<const __half*>(a.weight)[cc * 9 + j]);
+        else v = reinterpret_cast<const float*>(a.weight)[cc * 9 + j];
+      }
+      w[u][j] = v;
+    }
+  float al[4], bi[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    al[u] = (DT == PMX_I8 && c + u < C) ? a.alpha[c + u] : 1.f;
+    bi[u] = c + u < C ? a.bias[c + u] : 0.f;
   }
-  const float al0 = (DT == PMX_I8 && has0) ? a.alpha[c] : 1.f, al1 = (DT == PMX_I8 && has1) ? a.alpha[c + 1] : 1.f;
-  const float bi0 = has0 ? a.bias[c] : 0.f, bi1 = has1 ? a.bias[c + 1] : 0.f;
   float o_lo = INF, o_hi = -INF;
-  for (int j = 0; j < 32; ++j) {
+  for (int it = 0; it < 16; ++it) {
+    const int j = 2 * it + half;
     const int kj = __shfl_sync(0xffffffffu, k, j);
-    if (kj == 0) continue;  // warp-uniform
+    const int kpair = max(kj, __shfl_xor_sync(0xffffffffu, kj, 16));
+    if (kpair == 0) continue;  // warp-uniform
     const int64_t qj = __shfl_sync(0xffffffffu, q, j);
-    float m0 = -INF, m1 = -INF;
+    float m[4] = {-INF, -INF, -INF, -INF};
     auto point = [&](const float (&f)[9]) {
-      float2 acc = make_float2(0.f, 0.f);
+      float2 acc01 = make_float2(0.f, 0.f), acc23 = make_float2(0.f, 0.f);
 #pragma unroll
-      for (int t = 0; t < 9; ++t) acc = __ffma2_rn(make_float2(f[t], f[t]), make_float2(w0[t], w1[t]), acc);
+      for (int t = 0; t < 9; ++t) {
+        acc01 = __ffma2_rn(make_float2(f[t], f[t]), make_float2(w[0][t], w[1][t]), acc01);
+        acc23 = __ffma2_rn(make_float2(f[t], f[t]), make_float2(w[2][t], w[3][t]), acc23);
+      }
+      const float acc[4] = {acc01.x, acc01.y, acc23.x, acc23.y};
       if (a.bn_post == nullptr) {
-        m0 = nmax(m0, acc.x);
-        m1 = nmax(m1, acc.y);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) m[u] = nmax(m[u], acc[u]);
       } else {  // unfolded BN may have a negative gamma: finish every point
-        float y0, y1;
-        if constexpr (DT == PMX_I8) {
-          y0 = __fmaf_rn(acc.x, al0, bi0);
-          y1 = __fmaf_rn(acc.y, al1, bi1);
-        } else {
-          y0 = __fadd_rn(acc.x, bi0);
-          y1 = __fadd_rn(acc.y, bi1);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          float y;
+          if constexpr (DT == PMX_I8) y = __fmaf_rn(acc[u], al[u], bi[u]);
+          else y = __fadd_rn(acc[u], bi[u]);
+          if (c + u < C)
+            y = __fadd_rn(__fmul_rn(__fsub_rn(y, a.bn_post[c + u]), a.bn_post[C + c + u]), a.bn_post[2 * C + c + u]);
+          if (a.d.relu) y = fmaxf(y, 0.f);
+          m[u] = nmax(m[u], y);
         }
-        if (has0) y0 = __fadd_rn(__fmul_rn(__fsub_rn(y0, a.bn_post[c]), a.bn_post[C + c]), a.bn_post[2 * C + c]);
-        if (has1)
-          y1 = __fadd_rn(__fmul_rn(__fsub_rn(y1, a.bn_post[c + 1]), a.bn_post[C + c + 1]), a.bn_post[2 * C + c + 1]);
-        if (a.d.relu) { y0 = fmaxf(y0, 0.f); y1 = fmaxf(y1, 0.f); }
-        m0 = nmax(m0, y0);
-        m1 = nmax(m1, y1);
       }
     };
-    const int kk = kj < kSlots ? kj : kSlots;
-    for (int s = 0; s < kk; ++s) {
+    const int kk = kpair < kSlots ? kpair : kSlots;
+    for (int s2 = 0; s2 < kk; ++s2) {
+      if (s2 >= kj) continue;
       float f[9];
-      const uint4* src = reinterpret_cast<const uint4*>(sf[warp][j][s]);  // broadcast reads
+      const uint4* src = reinterpret_cast<const uint4*>(sf[warp][j][s2]);  // two broadcast addresses
       if constexpr (DT == PMX_I8) {
         const uint4 r = src[0];
-        const uint32_t w[3] = {r.x, r.y, r.z};
+        const uint32_t wd[3] = {r.x, r.y, r.z};
 #pragma unroll
-        for (int t = 0; t < 9; ++t) f[t] = (float)(int8_t)((w[t >> 2] >> (8 * (t & 3))) & 0xff);
+        for (int t = 0; t < 9; ++t) f[t] = (float)(int8_t)((wd[t >> 2] >> (8 * (t & 3))) & 0xff);
       } else if constexpr (DT == PMX_F16) {
         const uint4 r0 = src[0], r1 = src[1];
-        const uint32_t w[5] = {r0.x, r0.y, r0.z, r0.w, r1.x};
+        const uint32_t wd[5] = {r0.x, r0.y, r0.z, r0.w, r1.x};
 #pragma unroll
-        for (int t = 0; t < 9; ++t) f[t] = __half2float(__ushort_as_half((unsigned short)(w[t >> 1] >> (16 * (t & 1)))));
+        for (int t = 0; t < 9; ++t) f[t] = __half2float(__ushort_as_half((unsigned short)(wd[t >> 1] >> (16 * (t & 1)))));
       } else {
         const float4 f0 = reinterpret_cast<const float4*>(src)[0], f1 = reinterpret_cast<const float4*>(src)[1],
                      f2 = reinterpret_cast<const float4*>(src)[2];
@@ -430,11 +439,12 @@ __global__ void __launch_bounds__(kThreads) pfn_points_kernel(const PfnArgs a, c
       }
       point(f);
     }
-    if (kj > kSlots) {  // dense cluster: rebuild the remaining points (every lane, broadcast loads)
+    if (kpair > kSlots) {  // dense cluster: rebuild the remaining points (broadcast loads per half)
       const float* mt = smeta[warp][j];
       const int32_t* idj = a.pt_idx + qj * M;
-      for (int s = kSlots; s < kj; ++s) {
-        const float4 pt = __ldg(fp + __ldg(idj + s));
+      for (int s2 = kSlots; s2 < kpair; ++s2) {
+        if (s2 >= kj) continue;
+        const float4 pt = __ldg(fp + __ldg(idj + s2));
         float f[9];
         f[0] = pt.x; f[1] = pt.y; f[2] = pt.z; f[3] = pt.w;
         f[4] = __fsub_rn(pt.x, mt[0]); f[5] = __fsub_rn(pt.y, mt[1]); f[6] = __fsub_rn(pt.z, mt[2]);
@@ -444,30 +454,44 @@ __global__ void __launch_bounds__(kThreads) pfn_points_kernel(const PfnArgs a, c
         point(f);
       }
     }
-    float y0 = m0, y1 = m1;
-    if (a.bn_post == nullptr) {
-      if constexpr (DT == PMX_I8) {
-        y0 = __fmaf_rn(m0, al0, bi0);
-        y1 = __fmaf_rn(m1, al1, bi1);
-      } else {
-        y0 = __fadd_rn(m0, bi0);
-        y1 = __fadd_rn(m1, bi1);
-      }
-      if (a.d.relu) { y0 = fmaxf(y0, 0.f); y1 = fmaxf(y1, 0.f); }
-    }
-    if (has0) {
-      int64_t pix = qj;
-      if (!a.dense) {
-        const int2 cc = *reinterpret_cast<const int2*>(a.coords + 2 * qj);
-        pix = ((int64_t)b * a.g.grid_h + cc.x) * a.g.grid_w + cc.y;
-      }
+    if (kj == 0 || c >= C) continue;
+    float y[4];
 #pragma unroll
-      for (int o = 0; o < PMX_MAX_OUTS; ++o)
-        if (o < outs.n) store2(outs.o[o], pix, c, y0, y1, has1);
-      if (a.out_keys) {
-        o_lo = nmin(o_lo, y0); o_hi = nmax(o_hi, y0);
-        if (has1) { o_lo = nmin(o_lo, y1); o_hi = nmax(o_hi, y1); }
+    for (int u = 0; u < 4; ++u) {
+      y[u] = m[u];
+      if (a.bn_post == nullptr) {
+        if constexpr (DT == PMX_I8) y[u] = __fmaf_rn(m[u], al[u], bi[u]);
+        else y[u] = __fadd_rn(m[u], bi[u]);
+        if (a.d.relu) y[u] = fmaxf(y[u], 0.f);
       }
+    }
+    int64_t pix = qj;
+    if (!a.dense) {
+      const int2 cc = *reinterpret_cast<const int2*>(a.coords + 2 * qj);
+      pix = ((int64_t)b * a.g.grid_h + cc.x) * a.g.grid_w + cc.y;
+    }
+    const int nl = C - c < 4 ? C - c : 4;
+#pragma unroll
+    for (int o = 0; o < PMX_MAX_OUTS; ++o) {
+      if (o >= outs.n) break;
+      const OutDev& od = outs.o[o];
+      const int64_t off = pix * od.c_stride + od.c_offset + c;
+      if (nl == 4 && od.dtype == PMX_F16 && (off & 3) == 0) {
+        *reinterpret_cast<uint2*>(reinterpret_cast<__half*>(od.ptr) + off) =
+            make_uint2(f16x2_sat(y[0], y[1]), f16x2_sat(y[2], y[3]));
+      } else if (nl == 4 && od.dtype == PMX_I8 && (off & 3) == 0) {
+        uint32_t wd = 0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) wd |= (uint32_t)(quantize_exact(y[u], od.scale, od.inv) & 0xff) << (8 * u);
+        *reinterpret_cast<uint32_t*>(reinterpret_cast<int8_t*>(od.ptr) + off) = wd;
+      } else if (nl == 4 && od.dtype == PMX_F32 && (off & 3) == 0) {
+        *reinterpret_cast<float4*>(reinterpret_cast<float*>(od.ptr) + off) = make_float4(y[0], y[1], y[2], y[3]);
+      } else {
+        for (int u = 0; u < nl; ++u) store_one(od, pix, c + u, y[u]);
+      }
+    }
+    if (a.out_keys) {
+      for (int u = 0; u < nl; ++u) { o_lo = nmin(o_lo, y[u]); o_hi = nmax(o_hi, y[u]); }
     }
   }
   if (a.in_keys) block_minmax_commit<kThreads>(in_lo, in_hi, a.in_keys);
