@@ -229,24 +229,19 @@ def main():
     offs[1:] = np.cumsum([len(f) for f in frames])
     host_offs = torch.from_numpy(offs).pin_memory()
     rec_dev = D.pack_topk(eng.topk())
-    host_rec = torch.empty(rec_dev.shape, dtype=rec_dev.dtype).pin_memory()
     h2d = host_pts.numel() * 4 + host_offs.numel() * 8
-    d2h = host_rec.numel() * 4
+    d2h = rec_dev.numel() * 4
 
-    def e2e_step():
-        eng.cg.points[: host_pts.shape[0]].copy_(host_pts, non_blocking=True)
-        eng.cg.offsets.copy_(host_offs, non_blocking=True)
-        eng.run()
-        host_rec.copy_(D.pack_topk(eng.topk()), non_blocking=True)
-
-    for _ in range(args.warmup):
-        e2e_step()
+    # the public streaming API: batch i+1's H2D (pinned host -> device) overlaps batch
+    # i's graph, batch i's records come back D2H; every step pays its own copies
+    pipe = pm.PipelinedEngine(eng)
+    host_recs = [torch.empty(rec_dev.shape, dtype=rec_dev.dtype).pin_memory() for _ in range(2)]
+    pipe.run([(host_pts, host_offs)] * args.warmup, [host_recs[i % 2] for i in range(args.warmup)], D.pack_topk)
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
     start.record()
-    for _ in range(args.steps):
-        e2e_step()
+    pipe.run([(host_pts, host_offs)] * args.steps, [host_recs[i % 2] for i in range(args.steps)], D.pack_topk)
     end.record()
     torch.cuda.synchronize()
     e2e_ms = D.max_over_ranks(start.elapsed_time(end) / args.steps, device=dev)

@@ -1020,6 +1020,10 @@ Plan plan_for(const pmx_conv_desc& d, bool gather = false) {
   // N tile: the whole GEMM N up to 256 (the A tile is then read once); TMEM holds two
   int bn = (int)(ceil_div(p.n_gemm, 16) * 16);
   if (bn > 256) bn = 256;
+  {
+    const char* e = getenv("PMX_DECONV_BN");  // experiment: cap the deconv N tile
+    if (e && p.deconv && bn > atoi(e)) bn = atoi(e);
+  }
   // small M (batch-1 blocks.2: 27 M tiles): split N while the tile count still fits
   // one wave -- each CTA then streams a quarter of the weights and issues N=64 MMAs
   while (bn > 64 && bn % 32 == 0 && (int64_t)p.m_tiles * ceil_div(p.n_gemm, bn / 2) <= kNumSMs) bn /= 2;

@@ -595,8 +595,7 @@ class CompiledGraph:
         zero = [(t.data_ptr(), t.numel() * t.element_size()) for (t, _, _) in canvas.bufs.values()]
         in_keys = self._key_ptr(getattr(self, "pfn_in_slot", None))
         out_keys = self._key_ptr(canvas.slot)
-        pts = self.points.data_ptr() if self.source == "points" else None
-        offs = self.offsets.data_ptr() if self.source == "points" else None
+        src_points = self.source == "points"  # input buffers are read at launch time (swappable slots)
         feats = self.features.data_ptr() if self.source == "sample" else None
         mask = self.mask.data_ptr() if self.source == "sample" else None
         pt_idx = self.pt_idx.data_ptr() if self.source == "points" else None
@@ -610,7 +609,8 @@ class CompiledGraph:
             for ptr_, nbytes in zero:
                 N.check(lib.pmx_zero(ptr_, nbytes, s), "zero canvas")
             N.check(fn(
-                ctypes.byref(d), ctypes.byref(g), self.B, pcap, pts, offs, feats, mask, self.coords.data_ptr(),
+                ctypes.byref(d), ctypes.byref(g), self.B, pcap, self.points.data_ptr() if src_points else None,
+                self.offsets.data_ptr() if src_points else None, feats, mask, self.coords.data_ptr(),
                 self.counts.data_ptr(), pt_idx, self.n_pillars.data_ptr(), rec["w"].data_ptr(),
                 N.ptr(rec["alpha"]), rec["bias"].data_ptr(), N.ptr(rec["bn"]), arr, n, in_keys, out_keys, s),
                 f"pfn {l.name}")

@@ -27,6 +27,7 @@ from .model import BatchNorm, LayerSpec, ModelGraph, PrecisionPlan, apply_plan, 
 from .tensor_ops import ConvParams
 
 __all__ = ["PointPillarsConfig", "build_pointpillars", "make_frame", "make_frames", "PointPillarsEngine",
+           "PipelinedEngine",
            "MIXED_PLAN_LABEL", "HEADS"]
 
 # BASELINE config 3: first backbone conv + the three deconvs in FP16
@@ -243,3 +244,68 @@ class PointPillarsEngine:
     def pillars(self) -> dict:
         cg = self.cg
         return {"coords": cg.coords, "counts": cg.counts, "pt_idx": cg.pt_idx, "n_pillars": cg.n_pillars}
+
+
+class PipelinedEngine:
+    """Host-to-device streaming around a PointPillarsEngine: two input slots (points +
+    frame offsets) with one captured CUDA graph each; while the graph of batch i runs
+    on the compute stream, the pinned-host copy of batch i+1 lands in the other slot on
+    an H2D stream and the top-k records of batch i-1 go back on a D2H stream (the
+    copy engines overlap the SMs).  Every batch's H2D and D2H still happen."""
+
+    def __init__(self, eng: "PointPillarsEngine"):
+        import torch
+
+        self.eng = eng
+        cg = eng.cg
+        # slot 1 starts as a copy of slot 0: capture() warms up on whatever the slot holds
+        self.slots = [(cg.points, cg.offsets), (cg.points.clone(), cg.offsets.clone())]
+        self.graphs = []
+        for pts, offs in self.slots:
+            cg.points, cg.offsets = pts, offs
+            self.graphs.append(cg.capture())
+        cg.points, cg.offsets = self.slots[0]
+        cg.graph_exec = self.graphs[0]
+        self.h2d = torch.cuda.Stream()
+        self.d2h = torch.cuda.Stream()
+        self.copied = [torch.cuda.Event(), torch.cuda.Event()]
+        self.done = [torch.cuda.Event(), torch.cuda.Event()]
+        self.fetched = [torch.cuda.Event(), torch.cuda.Event()]
+        self._pending = 0
+
+    def _upload(self, i: int, host_points, host_offsets):
+        import torch
+
+        slot = i % 2
+        pts, offs = self.slots[slot]
+        with torch.cuda.stream(self.h2d):
+            if i >= 2:
+                self.h2d.wait_event(self.done[slot])  # batch i-2 finished reading this slot
+            pts[: host_points.shape[0]].copy_(host_points, non_blocking=True)
+            offs.copy_(host_offsets, non_blocking=True)
+            self.copied[slot].record(self.h2d)
+
+    def run(self, batches, host_out, pack):
+        """batches: list of (pinned points [N, 4] f32, pinned offsets [B + 1] i64);
+        host_out: list of pinned tensors receiving pack(topk) per batch (same length)."""
+        import torch
+
+        comp = torch.cuda.current_stream()
+        n = len(batches)
+        if n == 0:
+            return
+        self._upload(0, *batches[0])
+        for i in range(n):
+            slot = i % 2
+            if i + 1 < n:
+                self._upload(i + 1, *batches[i + 1])
+            comp.wait_event(self.copied[slot])
+            self.graphs[slot].replay()
+            rec = pack(self.eng.topk())
+            self.done[slot].record(comp)
+            with torch.cuda.stream(self.d2h):
+                self.d2h.wait_event(self.done[slot])
+                host_out[i].copy_(rec, non_blocking=True)
+                rec.record_stream(self.d2h)
+                self.fetched[slot].record(self.d2h)
+        comp.wait_stream(self.d2h)
