@@ -49,6 +49,10 @@ def build(force: bool = False, verbose: bool = False, ptxas_verbose: bool = Fals
     BUILD.mkdir(parents=True, exist_ok=True)
     nvcc = _nvcc()
     extra = ["-Xptxas", "-v"] if ptxas_verbose else []
+    if os.environ.get("PMX_TRACE_BUILD") == "1":  # per-role conv timeline (tools/op_profile.py --trace)
+        extra += ["-DPMX_CONV_TRACE"]
+    if os.environ.get("PMX_ABLATE"):  # epilogue ablation builds (experiments only)
+        extra += [f"-DPMX_ABLATE={int(os.environ['PMX_ABLATE'])}"]
 
     def compile_one(src: Path) -> Path:
         obj = BUILD / (src.stem + ".o")

@@ -15,7 +15,7 @@ from pathlib import Path
 import numpy as np
 
 PKG = Path(__file__).resolve().parent
-LIB_PATH = PKG / "libpmx.so"
+LIB_PATH = Path(os.environ["PMX_LIB"]) if os.environ.get("PMX_LIB") else PKG / "libpmx.so"  # PMX_LIB: A/B builds
 
 PMX_OK, PMX_ERR_INVALID, PMX_ERR_CUDA, PMX_ERR_UNSUPPORTED = 0, 1, 2, 3
 PMX_F32, PMX_F16, PMX_I8, PMX_F64 = 0, 1, 2, 3

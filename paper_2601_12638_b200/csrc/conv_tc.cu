@@ -219,6 +219,11 @@ struct TcParams {
   int nacc;        // TMEM accumulator buffers (power of two; MMA runs up to nacc tiles ahead)
   int nacc_shift;  // log2(nacc)
   int egroups;     // epilogue tile slots (1, 2 or 4)
+  // warp-transposed int8 stores (single int8 consumer): each epilogue warp stages its
+  // 4 chunks (32 rows x 64 B) in shared memory and every store instruction then
+  // writes 8 rows x 64 contiguous bytes (thread-per-row 16-byte stores scatter over
+  // 32 lines per instruction and run at ~1/4 of the write bandwidth)
+  int estage;
   // HALO mode
   uint32_t halo_tx;     // halo bytes per tile (TMA transaction size)
   uint32_t hp, hw;      // halo pixels, halo row width (pixels)
@@ -238,10 +243,18 @@ struct TcParams {
   int g_row_bytes;
 };
 
+// per-role timeline of CTA 0 (tools/op_profile.py --trace); compiled in only with
+// PMX_TRACE_BUILD=1 (-DPMX_CONV_TRACE) so the production kernels carry no trace code
+#ifdef PMX_CONV_TRACE
 #define PMX_TRACE(ev, idx)                                                              \
   do {                                                                                  \
     if (p.trace && blockIdx.x == 0 && (idx) < 64) p.trace[(ev) * 64 + (idx)] = clock64(); \
   } while (0)
+#else
+#define PMX_TRACE(ev, idx) \
+  do {                     \
+  } while (0)
+#endif
 
 struct TcMaps {
   CUtensorMap a[4];  // conv: [parity] maps (stride 2) or a[0]; GEMM: a[0] 2D
@@ -548,6 +561,8 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
   // per-channel alpha / bias copies (16-byte aligned, after the barriers + TMEM slot)
   float* s_alpha = reinterpret_cast<float*>(gbase + (((bar_base - base) + 8 * (2 * p.stages + 2 * p.nacc + 1) + 4 + 15) & ~15u));
   float* s_bias = s_alpha + ((p.out_c + 3) & ~3);
+  // epilogue store staging: 2 KB per epilogue warp (after alpha / bias / gather list)
+  const uint32_t s_estage = (smem_u32(s_bias + ((p.out_c + 3) & ~3)) + (GATHER ? 2304u : 0u) + 15u) & ~15u;
   auto full = [&](int s) { return bar_base + 8u * s; };
   auto empty = [&](int s) { return bar_base + 8u * (p.stages + s); };
   auto tfull = [&](int a) { return bar_base + 8u * (2 * p.stages + a); };
@@ -836,33 +851,30 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
       if (warp == 2 && lane == 0) PMX_TRACE(6, i);
       if (lane == 0 && i == 6) PMX_TRACE(8, 8 + 2 * (warp - 2));  // per-warp view of one steady-state tile
       const uint32_t trow = tmem + acc * (uint32_t)p.bn + ((uint32_t)(q * 32) << 16);
-#pragma unroll 1
-      for (int c = c_begin; c < c_end; ++c) {
-        // 5 warps share one SM sub-partition: 96 registers per thread leave no room
-        // to double-buffer the TMEM loads; the other tile slots hide the latency
-        uint32_t v[16];
-        tmem_ld16_issue(trow + 16 * c, v);
-        tmem_ld_wait(v);
-        const int nbase = n0 + 16 * c;
-        if (!valid || nbase >= p.n_gemm) continue;
-        // deconv: 16 consecutive GEMM columns share one tap (Cout % 16 == 0)
-        uint32_t pix = pix_in;
-        int cobase = nbase;
-        if (p.deconv) {
-          int tap;
-          if (p.oc_shift >= 0) {
-            tap = nbase >> p.oc_shift;
-            cobase = nbase & (p.out_c - 1);
-          } else {
-            tap = (int)fdiv((uint32_t)nbase, p.fd_oc);
-            cobase = nbase - tap * p.out_c;
+      // deconv: output pixel of tap (0, 0); tap (dy, dx) adds dy * out_w + dx
+      const uint32_t pbase = (ib * p.out_h + iy * p.stride) * p.out_w + ix * p.stride;
+      if constexpr (OUTK == 1) {
+        if (fast && p.estage) {
+          // this warp's 4 chunks = 64 consecutive output channels of its 32 rows: stage
+          // the codes (row-major, 16-byte slots XOR-swizzled by row / 2: conflict-free),
+          // then 4 store instructions of 8 rows x 64 bytes each
+          const uint32_t wstage = s_estage + (uint32_t)(warp - 2) * 2048u;
+          const int nbase0 = n0 + 16 * c_begin;
+          const bool live = nbase0 < p.n_gemm;  // warp-uniform (n_gemm % 64 == 0)
+          int cob0 = nbase0;
+          uint32_t mypix = pix_in;
+          if (p.deconv) {
+            const int tap = nbase0 >> p.oc_shift;
+            cob0 = nbase0 & (p.out_c - 1);
+            mypix = pbase + (uint32_t)(tap >> p.st_shift) * (uint32_t)p.out_w + (uint32_t)(tap & (p.stride - 1));
           }
-          const uint32_t ddy = (uint32_t)tap >> p.st_shift, ddx = (uint32_t)tap & (uint32_t)(p.stride - 1);
-          pix = (ib * p.out_h + iy * p.stride + ddy) * p.out_w + ix * p.stride + ddx;
-        }
-        if constexpr (OUTK == 1) {
-          if (fast) {
-            // one aligned int8 consumer, no unfolded BN / observer, full 16-column run
+#pragma unroll 1
+          for (int k = 0; k < 4; ++k) {
+            uint32_t v[16];
+            tmem_ld16_issue(trow + 16 * (c_begin + k), v);
+            tmem_ld_wait(v);
+            if (!valid || !live) continue;
+            const int cobase = cob0 + 16 * k;
             float y[16];
             const float4* b4p = reinterpret_cast<const float4*>(s_bias + cobase);
             const float4* a4p = reinterpret_cast<const float4*>(s_alpha + cobase);
@@ -890,6 +902,99 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
             uint4 code;
             const bool ok = p.relu ? quant16_noclamp<true>(y, o_inv, code) : quant16_noclamp<false>(y, o_inv, code);
             if (!ok) code = quant16(y, o_scale, o_inv, qlo);
+            const uint32_t sa = wstage + (uint32_t)lane * 64u + (((uint32_t)k ^ (((uint32_t)lane >> 1) & 3u)) << 4);
+            asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(sa), "r"(code.x), "r"(code.y), "r"(code.z),
+                         "r"(code.w)
+                         : "memory");
+          }
+          __syncwarp();
+          if (live) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const int r = 8 * j + (lane >> 2);
+              const uint32_t cc = (uint32_t)lane & 3u;
+              const uint32_t rp = __shfl_sync(0xffffffffu, mypix, r);
+              const int rv = __shfl_sync(0xffffffffu, (int)valid, r);
+              uint4 w;
+              const uint32_t la = wstage + (uint32_t)r * 64u + ((cc ^ (((uint32_t)r >> 1) & 3u)) << 4);
+              asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                           : "=r"(w.x), "=r"(w.y), "=r"(w.z), "=r"(w.w)
+                           : "r"(la)
+                           : "memory");
+              if (rv) *reinterpret_cast<uint4*>(o_ptr + (size_t)rp * o_cs + cob0 + 16 * cc) = w;
+            }
+          }
+          __syncwarp();
+          // release this accumulator buffer to the MMA warp
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(tempty(acc));
+          continue;
+        }
+      }
+#pragma unroll 1
+      for (int c = c_begin; c < c_end; ++c) {
+        // 5 warps share one SM sub-partition: 96 registers per thread leave no room
+        // to double-buffer the TMEM loads; the other tile slots hide the latency
+        uint32_t v[16];
+        tmem_ld16_issue(trow + 16 * c, v);
+        tmem_ld_wait(v);
+        const int nbase = n0 + 16 * c;
+        if (!valid || nbase >= p.n_gemm) continue;
+        // deconv: 16 consecutive GEMM columns share one tap (Cout % 16 == 0)
+        uint32_t pix = pix_in;
+        int cobase = nbase;
+        if (p.deconv) {
+          int tap;
+          if (p.oc_shift >= 0) {
+            tap = nbase >> p.oc_shift;
+            cobase = nbase & (p.out_c - 1);
+          } else {
+            tap = (int)fdiv((uint32_t)nbase, p.fd_oc);
+            cobase = nbase - tap * p.out_c;
+          }
+          const uint32_t ddy = (uint32_t)tap >> p.st_shift, ddx = (uint32_t)tap & (uint32_t)(p.stride - 1);
+          pix = pbase + ddy * (uint32_t)p.out_w + ddx;
+        }
+        if constexpr (OUTK == 1) {
+          if (fast) {
+            // one aligned int8 consumer, no unfolded BN / observer, full 16-column run
+#if defined(PMX_ABLATE) && PMX_ABLATE == 1
+            continue;
+#elif defined(PMX_ABLATE) && PMX_ABLATE == 3
+            *reinterpret_cast<uint4*>(o_ptr + (size_t)pix * o_cs + cobase) = make_uint4(v[0], v[5], v[10], v[15]);
+            continue;
+#endif
+            float y[16];
+            const float4* b4p = reinterpret_cast<const float4*>(s_bias + cobase);
+            const float4* a4p = reinterpret_cast<const float4*>(s_alpha + cobase);
+#pragma unroll
+            for (int j4 = 0; j4 < 4; ++j4) {
+              const float4 b4 = b4p[j4];
+              float2 r0, r1;
+              if constexpr (DT == PMX_I8) {
+                const float4 a4 = a4p[j4];
+                r0 = __ffma2_rn(make_float2((float)(int)v[4 * j4], (float)(int)v[4 * j4 + 1]),
+                                make_float2(a4.x, a4.y), make_float2(b4.x, b4.y));
+                r1 = __ffma2_rn(make_float2((float)(int)v[4 * j4 + 2], (float)(int)v[4 * j4 + 3]),
+                                make_float2(a4.z, a4.w), make_float2(b4.z, b4.w));
+              } else {
+                r0 = __fadd2_rn(make_float2(__uint_as_float(v[4 * j4]), __uint_as_float(v[4 * j4 + 1])),
+                                make_float2(b4.x, b4.y));
+                r1 = __fadd2_rn(make_float2(__uint_as_float(v[4 * j4 + 2]), __uint_as_float(v[4 * j4 + 3])),
+                                make_float2(b4.z, b4.w));
+              }
+              y[4 * j4] = r0.x;
+              y[4 * j4 + 1] = r0.y;
+              y[4 * j4 + 2] = r1.x;
+              y[4 * j4 + 3] = r1.y;
+            }
+            uint4 code;
+            const bool ok = p.relu ? quant16_noclamp<true>(y, o_inv, code) : quant16_noclamp<false>(y, o_inv, code);
+            if (!ok) code = quant16(y, o_scale, o_inv, qlo);
+#if defined(PMX_ABLATE) && PMX_ABLATE == 2
+            if ((code.x & code.y & code.z & code.w) == 0x7f7f7f7fu)
+#endif
             *reinterpret_cast<uint4*>(o_ptr + (size_t)pix * o_cs + cobase) = code;
             continue;
           }
@@ -958,7 +1063,16 @@ struct Plan {
 };
 
 // Can the tensor-core path run this layer?  (shape / alignment rules)
-Plan plan_for(const pmx_conv_desc& d, bool gather = false) {
+// warp-transposed epilogue stores (PMX_ESTAGE=0 turns them off for A/B runs)
+bool estage_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("PMX_ESTAGE");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+Plan plan_for(const pmx_conv_desc& d, bool gather = false, bool want_stage = false, int out_row_bytes = 0) {
   Plan pl{};
   pl.ok = false;
   if (d.in_dtype != PMX_I8 && d.in_dtype != PMX_F16) return pl;
@@ -1032,10 +1146,23 @@ Plan plan_for(const pmx_conv_desc& d, bool gather = false) {
   const int64_t tiles = (int64_t)p.m_tiles * p.n_tiles;
   pl.grid_x = (int)(tiles < kNumSMs ? tiles : kNumSMs);
   pl.grid_y = 1;
+  // warp-transposed int8 stores: every epilogue warp owns exactly 4 chunks (64
+  // channels) of a tile, groups never straddle a deconv tap
+  p.nacc = 2;
+  while (p.nacc < 8 && 2 * p.nacc * bn <= 512) p.nacc *= 2;
+  p.nacc_shift = __builtin_ctz((unsigned)p.nacc);
+  p.egroups = bn <= 64 ? 4 : (bn <= 128 ? 2 : 1);
+  if (p.egroups > p.nacc) p.egroups = p.nacc;
+  // (measured: a win for 128- and 384-byte output rows -- deconvs into the concat,
+  // blocks.1.0 -- a loss for the 64-byte rows of block 0, which are MMA-bound)
+  p.estage = want_stage && estage_enabled() && out_row_bytes >= 128 && (bn / 16) == 4 * (4 / p.egroups) &&
+             p.n_gemm % 64 == 0 &&
+             (!p.deconv || (p.oc_shift >= 0 && d.out_c % 64 == 0));
+  const uint32_t estage_bytes = p.estage ? (uint32_t)kEpiWarps * 2048u : 0u;
   p.a_bytes = 128u * kc_bytes;
   p.b_bytes = (uint32_t)bn * kc_bytes;
   const uint32_t stage = p.a_bytes + p.b_bytes;
-  int stages = (int)((200u * 1024u - 8u * (uint32_t)d.out_c) / stage);  // one persistent CTA per SM
+  int stages = (int)((200u * 1024u - 8u * (uint32_t)d.out_c - estage_bytes) / stage);  // one persistent CTA per SM
   if (stages > 12) stages = 12;
   if (stages < 2) stages = 2;
   p.stages = stages;
@@ -1049,7 +1176,12 @@ Plan plan_for(const pmx_conv_desc& d, bool gather = false) {
     const uint32_t bblk = (uint32_t)bn * kc_bytes;
     const uint32_t bres_total = 9u * p.cblocks * bblk;
     // dynamic smem minus alignment, barriers and the alpha / bias copies
-    const uint32_t budget = 227u * 1024u - 2048u - 8u * (uint32_t)((d.out_c + 3) & ~3) - (gather ? 2304u : 0u);
+    const uint32_t budget0 = 227u * 1024u - 2048u - 8u * (uint32_t)((d.out_c + 3) & ~3) - (gather ? 2304u : 0u);
+    uint32_t budget = budget0 - estage_bytes;
+    if (p.estage && bres_total + 2 * halo_al > budget && bres_total + 2 * halo_al <= budget0) {
+      p.estage = 0;  // resident weights + two halo stages win over the store staging
+      budget = budget0;
+    }
     if (bres_total + 2 * halo_al <= budget) {
       p.mode = MODE_HALO;
       p.tw = 8;
@@ -1080,11 +1212,6 @@ Plan plan_for(const pmx_conv_desc& d, bool gather = false) {
   p.fd_oc = make_fastdiv((uint32_t)d.out_c);
   // as many TMEM accumulators as fit (a power of two, 2..8): the MMA warp runs ahead
   // of the epilogue; the epilogue drains up to 4 tiles at once (tile slots)
-  p.nacc = 2;
-  while (p.nacc < 8 && 2 * p.nacc * bn <= 512) p.nacc *= 2;
-  p.nacc_shift = __builtin_ctz((unsigned)p.nacc);
-  p.egroups = bn <= 64 ? 4 : (bn <= 128 ? 2 : 1);
-  if (p.egroups > p.nacc) p.egroups = p.nacc;
   const int cols = p.nacc * bn;
   p.tmem_cols = cols <= 32 ? 32 : (cols <= 64 ? 64 : (cols <= 128 ? 128 : (cols <= 256 ? 256 : 512)));
   const uint32_t m_enc = 128u >> 4, n_enc = (uint32_t)bn >> 3;
@@ -1093,7 +1220,7 @@ Plan plan_for(const pmx_conv_desc& d, bool gather = false) {
   else
     p.idesc = (1u << 4) | (0u << 7) | (0u << 10) | (n_enc << 17) | (m_enc << 24);
   pl.smem = 1024 + (size_t)p.stages * (p.a_bytes + p.b_bytes) + p.bres_bytes + (2 * p.stages + 2 * p.nacc + 1) * 8 + 32 +
-            8 * (size_t)((d.out_c + 3) & ~3) + (gather ? 2304 : 0);
+            8 * (size_t)((d.out_c + 3) & ~3) + (gather ? 2304 : 0) + (p.estage ? 16 + kEpiWarps * 2048 : 0);
   pl.ok = true;
   return pl;
 }
@@ -1184,7 +1311,10 @@ pmx_status conv_tc_try(const pmx_conv_desc& d, const void* x, const void* w, con
                        bool* launched, const GatherIn* gin) {
   *launched = false;
   const bool gather = gin != nullptr;
-  Plan pl = plan_for(d, gather);
+  // OUTK 1: the common single int8 consumer with 16-byte aligned pixel rows
+  const bool one_i8 = outs.n == 1 && outs.o[0].dtype == PMX_I8 && outs.o[0].c_stride % 16 == 0 &&
+                      outs.o[0].c_offset % 16 == 0 && (reinterpret_cast<uintptr_t>(outs.o[0].ptr) & 15) == 0;
+  Plan pl = plan_for(d, gather, one_i8 && !bn_post && !keys, outs.o[0].c_stride);
   if (!pl.ok) return PMX_OK;
   if (gather && pl.p.mode != MODE_HALO) return PMX_OK;
   if ((reinterpret_cast<uintptr_t>(x) & 15) || (reinterpret_cast<uintptr_t>(w) & 15)) return PMX_OK;
@@ -1208,9 +1338,6 @@ pmx_status conv_tc_try(const pmx_conv_desc& d, const void* x, const void* w, con
     pl.p.g_row_bytes = d.in_c_stride * esz;
   }
   dim3 grid(pl.grid_x, pl.grid_y);
-  // OUTK 1: the common single int8 consumer with 16-byte aligned pixel rows
-  const bool one_i8 = outs.n == 1 && outs.o[0].dtype == PMX_I8 && outs.o[0].c_stride % 16 == 0 &&
-                      outs.o[0].c_offset % 16 == 0 && (reinterpret_cast<uintptr_t>(outs.o[0].ptr) & 15) == 0;
   auto launch = [&](auto kern, int threads) -> pmx_status {
     PMX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
     cudaLaunchConfig_t cfg{};

@@ -225,10 +225,22 @@ __device__ __forceinline__ uint4 quant16(const float (&y)[16], double s, float i
     tb[j + 1] = __float_as_uint(t.y);
   }
   if (!(dmax < kTieBand)) {
+    // redo only the flagged values (a tie-band value or NaN); the others keep their
+    // magic-add code.  Constant activations (empty canvas regions) make a tie channel
+    // hit every pixel, so the per-value patch matters.
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      const float yj = lo == 0.0f ? fmaxf(y[j], 0.0f) : y[j];
-      tb[j] = (uint32_t)quantize_exact(yj, s, inv);
+    for (int j = 0; j < 16; j += 2) {
+      float2 qv = __fmul2_rn(make_float2(y[j], y[j + 1]), I2);
+      qv.x = fmin_nan(fmax_nan(qv.x, lo), 127.0f);
+      qv.y = fmin_nan(fmax_nan(qv.y, lo), 127.0f);
+      const float2 d = __fadd2_rn(qv, __ffma2_rn(__fadd2_rn(qv, M2), NEG1, M2));
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        if (!(fabsf(h ? d.y : d.x) < kTieBand)) {
+          const float yj = lo == 0.0f ? fmaxf(y[j + h], 0.0f) : y[j + h];
+          tb[j + h] = (uint32_t)quantize_exact(yj, s, inv);
+        }
+      }
     }
   }
   return make_uint4(__byte_perm(__byte_perm(tb[0], tb[1], 0x0040), __byte_perm(tb[2], tb[3], 0x0040), 0x5410),
