@@ -261,9 +261,15 @@ struct TcMaps {
   CUtensorMap b;
 };
 
-constexpr int kEpiWarps = 16;                  // warps 2..17: four per TMEM lane quarter
+// Warp roles.  The SM sub-partition scheduler picks the eligible warp with the
+// HIGHEST id first, so the latency-critical single-thread roles get the top ids:
+// warps 0..15 epilogue (warp & 3 = TMEM lane quarter), 16 TMA producer (GATHER: a
+// halo builder), 17 MMA issuer, 18..19 the other GATHER halo builders.
+constexpr int kEpiWarps = 16;
+constexpr int kProdWarp = 16;
+constexpr int kMmaWarp = 17;
 constexpr int kThreads = 32 * (2 + kEpiWarps);  // + TMA producer warp + MMA warp
-constexpr int kGatherWarps = 3;                 // GATHER: warp 0 + warps 18, 19 build the halo tiles
+constexpr int kGatherWarps = 3;                 // GATHER: warps 16, 18, 19 build the halo tiles
 constexpr int kThreadsGather = kThreads + 32 * (kGatherWarps - 1);
 
 // 16 f32 values -> 16 exact int8 codes WITHOUT clamping: valid (returns true) when
@@ -444,6 +450,10 @@ __host__ __device__ constexpr int plane_p0(int hs, int q) {
   return hs == 2 ? (q == 0 ? 0 : (q == 1 ? 128 : (q == 2 ? 272 : 408))) : 0;
 }
 
+// smem of the gather producer (after alpha / bias): counters, two occupied-pixel
+// lists (load side, one per tile in flight) and one clear list per stage
+constexpr int kGatherSmem = 2304;  // gather producer: 4 counters + the occupied-pixel list (561 entries)
+
 template <int CINB, int HS, typename FullF, typename EmptyF>
 __device__ __forceinline__ void gather_producer(const TcParams& p, uint32_t a_smem, int gt, int lane, int total,
                                                 int32_t* s_list, int32_t* s_cnt, FullF full, EmptyF empty) {
@@ -562,7 +572,7 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
   float* s_alpha = reinterpret_cast<float*>(gbase + (((bar_base - base) + 8 * (2 * p.stages + 2 * p.nacc + 1) + 4 + 15) & ~15u));
   float* s_bias = s_alpha + ((p.out_c + 3) & ~3);
   // epilogue store staging: 2 KB per epilogue warp (after alpha / bias / gather list)
-  const uint32_t s_estage = (smem_u32(s_bias + ((p.out_c + 3) & ~3)) + (GATHER ? 2304u : 0u) + 15u) & ~15u;
+  const uint32_t s_estage = (smem_u32(s_bias + ((p.out_c + 3) & ~3)) + (GATHER ? (uint32_t)kGatherSmem : 0u) + 15u) & ~15u;
   auto full = [&](int s) { return bar_base + 8u * s; };
   auto empty = [&](int s) { return bar_base + 8u * (p.stages + s); };
   auto tfull = [&](int a) { return bar_base + 8u * (2 * p.stages + a); };
@@ -585,12 +595,11 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
     mbar_init(bfull, 1);
     if constexpr (GATHER) {
       int32_t* s_cnt = reinterpret_cast<int32_t*>(s_bias + ((p.out_c + 3) & ~3));
-      s_cnt[0] = 0;
-      s_cnt[1] = 0;
+      s_cnt[0] = s_cnt[1] = 0;
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 1) {
+  if (warp == kMmaWarp) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                  "r"(p.tmem_cols)
                  : "memory");
@@ -606,16 +615,16 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
   // overlap the previous layer's tail; the activations are read (and the outputs
   // written) only after griddepcontrol.wait.  The next layer may start launching now.
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  if (p.mode == MODE_HALO && warp == 0 && lane == 0) {
+  if (p.mode == MODE_HALO && warp == kProdWarp && lane == 0) {
     mbar_expect_tx(bfull, p.bres_bytes);
     for (int kb = 0; kb < nk; ++kb) {
       const int tap = kb / p.cblocks, cb = kb % p.cblocks;
       tma_load_2d(bres + kb * p.bblk_bytes, &maps.b, tap * (p.cblocks * p.kc) + cb * p.kc, 0, bfull);
     }
   }
-  if (warp >= 2) {
+  if (warp < kEpiWarps) {
     const int n0 = (blockIdx.x % p.n_tiles) * p.bn;
-    for (int c = (warp - 2) >> 2; c < p.bn / 16; c += 4) {
+    for (int c = warp >> 2; c < p.bn / 16; c += 4) {
       const int co = n0 + 16 * c < p.out_c ? n0 + 16 * c : 0;
       asm volatile("prefetch.global.L1 [%0];" ::"l"(p.bias + co));
       if (p.alpha) asm volatile("prefetch.global.L1 [%0];" ::"l"(p.alpha + co));
@@ -623,14 +632,14 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
   }
   asm volatile("griddepcontrol.wait;" ::: "memory");
 
-  if (GATHER && (warp == 0 || warp >= 2 + kEpiWarps)) {
+  if (GATHER && (warp == kProdWarp || warp > kMmaWarp)) {
     if constexpr (GATHER) {
       // smem after alpha / bias: two list counters, the occupied-pixel list
       int32_t* s_cnt = reinterpret_cast<int32_t*>(s_bias + ((p.out_c + 3) & ~3));
-      gather_producer<CINB, HS>(p, a_smem, warp == 0 ? lane : 32 * (warp - 1 - kEpiWarps) + lane, lane, total,
+      gather_producer<CINB, HS>(p, a_smem, warp == kProdWarp ? lane : 32 * (warp - kMmaWarp) + lane, lane, total,
                                 s_cnt + 4, s_cnt, full, empty);
     }
-  } else if (warp == 0) {
+  } else if (warp == kProdWarp) {
     if (lane == 0) {
       // ---------------- TMA producer
       uint32_t it = 0, s = 0, ph = 0;  // ring position, slot, phase
@@ -695,7 +704,7 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
       }
     }
     __syncwarp();
-  } else if (warp == 1) {
+  } else if (warp == kMmaWarp) {
     // ---------------- MMA issuer.  The whole warp walks the loop (barrier waits are
     // warp-wide, so the descriptors stay in uniform registers) and one elected lane
     // issues.  Descriptor words: hi = SBO | version | layout (constant), lo = LBO << 16
@@ -796,7 +805,7 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
     // range of up to 4 chunks of 16 accumulator columns and double-buffers its TMEM
     // loads.  Per-channel alpha / bias are staged once in shared memory.
     const int q = warp & 3;         // TMEM lane quarter this warp may access
-    const int e = (warp - 2) >> 2;  // 0..3
+    const int e = warp >> 2;  // 0..3
     const int egn = p.egroups, colsplit = 4 / egn;
     const int eg = e / colsplit, cg = e - eg * colsplit;
     const int row = q * 32 + lane;
@@ -804,7 +813,7 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
     const int cpw = (nchunks + colsplit - 1) / colsplit;
     const int c_begin = cg * cpw, c_end = min(nchunks, c_begin + cpw);
     {
-      const int et = threadIdx.x - 64;
+      const int et = threadIdx.x;
       for (int j = et; j < p.out_c; j += 32 * kEpiWarps) {
         s_alpha[j] = p.alpha ? p.alpha[j] : 0.0f;
         s_bias[j] = p.bias[j];
@@ -845,11 +854,11 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
           iy = tt - ib * (uint32_t)p.in_h;
         }
       }
-      if (warp == 2 && lane == 0) PMX_TRACE(5, i);
+      if (warp == 0 && lane == 0) PMX_TRACE(5, i);
       mbar_wait(tfull(acc), aph);
       tc_fence_after();
-      if (warp == 2 && lane == 0) PMX_TRACE(6, i);
-      if (lane == 0 && i == 6) PMX_TRACE(8, 8 + 2 * (warp - 2));  // per-warp view of one steady-state tile
+      if (warp == 0 && lane == 0) PMX_TRACE(6, i);
+      if (lane == 0 && i == 6) PMX_TRACE(8, 8 + 2 * warp);  // per-warp view of one steady-state tile
       const uint32_t trow = tmem + acc * (uint32_t)p.bn + ((uint32_t)(q * 32) << 16);
       // deconv: output pixel of tap (0, 0); tap (dy, dx) adds dy * out_w + dx
       const uint32_t pbase = (ib * p.out_h + iy * p.stride) * p.out_w + ix * p.stride;
@@ -858,7 +867,7 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
           // this warp's 4 chunks = 64 consecutive output channels of its 32 rows: stage
           // the codes (row-major, 16-byte slots XOR-swizzled by row / 2: conflict-free),
           // then 4 store instructions of 8 rows x 64 bytes each
-          const uint32_t wstage = s_estage + (uint32_t)(warp - 2) * 2048u;
+          const uint32_t wstage = s_estage + (uint32_t)warp * 2048u;
           const int nbase0 = n0 + 16 * c_begin;
           const bool live = nbase0 < p.n_gemm;  // warp-uniform (n_gemm % 64 == 0)
           int cob0 = nbase0;
@@ -1005,15 +1014,15 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(tempty(acc));
-      if (warp == 2 && lane == 0) PMX_TRACE(7, i);
-      if (lane == 0 && i == 6) PMX_TRACE(8, 9 + 2 * (warp - 2));
+      if (warp == 0 && lane == 0) PMX_TRACE(7, i);
+      if (lane == 0 && i == 6) PMX_TRACE(8, 9 + 2 * warp);
     }
     if (p.keys) block_minmax_commit<kThreads>(lo, hi, p.keys);
   }
   tc_fence_before();
   __syncthreads();
   if (threadIdx.x == 0) PMX_TRACE(8, 3);
-  if (warp == 1) {
+  if (warp == kMmaWarp) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(p.tmem_cols) : "memory");
   }
@@ -1070,6 +1079,13 @@ bool estage_enabled() {
     return !(e && e[0] == '0');
   }();
   return on;
+}
+int estage_min_row() {  // PMX_ESTAGE=2: stage every eligible layer (experiments)
+  static const int v = [] {
+    const char* e = getenv("PMX_ESTAGE");
+    return (e && e[0] == '2') ? 0 : 128;
+  }();
+  return v;
 }
 
 Plan plan_for(const pmx_conv_desc& d, bool gather = false, bool want_stage = false, int out_row_bytes = 0) {
@@ -1155,7 +1171,7 @@ Plan plan_for(const pmx_conv_desc& d, bool gather = false, bool want_stage = fal
   if (p.egroups > p.nacc) p.egroups = p.nacc;
   // (measured: a win for 128- and 384-byte output rows -- deconvs into the concat,
   // blocks.1.0 -- a loss for the 64-byte rows of block 0, which are MMA-bound)
-  p.estage = want_stage && estage_enabled() && out_row_bytes >= 128 && (bn / 16) == 4 * (4 / p.egroups) &&
+  p.estage = want_stage && estage_enabled() && out_row_bytes >= estage_min_row() && (bn / 16) == 4 * (4 / p.egroups) &&
              p.n_gemm % 64 == 0 &&
              (!p.deconv || (p.oc_shift >= 0 && d.out_c % 64 == 0));
   const uint32_t estage_bytes = p.estage ? (uint32_t)kEpiWarps * 2048u : 0u;
@@ -1176,13 +1192,14 @@ Plan plan_for(const pmx_conv_desc& d, bool gather = false, bool want_stage = fal
     const uint32_t bblk = (uint32_t)bn * kc_bytes;
     const uint32_t bres_total = 9u * p.cblocks * bblk;
     // dynamic smem minus alignment, barriers and the alpha / bias copies
-    const uint32_t budget0 = 227u * 1024u - 2048u - 8u * (uint32_t)((d.out_c + 3) & ~3) - (gather ? 2304u : 0u);
+    const uint32_t budget0 = 227u * 1024u - 2048u - 8u * (uint32_t)((d.out_c + 3) & ~3) - (gather ? (uint32_t)kGatherSmem : 0u);
     uint32_t budget = budget0 - estage_bytes;
-    if (p.estage && bres_total + 2 * halo_al > budget && bres_total + 2 * halo_al <= budget0) {
+    const uint32_t two_stages = 2 * halo_al;
+    if (p.estage && bres_total + two_stages > budget && bres_total + two_stages <= budget0) {
       p.estage = 0;  // resident weights + two halo stages win over the store staging
       budget = budget0;
     }
-    if (bres_total + 2 * halo_al <= budget) {
+    if (bres_total + two_stages <= budget) {
       p.mode = MODE_HALO;
       p.tw = 8;
       p.th = 16;
@@ -1220,7 +1237,7 @@ Plan plan_for(const pmx_conv_desc& d, bool gather = false, bool want_stage = fal
   else
     p.idesc = (1u << 4) | (0u << 7) | (0u << 10) | (n_enc << 17) | (m_enc << 24);
   pl.smem = 1024 + (size_t)p.stages * (p.a_bytes + p.b_bytes) + p.bres_bytes + (2 * p.stages + 2 * p.nacc + 1) * 8 + 32 +
-            8 * (size_t)((d.out_c + 3) & ~3) + (gather ? 2304 : 0) + (p.estage ? 16 + kEpiWarps * 2048 : 0);
+            8 * (size_t)((d.out_c + 3) & ~3) + (gather ? kGatherSmem : 0) + (p.estage ? 16 + kEpiWarps * 2048 : 0);
   pl.ok = true;
   return pl;
 }

@@ -50,12 +50,12 @@ def main():
         import numpy as np
 
         lib = N.load()
-        tr = torch.zeros(10 * 64, dtype=torch.int64, device="cuda")
+        tr = torch.zeros(16 * 64, dtype=torch.int64, device="cuda")
         lib.pmx_debug_trace(tr.data_ptr())
         fn(N.stream_ptr())
         torch.cuda.synchronize()
         lib.pmx_debug_trace(None)
-        t = tr.cpu().numpy().reshape(10, 64).astype(np.int64)
+        t = tr.cpu().numpy().reshape(16, 64).astype(np.int64)
         t0 = t[8, 0]
         print("prologue: setup %d, weights landed %d, teardown %d (cycles from entry)" %
               tuple((t[8, i] - t0) if t[8, i] else -1 for i in (1, 2, 3)))
@@ -68,6 +68,10 @@ def main():
             if not t[:8, i].any() and not t[9, i]:
                 break
             print(f"{i:4d} " + " ".join(f"{(t[e, i] - t0) if t[e, i] else -1:12d}" for e in (0, 1, 9, 2, 3, 4, 5, 6, 7)))
+        if t[10:14].any():
+            print("gather producer: iter_start, built, empty_ok, B1, stored, arrived")
+            for i in range(32):
+                print(f"{i:4d} " + " ".join(f"{(t[e, i] - t0) if t[e, i] else -1:10d}" for e in (0, 10, 1, 11, 12, 13)))
         return
     torch.cuda.profiler.start()
     fn(N.stream_ptr())
