@@ -5,11 +5,11 @@
 //             atomicAdd(cnt[cell], 1)                           -- coalesced float4 loads
 //  2 flags    per point block: #points that are the first of their cell
 //  3 thresh   per frame: T = index of the P_max-th first-seen point (cap rule), or INT_MAX
-//  4 cellcnt  per cell block: kept = cnt>0 && first<=T; (kept, kept points) block sums
-//  5 cellscan per frame: exclusive scan of block sums -> n_pillars
-//  6 emit     per cell block: pillar id in ascending flat order, coords, segment offsets
-//  7 slot     per point: atomic slot in its pillar's CSR segment (arbitrary order)
-//  8 select   warp per pillar: the first M points of the segment by scene index
+//  4 emit     per cell block (single pass, decoupled look-back): kept = cnt>0 &&
+//             first<=T; pillar id in ascending flat order, coords, segment offsets,
+//             n_pillars
+//  5 slot     per point: atomic slot in its pillar's CSR segment (arbitrary order)
+//  6 select   warp per pillar: the first M points of the segment by scene index
 //             (shuffle ranks; a warp threshold search when the cell holds > 32 points)
 #include <climits>
 
@@ -36,6 +36,8 @@ struct PillarWs {
   int32_t* csr;     // [B*Nmax]
   int32_t* ovf_n;   // [1] pillars with > 32 points (rare: dense clusters)
   int2* ovf;        // [B*Pcap] (frame, pillar) of those
+  unsigned long long* look;  // [B*CB] single-pass emit: per-block (flag, kept, points) look-back words
+  int32_t* ticket;           // [B] single-pass emit: block order per frame
 };
 
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -64,6 +66,8 @@ size_t carve(const pmx_grid* g, int32_t B, int64_t nmax, int32_t pcap, void* bas
   w.csr = (int32_t*)take(sizeof(int32_t) * B * (nmax > 0 ? nmax : 1));
   w.ovf_n = (int32_t*)take(sizeof(int32_t));
   w.ovf = (int2*)take(sizeof(int2) * B * pcap);
+  w.look = (unsigned long long*)take(sizeof(unsigned long long) * B * cb);
+  w.ticket = (int32_t*)take(sizeof(int32_t) * B);
   if (ws) *ws = w;
   return off;
 }
@@ -175,77 +179,84 @@ __global__ void __launch_bounds__(1024) thresh_kernel(const int64_t* __restrict_
   if (flag && inc == s_need) w.thresh[b] = (int)i;
 }
 
-__global__ void __launch_bounds__(1024) cellcount_kernel(const pmx_grid g, PillarWs w, int cb) {
+// Single pass of cellcount + cellscan + emit: every block reads its 4096 cells
+// once (int4 loads), takes its place in the frame's block order from a ticket, and
+// gets its exclusive (pillar, point) offsets by decoupled look-back over the blocks
+// before it (64-bit words: flag << 62 | kept prefix << 40 | point prefix).
+constexpr unsigned long long kLookAgg = 1ull << 62, kLookInc = 2ull << 62;
+constexpr unsigned long long kLookPtsMask = (1ull << 40) - 1, kLookKeptMask = (1ull << 22) - 1;
+
+__global__ void __launch_bounds__(1024) emit_fused_kernel(const pmx_grid g, PillarWs w, int cb, int32_t pcap,
+                                                          int32_t* coords, int32_t* counts, int32_t* n_pillars) {
   __shared__ int sh[32];
+  __shared__ int s_blk;
+  __shared__ unsigned long long s_prefix;
   const int b = blockIdx.y;
   const int64_t hw = (int64_t)g.grid_h * g.grid_w;
+  if (threadIdx.x == 0) s_blk = atomicAdd(w.ticket + b, 1);
+  __syncthreads();
+  const int blk = s_blk;
   const int T = w.thresh[b];
-  int kept = 0, pts = 0;
-  int64_t c0 = (int64_t)blockIdx.x * kCellBlock + threadIdx.x * kCellPerThr;
+  const int64_t c0 = (int64_t)blk * kCellBlock + threadIdx.x * kCellPerThr;
+  int keep[kCellPerThr], n[kCellPerThr], f[kCellPerThr];
+  if ((hw & 3) == 0 && c0 + kCellPerThr <= hw) {
+    const int4 n4 = __ldg(reinterpret_cast<const int4*>(w.cnt + b * hw + c0));
+    const int4 f4 = __ldg(reinterpret_cast<const int4*>(w.first + b * hw + c0));
+    n[0] = n4.x; n[1] = n4.y; n[2] = n4.z; n[3] = n4.w;
+    f[0] = f4.x; f[1] = f4.y; f[2] = f4.z; f[3] = f4.w;
+  } else {
 #pragma unroll
-  for (int j = 0; j < kCellPerThr; ++j) {
-    int64_t c = c0 + j;
-    if (c < hw) {
-      int n = w.cnt[b * hw + c];
-      if (n > 0 && w.first[b * hw + c] <= T) {
-        kept += 1;
-        pts += n;
-      }
+    for (int j = 0; j < kCellPerThr; ++j) {
+      n[j] = c0 + j < hw ? w.cnt[b * hw + c0 + j] : 0;
+      f[j] = c0 + j < hw ? w.first[b * hw + c0 + j] : INT_MAX;
     }
   }
-  int a = block_incl_scan(kept, sh);
-  int p = block_incl_scan(pts, sh);
-  if (threadIdx.x == blockDim.x - 1) w.cblk[b * cb + blockIdx.x] = make_int2(a, p);
-}
-
-__global__ void cellscan_kernel(PillarWs w, int cb, int32_t* n_pillars) {
-  const int b = blockIdx.x;
-  if (threadIdx.x != 0) return;
-  int a = 0, p = 0;
-  for (int k = 0; k < cb; ++k) {
-    int2 v = w.cblk[b * cb + k];
-    w.cblk[b * cb + k] = make_int2(a, p);
-    a += v.x;
-    p += v.y;
-  }
-  n_pillars[b] = a;
-}
-
-__global__ void __launch_bounds__(1024) emit_kernel(const pmx_grid g, PillarWs w, int cb, int32_t pcap,
-                                                    int32_t* coords, int32_t* counts) {
-  __shared__ int sh[32];
-  const int b = blockIdx.y;
-  const int64_t hw = (int64_t)g.grid_h * g.grid_w;
-  const int T = w.thresh[b];
-  int64_t c0 = (int64_t)blockIdx.x * kCellBlock + threadIdx.x * kCellPerThr;
-  int keep[kCellPerThr], n[kCellPerThr];
   int kept = 0, pts = 0;
 #pragma unroll
   for (int j = 0; j < kCellPerThr; ++j) {
-    int64_t c = c0 + j;
-    keep[j] = 0;
-    n[j] = 0;
-    if (c < hw) {
-      n[j] = w.cnt[b * hw + c];
-      keep[j] = n[j] > 0 && w.first[b * hw + c] <= T;
-    }
+    keep[j] = n[j] > 0 && f[j] <= T;
     kept += keep[j];
     pts += keep[j] ? n[j] : 0;
   }
-  int a = block_incl_scan(kept, sh) - kept;
-  int p = block_incl_scan(pts, sh) - pts;
-  int2 base = w.cblk[b * cb + blockIdx.x];
-  a += base.x;
-  p += base.y;
+  int a = block_incl_scan(kept, sh);
+  const int kept_tot = sh[31];
+  __syncthreads();
+  int p = block_incl_scan(pts, sh);
+  const int pts_tot = sh[31];
+  a -= kept;
+  p -= pts;
+  if (threadIdx.x == 0) {
+    unsigned long long* look = w.look + (int64_t)b * cb;
+    const unsigned long long agg = ((unsigned long long)kept_tot << 40) | (unsigned long long)pts_tot;
+    unsigned long long excl = 0;
+    if (blk == 0) {
+      atomicExch(look + blk, kLookInc | agg);
+    } else {
+      atomicExch(look + blk, kLookAgg | agg);
+      for (int j = blk - 1; j >= 0; --j) {
+        unsigned long long v;
+        do {
+          v = atomicAdd(look + j, 0ull);  // L2-coherent read
+        } while ((v >> 62) == 0);
+        excl += v & ~(3ull << 62);
+        if ((v >> 62) == 2) break;
+      }
+      atomicExch(look + blk, kLookInc | (excl + agg));
+    }
+    s_prefix = excl;
+    if (blk == cb - 1) n_pillars[b] = (int)(((excl + agg) >> 40) & kLookKeptMask);
+  }
+  __syncthreads();
+  a += (int)((s_prefix >> 40) & kLookKeptMask);
+  p += (int)(s_prefix & kLookPtsMask);
 #pragma unroll
   for (int j = 0; j < kCellPerThr; ++j) {
-    int64_t c = c0 + j;
+    const int64_t c = c0 + j;
     if (c >= hw) break;
     if (keep[j]) {
-      int64_t q = (int64_t)b * pcap + a;
-      w.pid[b * hw + c] = a + 1;  // slot + 1 (0 = empty: TMA out-of-bounds fill reads as empty)
-      coords[2 * q + 0] = (int)(c / g.grid_w);
-      coords[2 * q + 1] = (int)(c % g.grid_w);
+      const int64_t q = (int64_t)b * pcap + a;
+      w.pid[b * hw + c] = a + 1;  // slot + 1 (0 = empty)
+      *reinterpret_cast<int2*>(coords + 2 * q) = make_int2((int)(c / g.grid_w), (int)(c % g.grid_w));
       counts[q] = n[j] < g.max_points ? n[j] : g.max_points;
       w.segoff[q] = p;
       a += 1;
@@ -443,7 +454,7 @@ pmx_status pmx_pillarize(const float* points, const int64_t* frame_offsets, int3
   PMX_REQUIRE(batch >= 0 && max_points_per_frame >= 0, "negative extent");
   PMX_REQUIRE(max_points_per_frame < INT_MAX, "too many points per frame");
   const int64_t hw = (int64_t)g.grid_h * g.grid_w;
-  PMX_REQUIRE(hw < INT_MAX / 2, "grid too large");
+  PMX_REQUIRE(hw < (1 << 22), "grid too large (> 4M cells)");
   if (g.max_pillars > 0) {
     PMX_REQUIRE(pcap >= g.max_pillars, "pcap < max_pillars");
   } else {
@@ -461,13 +472,13 @@ pmx_status pmx_pillarize(const float* points, const int64_t* frame_offsets, int3
   PMX_CUDA(cudaMemsetAsync(w.cnt, 0, sizeof(int32_t) * batch * hw, stream));
   PMX_CUDA(cudaMemsetAsync(w.fill, 0, sizeof(int32_t) * batch * pcap, stream));
   PMX_CUDA(cudaMemsetAsync(w.ovf_n, 0, sizeof(int32_t), stream));
+  PMX_CUDA(cudaMemsetAsync(w.look, 0, sizeof(unsigned long long) * batch * cb, stream));
+  PMX_CUDA(cudaMemsetAsync(w.ticket, 0, sizeof(int32_t) * batch, stream));
   const int ptx = (int)std::min<int64_t>(ceil_div(nmax, 256), 4096);
   bin_kernel<<<dim3(ptx, batch), 256, 0, stream>>>(reinterpret_cast<const float4*>(points), frame_offsets, nmax, g, w);
   flag_kernel<<<dim3(nb, batch), kPtBlock, 0, stream>>>(frame_offsets, nmax, g, w, nb);
   thresh_kernel<<<batch, 1024, 0, stream>>>(frame_offsets, nmax, g, w, nb);
-  cellcount_kernel<<<dim3(cb, batch), 1024, 0, stream>>>(g, w, cb);
-  cellscan_kernel<<<batch, 32, 0, stream>>>(w, cb, n_pillars);
-  emit_kernel<<<dim3(cb, batch), 1024, 0, stream>>>(g, w, cb, pcap, coords, counts);
+  emit_fused_kernel<<<dim3(cb, batch), 1024, 0, stream>>>(g, w, cb, pcap, coords, counts, n_pillars);
   slot_kernel<<<dim3(ptx, batch), 256, 0, stream>>>(frame_offsets, nmax, g, w, pcap);
   select_small_kernel<<<dim3((int)ceil_div(pcap, 256), batch), 256, 0, stream>>>(nmax, g, w, pcap, n_pillars, pt_idx);
   // overflow pillars (> 32 points): one warp each, grid-stride over the device-side list
