@@ -18,7 +18,7 @@
 namespace pmx {
 namespace {
 
-constexpr int kChunk = 2048;  // anchors per CTA
+constexpr int kChunk = 8192;  // anchors per CTA (13 CTAs per KITTI frame: fewer, fuller waves)
 constexpr int kThreads = 1024;
 constexpr int kCap = 4096;    // candidates sorted in shared memory
 
