@@ -224,6 +224,10 @@ struct TcParams {
   // writes 8 rows x 64 contiguous bytes (thread-per-row 16-byte stores scatter over
   // 32 lines per instruction and run at ~1/4 of the write bandwidth)
   int estage;
+  // the same for the (int8, f16) consumer pair of a block's last conv (next block +
+  // its FP16 deblock): the int8 codes go straight out (64-byte rows), the binary16
+  // values (128 bytes per row and warp) are staged -- 4 KB per warp
+  int estage2;
   // HALO mode
   uint32_t halo_tx;     // halo bytes per tile (TMA transaction size)
   uint32_t hp, hw;      // halo pixels, halo row width (pixels)
@@ -862,6 +866,92 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
       const uint32_t trow = tmem + acc * (uint32_t)p.bn + ((uint32_t)(q * 32) << 16);
       // deconv: output pixel of tap (0, 0); tap (dy, dx) adds dy * out_w + dx
       const uint32_t pbase = (ib * p.out_h + iy * p.stride) * p.out_w + ix * p.stride;
+      if constexpr (OUTK == 0) {
+        if (p.estage2) {
+          // int8 consumer and f16 consumer (no dynamic indexing of the parameter struct)
+          const bool i8first = outs.o[0].dtype == PMX_I8;
+          int8_t* const p8 = reinterpret_cast<int8_t*>(i8first ? outs.o[0].ptr : outs.o[1].ptr) +
+                             (i8first ? outs.o[0].c_offset : outs.o[1].c_offset);
+          const uint32_t cs8 = (uint32_t)(i8first ? outs.o[0].c_stride : outs.o[1].c_stride);
+          const double sc8 = i8first ? outs.o[0].scale : outs.o[1].scale;
+          const float inv8 = i8first ? outs.o[0].inv : outs.o[1].inv;
+          __half* const ph = reinterpret_cast<__half*>(i8first ? outs.o[1].ptr : outs.o[0].ptr) +
+                             (i8first ? outs.o[1].c_offset : outs.o[0].c_offset);
+          const uint32_t csh = (uint32_t)(i8first ? outs.o[1].c_stride : outs.o[0].c_stride);
+          const uint32_t wstage = s_estage + (uint32_t)warp * 4096u;
+          const int nbase0 = n0 + 16 * c_begin;
+          const bool live = nbase0 < p.n_gemm;  // warp-uniform (n_gemm % 64 == 0)
+#pragma unroll 1
+          for (int k = 0; k < 4; ++k) {
+            uint32_t v[16];
+            tmem_ld16_issue(trow + 16 * (c_begin + k), v);
+            tmem_ld_wait(v);
+            if (!valid || !live) continue;
+            const int cobase = nbase0 + 16 * k;
+            float y[16];
+            const float4* b4p = reinterpret_cast<const float4*>(s_bias + cobase);
+            const float4* a4p = reinterpret_cast<const float4*>(s_alpha + cobase);
+#pragma unroll
+            for (int j4 = 0; j4 < 4; ++j4) {
+              const float4 b4 = b4p[j4];
+              float2 r0, r1;
+              if constexpr (DT == PMX_I8) {
+                const float4 a4 = a4p[j4];
+                r0 = __ffma2_rn(make_float2((float)(int)v[4 * j4], (float)(int)v[4 * j4 + 1]),
+                                make_float2(a4.x, a4.y), make_float2(b4.x, b4.y));
+                r1 = __ffma2_rn(make_float2((float)(int)v[4 * j4 + 2], (float)(int)v[4 * j4 + 3]),
+                                make_float2(a4.z, a4.w), make_float2(b4.z, b4.w));
+              } else {
+                r0 = __fadd2_rn(make_float2(__uint_as_float(v[4 * j4]), __uint_as_float(v[4 * j4 + 1])),
+                                make_float2(b4.x, b4.y));
+                r1 = __fadd2_rn(make_float2(__uint_as_float(v[4 * j4 + 2]), __uint_as_float(v[4 * j4 + 3])),
+                                make_float2(b4.z, b4.w));
+              }
+              y[4 * j4] = r0.x;
+              y[4 * j4 + 1] = r0.y;
+              y[4 * j4 + 2] = r1.x;
+              y[4 * j4 + 3] = r1.y;
+            }
+            if (p.relu) {
+#pragma unroll
+              for (int j = 0; j < 16; ++j) y[j] = fmaxf(y[j], 0.f);
+            }
+            *reinterpret_cast<uint4*>(p8 + (size_t)pix_in * cs8 + cobase) = quant16(y, sc8, inv8);
+            // f16: two 16-byte slots (2k, 2k + 1) of this row's 128 bytes, XOR-swizzled by row % 8
+            const uint32_t rb = wstage + (uint32_t)lane * 128u, sw = (uint32_t)lane & 7u;
+            asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(rb + (((2u * k) ^ sw) << 4)),
+                         "r"(f16x2_sat(y[0], y[1])), "r"(f16x2_sat(y[2], y[3])), "r"(f16x2_sat(y[4], y[5])),
+                         "r"(f16x2_sat(y[6], y[7]))
+                         : "memory");
+            asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(rb + (((2u * k + 1u) ^ sw) << 4)),
+                         "r"(f16x2_sat(y[8], y[9])), "r"(f16x2_sat(y[10], y[11])), "r"(f16x2_sat(y[12], y[13])),
+                         "r"(f16x2_sat(y[14], y[15]))
+                         : "memory");
+          }
+          __syncwarp();
+          if (live) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const int r = 4 * j + (lane >> 3);
+              const uint32_t sl = (uint32_t)lane & 7u;
+              const uint32_t rp = __shfl_sync(0xffffffffu, pix_in, r);
+              const int rv = __shfl_sync(0xffffffffu, (int)valid, r);
+              uint4 w;
+              asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                           : "=r"(w.x), "=r"(w.y), "=r"(w.z), "=r"(w.w)
+                           : "r"(wstage + (uint32_t)r * 128u + ((sl ^ ((uint32_t)r & 7u)) << 4))
+                           : "memory");
+              if (rv)
+                *reinterpret_cast<uint4*>(ph + (size_t)rp * csh + nbase0 + 8 * sl) = w;
+            }
+          }
+          __syncwarp();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(tempty(acc));
+          continue;
+        }
+      }
       if constexpr (OUTK == 1) {
         if (fast && p.estage) {
           // this warp's 4 chunks = 64 consecutive output channels of its 32 rows: stage
@@ -1088,7 +1178,8 @@ int estage_min_row() {  // PMX_ESTAGE=2: stage every eligible layer (experiments
   return v;
 }
 
-Plan plan_for(const pmx_conv_desc& d, bool gather = false, bool want_stage = false, int out_row_bytes = 0) {
+Plan plan_for(const pmx_conv_desc& d, bool gather = false, bool want_stage = false, int out_row_bytes = 0,
+              bool want_stage2 = false) {
   Plan pl{};
   pl.ok = false;
   if (d.in_dtype != PMX_I8 && d.in_dtype != PMX_F16) return pl;
@@ -1174,7 +1265,9 @@ Plan plan_for(const pmx_conv_desc& d, bool gather = false, bool want_stage = fal
   p.estage = want_stage && estage_enabled() && out_row_bytes >= estage_min_row() && (bn / 16) == 4 * (4 / p.egroups) &&
              p.n_gemm % 64 == 0 &&
              (!p.deconv || (p.oc_shift >= 0 && d.out_c % 64 == 0));
-  const uint32_t estage_bytes = p.estage ? (uint32_t)kEpiWarps * 2048u : 0u;
+  p.estage2 = want_stage2 && estage_enabled() && !p.deconv && (bn / 16) == 4 * (4 / p.egroups) &&
+              p.n_gemm % 64 == 0;
+  const uint32_t estage_bytes = p.estage ? (uint32_t)kEpiWarps * 2048u : (p.estage2 ? (uint32_t)kEpiWarps * 4096u : 0u);
   p.a_bytes = 128u * kc_bytes;
   p.b_bytes = (uint32_t)bn * kc_bytes;
   const uint32_t stage = p.a_bytes + p.b_bytes;
@@ -1195,8 +1288,8 @@ Plan plan_for(const pmx_conv_desc& d, bool gather = false, bool want_stage = fal
     const uint32_t budget0 = 227u * 1024u - 2048u - 8u * (uint32_t)((d.out_c + 3) & ~3) - (gather ? (uint32_t)kGatherSmem : 0u);
     uint32_t budget = budget0 - estage_bytes;
     const uint32_t two_stages = 2 * halo_al;
-    if (p.estage && bres_total + two_stages > budget && bres_total + two_stages <= budget0) {
-      p.estage = 0;  // resident weights + two halo stages win over the store staging
+    if ((p.estage || p.estage2) && bres_total + two_stages > budget && bres_total + two_stages <= budget0) {
+      p.estage = p.estage2 = 0;  // resident weights + two halo stages win over the store staging
       budget = budget0;
     }
     if (bres_total + two_stages <= budget) {
@@ -1237,7 +1330,7 @@ Plan plan_for(const pmx_conv_desc& d, bool gather = false, bool want_stage = fal
   else
     p.idesc = (1u << 4) | (0u << 7) | (0u << 10) | (n_enc << 17) | (m_enc << 24);
   pl.smem = 1024 + (size_t)p.stages * (p.a_bytes + p.b_bytes) + p.bres_bytes + (2 * p.stages + 2 * p.nacc + 1) * 8 + 32 +
-            8 * (size_t)((d.out_c + 3) & ~3) + (gather ? kGatherSmem : 0) + (p.estage ? 16 + kEpiWarps * 2048 : 0);
+            8 * (size_t)((d.out_c + 3) & ~3) + (gather ? kGatherSmem : 0) + (p.estage ? 16 + kEpiWarps * 2048 : (p.estage2 ? 16 + kEpiWarps * 4096 : 0));
   pl.ok = true;
   return pl;
 }
@@ -1331,7 +1424,14 @@ pmx_status conv_tc_try(const pmx_conv_desc& d, const void* x, const void* w, con
   // OUTK 1: the common single int8 consumer with 16-byte aligned pixel rows
   const bool one_i8 = outs.n == 1 && outs.o[0].dtype == PMX_I8 && outs.o[0].c_stride % 16 == 0 &&
                       outs.o[0].c_offset % 16 == 0 && (reinterpret_cast<uintptr_t>(outs.o[0].ptr) & 15) == 0;
-  Plan pl = plan_for(d, gather, one_i8 && !bn_post && !keys, outs.o[0].c_stride);
+  // (int8, f16) consumer pair with 16-byte aligned rows: staged f16 stores
+  bool pair = outs.n == 2 && !bn_post && !keys && (outs.o[0].dtype == PMX_I8) != (outs.o[1].dtype == PMX_I8);
+  for (int i = 0; pair && i < 2; ++i) {
+    const int esz = outs.o[i].dtype == PMX_I8 ? 1 : 2;
+    pair = (outs.o[i].dtype == PMX_I8 || outs.o[i].dtype == PMX_F16) && (outs.o[i].c_stride * esz) % 16 == 0 &&
+           (outs.o[i].c_offset * esz) % 16 == 0 && (reinterpret_cast<uintptr_t>(outs.o[i].ptr) & 15) == 0;
+  }
+  Plan pl = plan_for(d, gather, one_i8 && !bn_post && !keys, outs.o[0].c_stride, pair);
   if (!pl.ok) return PMX_OK;
   if (gather && pl.p.mode != MODE_HALO) return PMX_OK;
   if ((reinterpret_cast<uintptr_t>(x) & 15) || (reinterpret_cast<uintptr_t>(w) & 15)) return PMX_OK;
