@@ -878,17 +878,11 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
           __half* const ph = reinterpret_cast<__half*>(i8first ? outs.o[1].ptr : outs.o[0].ptr) +
                              (i8first ? outs.o[1].c_offset : outs.o[0].c_offset);
           const uint32_t csh = (uint32_t)(i8first ? outs.o[1].c_stride : outs.o[0].c_stride);
-          const uint32_t wstage = s_estage + (uint32_t)warp * 4096u;
           const int nbase0 = n0 + 16 * c_begin;
           const bool live = nbase0 < p.n_gemm;  // warp-uniform (n_gemm % 64 == 0)
-#pragma unroll 1
-          for (int k = 0; k < 4; ++k) {
-            uint32_t v[16];
-            tmem_ld16_issue(trow + 16 * (c_begin + k), v);
-            tmem_ld_wait(v);
-            if (!valid || !live) continue;
+          // y = epilogue of chunk k of this row; int8 codes stored directly
+          auto chunk = [&](int k, const uint32_t (&v)[16], float (&y)[16]) {
             const int cobase = nbase0 + 16 * k;
-            float y[16];
             const float4* b4p = reinterpret_cast<const float4*>(s_bias + cobase);
             const float4* a4p = reinterpret_cast<const float4*>(s_alpha + cobase);
 #pragma unroll
@@ -917,35 +911,81 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
               for (int j = 0; j < 16; ++j) y[j] = fmaxf(y[j], 0.f);
             }
             *reinterpret_cast<uint4*>(p8 + (size_t)pix_in * cs8 + cobase) = quant16(y, sc8, inv8);
-            // f16: two 16-byte slots (2k, 2k + 1) of this row's 128 bytes, XOR-swizzled by row % 8
-            const uint32_t rb = wstage + (uint32_t)lane * 128u, sw = (uint32_t)lane & 7u;
-            asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(rb + (((2u * k) ^ sw) << 4)),
-                         "r"(f16x2_sat(y[0], y[1])), "r"(f16x2_sat(y[2], y[3])), "r"(f16x2_sat(y[4], y[5])),
-                         "r"(f16x2_sat(y[6], y[7]))
+          };
+          auto sts_f16 = [&](uint32_t a0, uint32_t a1, const float (&y)[16]) {
+            asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a0), "r"(f16x2_sat(y[0], y[1])),
+                         "r"(f16x2_sat(y[2], y[3])), "r"(f16x2_sat(y[4], y[5])), "r"(f16x2_sat(y[6], y[7]))
                          : "memory");
-            asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(rb + (((2u * k + 1u) ^ sw) << 4)),
-                         "r"(f16x2_sat(y[8], y[9])), "r"(f16x2_sat(y[10], y[11])), "r"(f16x2_sat(y[12], y[13])),
-                         "r"(f16x2_sat(y[14], y[15]))
+            asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a1), "r"(f16x2_sat(y[8], y[9])),
+                         "r"(f16x2_sat(y[10], y[11])), "r"(f16x2_sat(y[12], y[13])), "r"(f16x2_sat(y[14], y[15]))
                          : "memory");
-          }
-          __syncwarp();
-          if (live) {
+          };
+          if (p.estage2 == 2) {
+            // small staging (1 KB per warp): each chunk's 32 bytes per row go out right away
+            // as 16 rows x 32 bytes (full sectors) per store instruction
+            const uint32_t wstage = s_estage + (uint32_t)warp * 1024u;
+            const uint32_t sw = ((uint32_t)lane >> 2) & 1u;  // 16-byte slot swizzle (row / 4)
+#pragma unroll 1
+            for (int k = 0; k < 4; ++k) {
+              uint32_t v[16];
+              tmem_ld16_issue(trow + 16 * (c_begin + k), v);
+              tmem_ld_wait(v);
+              if (valid && live) {
+                float y[16];
+                chunk(k, v, y);
+                sts_f16(wstage + (uint32_t)lane * 32u + (sw << 4), wstage + (uint32_t)lane * 32u + ((1u ^ sw) << 4), y);
+              }
+              __syncwarp();
+              if (live) {
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              const int r = 4 * j + (lane >> 3);
-              const uint32_t sl = (uint32_t)lane & 7u;
-              const uint32_t rp = __shfl_sync(0xffffffffu, pix_in, r);
-              const int rv = __shfl_sync(0xffffffffu, (int)valid, r);
-              uint4 w;
-              asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-                           : "=r"(w.x), "=r"(w.y), "=r"(w.z), "=r"(w.w)
-                           : "r"(wstage + (uint32_t)r * 128u + ((sl ^ ((uint32_t)r & 7u)) << 4))
-                           : "memory");
-              if (rv)
-                *reinterpret_cast<uint4*>(ph + (size_t)rp * csh + nbase0 + 8 * sl) = w;
+                for (int j = 0; j < 2; ++j) {
+                  const int r = 16 * j + (lane >> 1);
+                  const uint32_t sl = (uint32_t)lane & 1u;
+                  const uint32_t rp = __shfl_sync(0xffffffffu, pix_in, r);
+                  const int rv = __shfl_sync(0xffffffffu, (int)valid, r);
+                  uint4 w;
+                  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                               : "=r"(w.x), "=r"(w.y), "=r"(w.z), "=r"(w.w)
+                               : "r"(wstage + (uint32_t)r * 32u + ((sl ^ (((uint32_t)r >> 2) & 1u)) << 4))
+                               : "memory");
+                  if (rv) *reinterpret_cast<uint4*>(ph + (size_t)rp * csh + nbase0 + 16 * k + 8 * sl) = w;
+                }
+              }
+              __syncwarp();
             }
+          } else {
+            // 4 KB per warp: the warp's 64 channels of f16 (128 bytes per row), slots
+            // (2k, 2k + 1) XOR-swizzled by row % 8; then 4 rows x 128 bytes per store
+            const uint32_t wstage = s_estage + (uint32_t)warp * 4096u;
+            const uint32_t rb = wstage + (uint32_t)lane * 128u, sw = (uint32_t)lane & 7u;
+#pragma unroll 1
+            for (int k = 0; k < 4; ++k) {
+              uint32_t v[16];
+              tmem_ld16_issue(trow + 16 * (c_begin + k), v);
+              tmem_ld_wait(v);
+              if (!valid || !live) continue;
+              float y[16];
+              chunk(k, v, y);
+              sts_f16(rb + (((2u * k) ^ sw) << 4), rb + (((2u * k + 1u) ^ sw) << 4), y);
+            }
+            __syncwarp();
+            if (live) {
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                const int r = 4 * j + (lane >> 3);
+                const uint32_t sl = (uint32_t)lane & 7u;
+                const uint32_t rp = __shfl_sync(0xffffffffu, pix_in, r);
+                const int rv = __shfl_sync(0xffffffffu, (int)valid, r);
+                uint4 w;
+                asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                             : "=r"(w.x), "=r"(w.y), "=r"(w.z), "=r"(w.w)
+                             : "r"(wstage + (uint32_t)r * 128u + ((sl ^ ((uint32_t)r & 7u)) << 4))
+                             : "memory");
+                if (rv) *reinterpret_cast<uint4*>(ph + (size_t)rp * csh + nbase0 + 8 * sl) = w;
+              }
+            }
+            __syncwarp();
           }
-          __syncwarp();
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(tempty(acc));
@@ -1267,7 +1307,11 @@ Plan plan_for(const pmx_conv_desc& d, bool gather = false, bool want_stage = fal
              (!p.deconv || (p.oc_shift >= 0 && d.out_c % 64 == 0));
   p.estage2 = want_stage2 && estage_enabled() && !p.deconv && (bn / 16) == 4 * (4 / p.egroups) &&
               p.n_gemm % 64 == 0;
-  const uint32_t estage_bytes = p.estage ? (uint32_t)kEpiWarps * 2048u : (p.estage2 ? (uint32_t)kEpiWarps * 4096u : 0u);
+  auto estage_bytes_of = [&] {
+    return p.estage ? (uint32_t)kEpiWarps * 2048u
+                    : (p.estage2 == 1 ? (uint32_t)kEpiWarps * 4096u : (p.estage2 == 2 ? (uint32_t)kEpiWarps * 1024u : 0u));
+  };
+  uint32_t estage_bytes = estage_bytes_of();
   p.a_bytes = 128u * kc_bytes;
   p.b_bytes = (uint32_t)bn * kc_bytes;
   const uint32_t stage = p.a_bytes + p.b_bytes;
@@ -1288,6 +1332,12 @@ Plan plan_for(const pmx_conv_desc& d, bool gather = false, bool want_stage = fal
     const uint32_t budget0 = 227u * 1024u - 2048u - 8u * (uint32_t)((d.out_c + 3) & ~3) - (gather ? (uint32_t)kGatherSmem : 0u);
     uint32_t budget = budget0 - estage_bytes;
     const uint32_t two_stages = 2 * halo_al;
+    if (p.estage2 == 1 && bres_total + two_stages > budget &&
+        bres_total + two_stages <= budget0 - (uint32_t)kEpiWarps * 1024u) {
+      p.estage2 = 2;  // resident weights + two halo stages fit next to the 1 KB-per-warp staging
+      estage_bytes = estage_bytes_of();
+      budget = budget0 - estage_bytes;
+    }
     if ((p.estage || p.estage2) && bres_total + two_stages > budget && bres_total + two_stages <= budget0) {
       p.estage = p.estage2 = 0;  // resident weights + two halo stages win over the store staging
       budget = budget0;
@@ -1330,7 +1380,7 @@ Plan plan_for(const pmx_conv_desc& d, bool gather = false, bool want_stage = fal
   else
     p.idesc = (1u << 4) | (0u << 7) | (0u << 10) | (n_enc << 17) | (m_enc << 24);
   pl.smem = 1024 + (size_t)p.stages * (p.a_bytes + p.b_bytes) + p.bres_bytes + (2 * p.stages + 2 * p.nacc + 1) * 8 + 32 +
-            8 * (size_t)((d.out_c + 3) & ~3) + (gather ? kGatherSmem : 0) + (p.estage ? 16 + kEpiWarps * 2048 : (p.estage2 ? 16 + kEpiWarps * 4096 : 0));
+            8 * (size_t)((d.out_c + 3) & ~3) + (gather ? kGatherSmem : 0) + (estage_bytes ? 16 + estage_bytes : 0);
   pl.ok = true;
   return pl;
 }
