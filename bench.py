@@ -270,8 +270,19 @@ def main():
         t_bound = sum(max(info[k]["flops"] / (pk.get(info[k]["precision"], peaks["bf16_tflops"]) * 1e12),
                           info[k].get("bytes", 0) / (peaks["hbm_gbs"] * 1e9)) for k in info)
         achieved = conv_flops / (conv_ms / 1e3) / 1e12
+        # DRAM traffic of the same 20 conv launches (one step, batch 32) from the committed ncu
+        # capture (tools/traffic.py) next to their algorithmic bytes
+        traffic = None
+        tf = ROOT / "profiles" / "r1_step_traffic.json"
+        if tf.exists():
+            traffic = json.loads(tf.read_text()).get("conv_dram_bytes")
+        alg_bytes = sum(info[k].get("bytes", 0) for k in info)
         roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                    "frac": achieved / peak, "traffic": None,
+                    "frac": achieved / peak, "traffic": traffic,
+                    "traffic_note": "bytes per step: DRAM read+write of the 20 conv launches (ncu, "
+                                    "profiles/r1_step_traffic.json) vs algorithmic_bytes (each layer's input + "
+                                    "weights + outputs once)",
+                    "algorithmic_bytes": alg_bytes,
                     "kernel": "pmx_conv implicit GEMM, all 20 conv/deconv/head launches of a step",
                     "algorithmic": f"{conv_flops / B / 1e9:.2f} GFLOP/frame x {B} frames per step",
                     "share_of_step": conv_ms / step_ms_eager,

@@ -431,14 +431,17 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
 // tile of the (virtual) canvas x[b, y, x, :] = feats[b * pcap + map[b, y, x] - 1, :]
 // (0 where map == 0 or outside the grid) is built in shared memory by 96 threads in
 // exactly the layout the TMA halo path produces -- per parity plane, [channel
-// group][plane pixel][16 B].  Every thread owns up to kPixPerThr fixed halo pixels;
-// per tile:
-//   A  its pixels' cell-map entries (loaded during the previous tile) -> compact
-//      list of occupied halo pixels (~7% at KITTI density); the next tile's map
-//      entries are loaded right away so that round trip overlaps this tile;
-//   B2 the 16-byte feature loads of the listed pixels (one round trip per tile);
-//   B1 zero-fill the stage, barrier, then B2's stores overwrite the occupied pixels;
-//      a proxy fence publishes the generic-proxy stores to the tensor core.
+// group][plane pixel][16 B].  Every thread owns kPixPerThr fixed halo pixels and,
+// per tile, independently of the others (no barriers, no shared lists):
+//   waits for the stage, zeroes its pixels the stage's previous tile filled, copies
+//   the feature rows of its occupied pixels (~7% at KITTI density) with cp.async
+//   straight into the stage, and arrives on the stage's full barrier through
+//   cp.async.mbarrier.arrive (the arrival lands when its copies have); the cell-map
+//   entries of its next tile are loaded meanwhile.
+// The MMA warp's tcgen05.mma reads the stage through the async proxy: it issues a
+// proxy fence after the full-barrier wait.  (The tensor core saturates shared-memory
+// bandwidth on this N = 64 layer, so the producer avoids every dependent
+// shared-memory round trip.)
 // Replaces the canvas write of pm/tensor_ops.py:138-160 + the conv's canvas read.
 template <int HS>
 struct GatherGeom {
@@ -456,18 +459,26 @@ __host__ __device__ constexpr int plane_p0(int hs, int q) {
 
 // smem of the gather producer (after alpha / bias): counters, two occupied-pixel
 // lists (load side, one per tile in flight) and one clear list per stage
-constexpr int kGatherSmem = 2304;  // gather producer: 4 counters + the occupied-pixel list (561 entries)
+constexpr int kGatherSmem = 0;  // the cp.async gather producer keeps its state in registers
+
+// 16 zero bytes into shared memory through cp.async (src-size 0: nothing is read)
+__device__ __forceinline__ void cp_async_zero16(uint32_t dst, const void* any_global) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, 0;" ::"r"(dst), "l"(any_global) : "memory");
+}
 
 template <int CINB, int HS, typename FullF, typename EmptyF>
-__device__ __forceinline__ void gather_producer(const TcParams& p, uint32_t a_smem, int gt, int lane, int total,
-                                                int32_t* s_list, int32_t* s_cnt, FullF full, EmptyF empty) {
+__device__ __forceinline__ void gather_producer(const TcParams& p, uint32_t a_smem, int gt, int total, FullF full,
+                                                EmptyF empty) {
   using Geo = GatherGeom<HS>;
   constexpr int G = CINB / 16;  // 16-byte channel groups per pixel
   constexpr int NT = 32 * kGatherWarps;
   static_assert(NT * kPixPerThr >= Geo::HPX_TOTAL, "halo pixels per thread");
   const char* feats = reinterpret_cast<const char*>(p.g_feats);
-  // my halo pixels: offset from the tile's input origin and the list code (plane << 10 | pixel)
-  int ry[kPixPerThr], rx[kPixPerThr], code[kPixPerThr];
+  // my halo pixels: offset from the tile's input origin and the stage offset of
+  // channel group 0 (group g adds g * plane pixels * 16 bytes)
+  int ry[kPixPerThr], rx[kPixPerThr];
+  uint32_t dst0[kPixPerThr], gstep[kPixPerThr];
+  uint32_t have = 0;  // bit j: pixel j exists
 #pragma unroll
   for (int j = 0; j < kPixPerThr; ++j) {
     const int hp = gt + NT * j;
@@ -479,7 +490,9 @@ __device__ __forceinline__ void gather_producer(const TcParams& p, uint32_t a_sm
     const int py = q >> 1, px = q & 1;
     ry[j] = HS == 2 ? 2 * (r - py) + py : r - 1;  // iy = stride * oy0 + ry
     rx[j] = HS == 2 ? 2 * (c - px) + px : c - 1;
-    code[j] = hp < Geo::HPX_TOTAL ? (pp | (q << 10)) : -1;
+    dst0[j] = (uint32_t)(plane_p0(HS, q) * G + pp) * 16u;
+    gstep[j] = (uint32_t)plane_hpx(HS, q) * 16u;
+    if (hp < Geo::HPX_TOTAL) have |= 1u << j;
   }
   auto load_map = [&](int t, int (&m)[kPixPerThr]) {
     const int tq = (int)fdiv((uint32_t)t, p.fd_tx), tx = t - tq * p.tiles_x;
@@ -490,70 +503,54 @@ __device__ __forceinline__ void gather_producer(const TcParams& p, uint32_t a_sm
     for (int j = 0; j < kPixPerThr; ++j) {
       const int iy = HS * oy0 + ry[j], ix = HS * ox0 + rx[j];
       m[j] = 0;
-      if (code[j] >= 0 && (unsigned)iy < (unsigned)p.in_h && (unsigned)ix < (unsigned)p.in_w)
+      if (((have >> j) & 1) && (unsigned)iy < (unsigned)p.in_h && (unsigned)ix < (unsigned)p.in_w)
         m[j] = __ldg(map + iy * p.in_w + ix);
     }
   };
+  // every thread owns its pixels in every stage: zero them once, afterwards clear only
+  // the pixels the stage's previous tile filled (bits in clr, kPixPerThr per stage).
+  // Zeros are written by cp.async with a zero source size, so every write to a stage
+  // is tracked by the thread's cp.async.mbarrier.arrive on the stage's full barrier.
+  for (int st = 0; st < p.stages; ++st)
+#pragma unroll
+    for (int j = 0; j < kPixPerThr; ++j)
+      if ((have >> j) & 1)
+        for (int g = 0; g < G; ++g)
+          cp_async_zero16(a_smem + st * p.a_bytes + dst0[j] + g * gstep[j], feats);
+  uint64_t clr = 0;
   int mcur[kPixPerThr];
   if (blockIdx.x < total) load_map(blockIdx.x, mcur);
   uint32_t s = 0, ph = 0;
-  int i = 0;
-  for (int t = blockIdx.x; t < total; t += gridDim.x, ++i) {
+  for (int t = blockIdx.x; t < total; t += gridDim.x) {
     const int tb = (int)fdiv(fdiv((uint32_t)t, p.fd_tx), p.fd_ty);
     const char* fb = feats + (int64_t)tb * p.g_pcap * p.g_row_bytes;
-    int32_t* cnt = s_cnt + (i & 1);
-    // A: occupied pixels -> s_list (code | (slot << 12))
-#pragma unroll
-    for (int j = 0; j < kPixPerThr; ++j)
-      if (mcur[j] != 0) s_list[atomicAdd(cnt, 1)] = code[j] | ((mcur[j] - 1) << 12);
-    const int tn = t + gridDim.x;
-    if (tn < total) load_map(tn, mcur);  // next tile's map: in flight during B
-    asm volatile("bar.sync 2, %0;" ::"r"(NT) : "memory");
-    if (gt == 0) s_cnt[(i + 1) & 1] = 0;
-    const int n_items = *cnt * G;
-    // B2 (first batch): feature loads of the occupied pixels
-    uint4 v[4];
-    uint32_t dst[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int it = gt + u * NT;
-      dst[u] = 0;
-      if (it < n_items) {
-        const uint32_t e = (uint32_t)s_list[it / G];
-        const int g = it % G, pp = e & 1023, q = (e >> 10) & 3;
-        const int m = (int)(e >> 12);
-        v[u] = __ldg(reinterpret_cast<const uint4*>(fb + (int64_t)m * p.g_row_bytes + g * 16));
-        dst[u] = (uint32_t)(plane_p0(HS, q) * G + g * plane_hpx(HS, q) + pp) * 16u;
-      }
-    }
-    // B1: zero-fill the stage
     mbar_wait(empty(s), ph ^ 1);
     const uint32_t slot = a_smem + s * p.a_bytes;
-    for (int it = gt; it < Geo::HPX_TOTAL * G; it += NT)
-      asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(slot + 16u * it), "r"(0) : "memory");
-    asm volatile("bar.sync 2, %0;" ::"r"(NT) : "memory");
+    const uint32_t old = (uint32_t)(clr >> (kPixPerThr * s)) & ((1u << kPixPerThr) - 1);
+    uint32_t now = 0;
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
-      if (gt + u * NT < n_items)
-        asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(slot + dst[u]), "r"(v[u].x), "r"(v[u].y),
-                     "r"(v[u].z), "r"(v[u].w)
-                     : "memory");
-    // dense tiles (> 4 NT chunks): the rest
-    for (int it = gt + 4 * NT; it < n_items; it += NT) {
-      const uint32_t e = (uint32_t)s_list[it / G];
-      const int g = it % G, pp = e & 1023, q = (e >> 10) & 3;
-      const int m = (int)(e >> 12);
-      const uint4 w4 = __ldg(reinterpret_cast<const uint4*>(fb + (int64_t)m * p.g_row_bytes + g * 16));
-      asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(
-                       slot + (uint32_t)(plane_p0(HS, q) * G + g * plane_hpx(HS, q) + pp) * 16u),
-                   "r"(w4.x), "r"(w4.y), "r"(w4.z), "r"(w4.w)
-                   : "memory");
+    for (int j = 0; j < kPixPerThr; ++j) {
+      if ((old >> j) & 1)
+        for (int g = 0; g < G; ++g)
+          cp_async_zero16(slot + dst0[j] + g * gstep[j], feats);
+      if (mcur[j] != 0) {
+        // occupied pixel: its feature row (G x 16 bytes) straight into the stage
+        const char* src = fb + (int64_t)(mcur[j] - 1) * p.g_row_bytes;
+        for (int g = 0; g < G; ++g)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(slot + dst0[j] + g * gstep[j]),
+                       "l"(src + 16 * g)
+                       : "memory");
+        now |= 1u << j;
+      }
     }
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    __syncwarp();
-    if (lane == 0) mbar_arrive(full(s));
+    clr = (clr & ~((uint64_t)((1u << kPixPerThr) - 1) << (kPixPerThr * s))) | ((uint64_t)now << (kPixPerThr * s));
+    // the stage's full barrier counts this thread once its copies have landed
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(full(s)) : "memory");
+    const int tn = t + gridDim.x;
+    if (tn < total) load_map(tn, mcur);  // in flight while the next stage frees up
     if (++s == (uint32_t)p.stages) s = 0, ph ^= 1;
   }
+  asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
 // Persistent: grid = min(tiles, SMs); every role walks the same static tile sequence.
@@ -589,7 +586,7 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
   if (threadIdx.x == 0) {
     PMX_TRACE(8, 0);
     for (int s = 0; s < p.stages; ++s) {
-      mbar_init(full(s), GATHER ? kGatherWarps : 1);  // TMA: expect_tx; gather: one arrive per warp
+      mbar_init(full(s), GATHER ? 32 * kGatherWarps : 1);  // TMA: expect_tx; gather: one cp.async arrive per thread
       mbar_init(empty(s), 1);
     }
     for (int a = 0; a < p.nacc; ++a) {
@@ -597,10 +594,6 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
       mbar_init(tempty(a), 4 * (4 / p.egroups));  // the warps draining one tile
     }
     mbar_init(bfull, 1);
-    if constexpr (GATHER) {
-      int32_t* s_cnt = reinterpret_cast<int32_t*>(s_bias + ((p.out_c + 3) & ~3));
-      s_cnt[0] = s_cnt[1] = 0;
-    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == kMmaWarp) {
@@ -638,10 +631,8 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
 
   if (GATHER && (warp == kProdWarp || warp > kMmaWarp)) {
     if constexpr (GATHER) {
-      // smem after alpha / bias: two list counters, the occupied-pixel list
-      int32_t* s_cnt = reinterpret_cast<int32_t*>(s_bias + ((p.out_c + 3) & ~3));
-      gather_producer<CINB, HS>(p, a_smem, warp == kProdWarp ? lane : 32 * (warp - kMmaWarp) + lane, lane, total,
-                                s_cnt + 4, s_cnt, full, empty);
+      gather_producer<CINB, HS>(p, a_smem, warp == kProdWarp ? lane : 32 * (warp - kMmaWarp) + lane, total, full,
+                                empty);
     }
   } else if (warp == kProdWarp) {
     if (lane == 0) {
@@ -734,6 +725,8 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
         if (lane == 0) PMX_TRACE(2, i);
         mbar_spin(full(s), ph);
         tc_fence_after();
+        // GATHER: the stage was written through the generic proxy (st.shared, cp.async)
+        if constexpr (GATHER) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         if (elect_one()) {
           PMX_TRACE(3, i);
           const uint32_t alo = (a_smem + s * p.a_bytes) >> 4;

@@ -18,7 +18,7 @@ from paper_2601_12638_b200 import _native as N  # noqa: E402
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--op", default="conv backbone.blocks.0.3")
+    ap.add_argument("--op", default="conv backbone.blocks.0.3", help='an op name (--list) or "all"')
     ap.add_argument("--batch", type=int, default=32)
     ap.add_argument("--points", type=int, default=120000)
     ap.add_argument("--plan", default="FP16: 2,18,19,20")
@@ -37,7 +37,12 @@ def main():
     for _ in range(2):
         eng.run()
     torch.cuda.synchronize()
-    fn = dict(eng.cg.ops)[args.op]
+    if args.op == "all":  # one whole eager step (every op in order) inside the profiler range
+        def fn(stream):
+            for _, f in eng.cg.ops:
+                f(stream)
+    else:
+        fn = dict(eng.cg.ops)[args.op]
     if args.time:
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
