@@ -518,8 +518,11 @@ __device__ __forceinline__ void gather_producer(const TcParams& p, uint32_t a_sm
         for (int g = 0; g < G; ++g)
           cp_async_zero16(a_smem + st * p.a_bytes + dst0[j] + g * gstep[j], feats);
   uint64_t clr = 0;
-  int mcur[kPixPerThr];
+  // cell-map entries of this tile and of the next one (loaded a whole tile ahead, so
+  // the copies of a stage wait for one L2 round trip, not two)
+  int mcur[kPixPerThr], mnext[kPixPerThr];
   if (blockIdx.x < total) load_map(blockIdx.x, mcur);
+  if (blockIdx.x + (int)gridDim.x < total) load_map(blockIdx.x + gridDim.x, mnext);
   uint32_t s = 0, ph = 0;
   for (int t = blockIdx.x; t < total; t += gridDim.x) {
     const int tb = (int)fdiv(fdiv((uint32_t)t, p.fd_tx), p.fd_ty);
@@ -546,8 +549,10 @@ __device__ __forceinline__ void gather_producer(const TcParams& p, uint32_t a_sm
     clr = (clr & ~((uint64_t)((1u << kPixPerThr) - 1) << (kPixPerThr * s))) | ((uint64_t)now << (kPixPerThr * s));
     // the stage's full barrier counts this thread once its copies have landed
     asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(full(s)) : "memory");
-    const int tn = t + gridDim.x;
-    if (tn < total) load_map(tn, mcur);  // in flight while the next stage frees up
+#pragma unroll
+    for (int j = 0; j < kPixPerThr; ++j) mcur[j] = mnext[j];
+    const int tn2 = t + 2 * (int)gridDim.x;
+    if (tn2 < total) load_map(tn2, mnext);  // in flight for a whole tile
     if (++s == (uint32_t)p.stages) s = 0, ph ^= 1;
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
