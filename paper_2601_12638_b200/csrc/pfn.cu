@@ -228,13 +228,14 @@ __global__ void __launch_bounds__(kThreads) pfn_kernel(const PfnArgs a, const Ou
 //   32 pillars, the FMA chain over the features (broadcast shared-memory reads) and the
 //   max over points; epilogue once per pillar; 128-byte coalesced row stores.
 // Points beyond kSlots (dense clusters, M up to 32) are rebuilt in phase B.
-constexpr int kSlots = 8;
-// one point record = the 9 transformed features in layer 1's storage type, padded to
-// whole 16-byte rows: int8 codes 16 B, binary16 32 B, f32 48 B
+constexpr int kSlots = 4;  // KITTI pillars hold ~1.3 points; more are rebuilt in phase B
+// one point record = the 9 transformed features (int8 codes / binary16 values are
+// exact in f32) as f32, padded to 48 bytes: phase B reads three broadcast float4 and
+// converts nothing
 template <int DT>
 struct Rec {
-  using T = typename std::conditional<DT == PMX_I8, int8_t, typename std::conditional<DT == PMX_F16, __half, float>::type>::type;
-  static constexpr int N = DT == PMX_I8 ? 16 : (DT == PMX_F16 ? 16 : 12);  // elements per record
+  using T = float;
+  static constexpr int N = 12;  // elements per record
   static constexpr int BYTES = N * (int)sizeof(T);
 };
 template <int DT>
@@ -259,7 +260,7 @@ __device__ __forceinline__ void store2(const OutDev& o, int64_t pix, int c, floa
 }
 
 template <int DT>
-__global__ void __launch_bounds__(kThreads, 3) pfn_points_kernel(const PfnArgs a, const Outs outs) {
+__global__ void __launch_bounds__(kThreads, 2) pfn_points_kernel(const PfnArgs a, const Outs outs) {
   using R = Rec<DT>;
   using T = typename R::T;
   extern __shared__ __align__(16) uint8_t pfn_smem[];
@@ -318,10 +319,12 @@ __global__ void __launch_bounds__(kThreads, 3) pfn_points_kernel(const PfnArgs a
   const float fk = (float)(k > 0 ? k : 1);
   const float mxm = __fdiv_rn(sx, fk), mym = __fdiv_rn(sy, fk), mzm = __fdiv_rn(sz, fk);
   float xc = 0.f, yc = 0.f;
+  int64_t mypix = q;  // output row of this lane's pillar (canvas pixel, or the pillar slot)
   if (live) {
     const int2 cc = *reinterpret_cast<const int2*>(a.coords + 2 * q);
     xc = __fadd_rn(__fmul_rn((float)cc.y, a.g.cell_w), xoff);
     yc = __fadd_rn(__fmul_rn((float)cc.x, a.g.cell_h), yoff);
+    if (!a.dense) mypix = ((int64_t)b * a.g.grid_h + cc.x) * a.g.grid_w + cc.y;
   }
   if (live && k < M) { in_lo = 0.f; in_hi = 0.f; }  // zero padding rows are part of layer 1's input
   auto feats = [&](const float4& pt, float (&f)[9]) {
@@ -338,14 +341,13 @@ __global__ void __launch_bounds__(kThreads, 3) pfn_points_kernel(const PfnArgs a
 #pragma unroll
         for (int j = 0; j < 9; ++j) { in_lo = nmin(in_lo, f[j]); in_hi = nmax(in_hi, f[j]); }
       }
-      T* dst = sf[warp][lane][s];
+      float t9[9];
 #pragma unroll
-      for (int j = 0; j < 9; ++j) {
-        const float v = transform_in<DT>(f[j], a);  // exactly representable in T
-        if constexpr (DT == PMX_I8) dst[j] = (int8_t)(int)v;
-        else if constexpr (DT == PMX_F16) dst[j] = __float2half_rn(v);
-        else dst[j] = v;
-      }
+      for (int j = 0; j < 9; ++j) t9[j] = transform_in<DT>(f[j], a);  // exact in f32
+      float4* dst = reinterpret_cast<float4*>(sf[warp][lane][s]);
+      dst[0] = make_float4(t9[0], t9[1], t9[2], t9[3]);
+      dst[1] = make_float4(t9[4], t9[5], t9[6], t9[7]);
+      dst[2] = make_float4(t9[8], 0.f, 0.f, 0.f);
     }
   }
   if (k > kSlots) {
@@ -385,6 +387,9 @@ __global__ void __launch_bounds__(kThreads, 3) pfn_points_kernel(const PfnArgs a
     bi[u] = c + u < C ? a.bias[c + u] : 0.f;
   }
   float o_lo = INF, o_hi = -INF;
+  // single f16 consumer with 8-byte aligned 4-channel runs (kernel-uniform)
+  const bool f16_only = outs.n == 1 && outs.o[0].dtype == PMX_F16 && (outs.o[0].c_stride & 3) == 0 &&
+                        (outs.o[0].c_offset & 3) == 0;
   for (int it = 0; it < 16; ++it) {
     const int j = 2 * it + half;
     const int kj = __shfl_sync(0xffffffffu, k, j);
@@ -420,23 +425,10 @@ __global__ void __launch_bounds__(kThreads, 3) pfn_points_kernel(const PfnArgs a
     for (int s2 = 0; s2 < kk; ++s2) {
       if (s2 >= kj) continue;
       float f[9];
-      const uint4* src = reinterpret_cast<const uint4*>(sf[warp][j][s2]);  // two broadcast addresses
-      if constexpr (DT == PMX_I8) {
-        const uint4 r = src[0];
-        const uint32_t wd[3] = {r.x, r.y, r.z};
-#pragma unroll
-        for (int t = 0; t < 9; ++t) f[t] = (float)(int8_t)((wd[t >> 2] >> (8 * (t & 3))) & 0xff);
-      } else if constexpr (DT == PMX_F16) {
-        const uint4 r0 = src[0], r1 = src[1];
-        const uint32_t wd[5] = {r0.x, r0.y, r0.z, r0.w, r1.x};
-#pragma unroll
-        for (int t = 0; t < 9; ++t) f[t] = __half2float(__ushort_as_half((unsigned short)(wd[t >> 1] >> (16 * (t & 1)))));
-      } else {
-        const float4 f0 = reinterpret_cast<const float4*>(src)[0], f1 = reinterpret_cast<const float4*>(src)[1],
-                     f2 = reinterpret_cast<const float4*>(src)[2];
-        f[0] = f0.x; f[1] = f0.y; f[2] = f0.z; f[3] = f0.w; f[4] = f1.x; f[5] = f1.y; f[6] = f1.z; f[7] = f1.w;
-        f[8] = f2.x;
-      }
+      const float4* src = reinterpret_cast<const float4*>(sf[warp][j][s2]);  // two broadcast addresses
+      const float4 f0 = src[0], f1 = src[1], f2 = src[2];
+      f[0] = f0.x; f[1] = f0.y; f[2] = f0.z; f[3] = f0.w; f[4] = f1.x; f[5] = f1.y; f[6] = f1.z; f[7] = f1.w;
+      f[8] = f2.x;
       point(f);
     }
     if (kpair > kSlots) {  // dense cluster: rebuild the remaining points (broadcast loads per half)
@@ -465,12 +457,17 @@ __global__ void __launch_bounds__(kThreads, 3) pfn_points_kernel(const PfnArgs a
         if (a.d.relu) y[u] = fmaxf(y[u], 0.f);
       }
     }
-    int64_t pix = qj;
-    if (!a.dense) {
-      const int2 cc = *reinterpret_cast<const int2*>(a.coords + 2 * qj);
-      pix = ((int64_t)b * a.g.grid_h + cc.x) * a.g.grid_w + cc.y;
-    }
+    const int64_t pix = __shfl_sync(0xffffffffu, mypix, j);
     const int nl = C - c < 4 ? C - c : 4;
+    if (f16_only && nl == 4) {
+      // the common single binary16 consumer (next layer FP16): one 8-byte store
+      *reinterpret_cast<uint2*>(reinterpret_cast<__half*>(outs.o[0].ptr) + pix * outs.o[0].c_stride +
+                                outs.o[0].c_offset + c) = make_uint2(f16x2_sat(y[0], y[1]), f16x2_sat(y[2], y[3]));
+      if (a.out_keys) {
+        for (int u = 0; u < nl; ++u) { o_lo = nmin(o_lo, y[u]); o_hi = nmax(o_hi, y[u]); }
+      }
+      continue;
+    }
 #pragma unroll
     for (int o = 0; o < PMX_MAX_OUTS; ++o) {
       if (o >= outs.n) break;
