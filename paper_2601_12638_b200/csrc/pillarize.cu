@@ -312,6 +312,49 @@ __global__ void __launch_bounds__(256) select_small_kernel(int64_t nmax, const p
   }
 }
 
+// M == 32 variant: lane = pillar builds its 128-byte row in shared memory (16-byte
+// chunks XOR-swizzled by lane % 8: conflict-free), then the warp writes 4 whole rows
+// per store instruction (a thread-per-row store scatters over 32 lines).
+__global__ void __launch_bounds__(256) select_small32_kernel(int64_t nmax, const pmx_grid g, PillarWs w,
+                                                             int32_t pcap, const int32_t* __restrict__ n_pillars,
+                                                             int32_t* pt_idx) {
+  __shared__ int4 rows[8][32][8];  // [warp][pillar][16-byte chunk]
+  const int b = blockIdx.y;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int p0 = (blockIdx.x * 8 + wid) * 32;
+  const int P = n_pillars[b];
+  if (p0 >= P) return;  // warp-uniform
+  const int p = p0 + lane;
+  bool mine = p < P;
+  const int64_t q = (int64_t)b * pcap + p;
+  const int c = mine ? w.fill[q] : 0;
+  if (mine && c > 32) {  // dense cluster: the warp-per-pillar kernel writes this row
+    w.ovf[atomicAdd(w.ovf_n, 1)] = make_int2(b, p);
+    mine = false;
+  }
+  const int sw = lane & 7;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) rows[wid][lane][k ^ sw] = make_int4(-1, -1, -1, -1);
+  if (mine) {
+    const int* seg = w.csr + b * nmax + w.segoff[q];
+    int* r32 = reinterpret_cast<int*>(rows[wid][lane]);
+    for (int i = 0; i < c; ++i) {
+      const int v = seg[i];
+      int r = 0;
+      for (int j = 0; j < c; ++j) r += seg[j] < v;
+      r32[(((r >> 2) ^ sw) << 2) + (r & 3)] = v;  // r < c <= 32
+    }
+  }
+  const unsigned keep = __ballot_sync(0xffffffffu, mine);
+  __syncwarp();
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const int r = 4 * j + (lane >> 3), k = lane & 7;
+    if ((keep >> r) & 1)
+      reinterpret_cast<int4*>(pt_idx + ((int64_t)b * pcap + p0 + r) * 32)[k] = rows[wid][r][k ^ (r & 7)];
+  }
+}
+
 __global__ void __launch_bounds__(256) select_kernel(const int64_t* __restrict__ offs, int64_t nmax,
                                                      const pmx_grid g, PillarWs w, int32_t pcap,
                                                      const int32_t* __restrict__ n_pillars, int32_t* pt_idx) {
@@ -480,7 +523,12 @@ pmx_status pmx_pillarize(const float* points, const int64_t* frame_offsets, int3
   thresh_kernel<<<batch, 1024, 0, stream>>>(frame_offsets, nmax, g, w, nb);
   emit_fused_kernel<<<dim3(cb, batch), 1024, 0, stream>>>(g, w, cb, pcap, coords, counts, n_pillars);
   slot_kernel<<<dim3(ptx, batch), 256, 0, stream>>>(frame_offsets, nmax, g, w, pcap);
-  select_small_kernel<<<dim3((int)ceil_div(pcap, 256), batch), 256, 0, stream>>>(nmax, g, w, pcap, n_pillars, pt_idx);
+  if (g.max_points == 32)
+    select_small32_kernel<<<dim3((int)ceil_div(pcap, 256), batch), 256, 0, stream>>>(nmax, g, w, pcap, n_pillars,
+                                                                                      pt_idx);
+  else
+    select_small_kernel<<<dim3((int)ceil_div(pcap, 256), batch), 256, 0, stream>>>(nmax, g, w, pcap, n_pillars,
+                                                                                    pt_idx);
   // overflow pillars (> 32 points): one warp each, grid-stride over the device-side list
   select_kernel<<<kNumSMs, 256, 0, stream>>>(frame_offsets, nmax, g, w, pcap, n_pillars, pt_idx);
   return check_launch("pmx_pillarize");
