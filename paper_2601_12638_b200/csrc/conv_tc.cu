@@ -219,6 +219,10 @@ struct TcParams {
   int nacc;        // TMEM accumulator buffers (power of two; MMA runs up to nacc tiles ahead)
   int nacc_shift;  // log2(nacc)
   int egroups;     // epilogue tile slots (1, 2 or 4)
+  // stride-1 HALO with a swizzled pixel-major halo (16 x 18 pixels, one TMA box
+  // whose inner dimension is a whole pixel: 288 requests instead of 180 * groups)
+  int hswz;
+  int hswz_bo;  // descriptor base-offset rule (experiment): 0 none, 1 (addr>>7)&7, 2 (addr>>7)&3
   // warp-transposed int8 stores (single int8 consumer): each epilogue warp stages its
   // 4 chunks (32 rows x 64 B) in shared memory and every store instruction then
   // writes 8 rows x 64 contiguous bytes (thread-per-row 16-byte stores scatter over
@@ -653,7 +657,8 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
           mbar_expect_tx(full(s), p.halo_tx);
           const uint32_t slot = a_smem + s * p.a_bytes;
           if (p.stride == 1) {
-            tma_load_5d(slot, &maps.a[0], 0, ox0 - 1, oy0 - 1, 0, tb, full(s));
+            if (p.hswz) tma_load_4d(slot, &maps.a[0], 0, ox0 - 1, oy0 - 1, tb, full(s));
+            else tma_load_5d(slot, &maps.a[0], 0, ox0 - 1, oy0 - 1, 0, tb, full(s));
           } else {
             // four parity planes (py, px): (16 + py) x (8 + px) pixels from (oy0 - py, ox0 - px)
             uint32_t off = 0;
@@ -732,7 +737,35 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
         tc_fence_after();
         // GATHER: the stage was written through the generic proxy (st.shared, cp.async)
         if constexpr (GATHER) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        if (elect_one()) {
+        if (HS == 1 && p.hswz) {
+          if (elect_one()) {
+            // pixel-major halo rows of CINB bytes (SW128 / SW64, TMA-swizzled by address):
+            // tap (dy, dx) starts at halo pixel (dy + 1) * 16 + dx + 1; 8-row groups are
+            // 16 pixels = whole swizzle patterns apart; the start's pattern phase goes in
+            // the descriptor's base offset
+            const uint32_t sbase = a_smem + s * p.a_bytes;
+            constexpr uint32_t lay = CINB == 128 ? 2u : 4u;
+            const uint32_t hi0 = (uint32_t)(16 * CINB) >> 4 | (1u << 14) | (lay << 29);
+#pragma unroll
+            for (int tap = 0; tap < 9; ++tap) {
+              const int dy = tap / 3 - 1, dx = tap % 3 - 1;
+              const uint32_t st0 = sbase + (uint32_t)(((dy + 1) * 16 + dx + 1) * CINB);
+#pragma unroll
+              for (int k = 0; k < CINB / 32; ++k) {
+                const int kb = k * 32;
+                const uint32_t sa = st0 + kb;
+                const uint32_t bo = p.hswz_bo == 0 ? 0u : (p.hswz_bo == 1 ? ((st0 >> 7) & 7u) : ((st0 >> 7) & 3u));
+                const uint32_t hi = hi0 | (bo << 17);
+                const uint64_t ad = ((uint64_t)hi << 32) | ((1u << 16) | ((sa & 0x3FFFFu) >> 4));
+                const uint32_t boff = (uint32_t)((tap * CB + kb / KCB)) * bblk + (uint32_t)(kb % KCB);
+                const uint64_t bd = ((uint64_t)b_hi << 32) | (b_lo0 + (boff >> 4));
+                tc_mma<DT>(d, ad, bd, idesc, (tap | k) != 0);
+              }
+            }
+            tc_commit(empty(s));
+            tc_commit(tfull(acc));
+          }
+        } else if (elect_one()) {
           PMX_TRACE(3, i);
           const uint32_t alo = (a_smem + s * p.a_bytes) >> 4;
 #pragma unroll
@@ -1201,6 +1234,14 @@ struct Plan {
 
 // Can the tensor-core path run this layer?  (shape / alignment rules)
 // warp-transposed epilogue stores (PMX_ESTAGE=0 turns them off for A/B runs)
+bool halo_swz_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("PMX_HALO_SWZ");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 bool estage_enabled() {
   static const bool on = [] {
     const char* e = getenv("PMX_ESTAGE");
@@ -1321,7 +1362,15 @@ Plan plan_for(const pmx_conv_desc& d, bool gather = false, bool want_stage = fal
   if (conv3 && g_conv_backend_mode != 2 && cin_bytes == kc_bytes && p.n_tiles == 1 && d.out_w >= 8) {
     // stride 1: one (16 + 2) x (8 + 2) halo; stride 2: four parity planes of
     // (16 + py) x (8 + px) pixels (561 in total) -- see the producer
-    const uint32_t hw = 10, hp = p.stride == 1 ? 180u : 561u;
+    // stride 1, 64 / 128 channel bytes: swizzled pixel-major halo 16 x 18 (PMX_HALO_SWZ=0: off)
+    // (not for a 128-channel (int8, f16) pair: its larger halo would evict the f16 staging)
+    p.hswz = (p.stride == 1 && !gather && (cin_bytes == 64 || cin_bytes == 128) && halo_swz_enabled() &&
+              !(p.estage2 && cin_bytes == 128)) ? 1 : 0;
+    {
+      const char* e = getenv("PMX_HSWZ_BO");
+      p.hswz_bo = e ? atoi(e) : 0;  // measured: the swizzle follows the absolute address
+    }
+    const uint32_t hw = p.hswz ? 16 : 10, hp = p.stride == 1 ? (p.hswz ? 288u : 180u) : 561u;
     const uint32_t halo = hp * (uint32_t)cin_bytes;
     const uint32_t halo_al = (halo + 1023u) & ~1023u;
     const uint32_t bblk = (uint32_t)bn * kc_bytes;
@@ -1338,6 +1387,7 @@ Plan plan_for(const pmx_conv_desc& d, bool gather = false, bool want_stage = fal
     }
     if ((p.estage || p.estage2) && bres_total + two_stages > budget && bres_total + two_stages <= budget0) {
       p.estage = p.estage2 = 0;  // resident weights + two halo stages win over the store staging
+      estage_bytes = 0;
       budget = budget0;
     }
     if (bres_total + two_stages <= budget) {
@@ -1359,6 +1409,8 @@ Plan plan_for(const pmx_conv_desc& d, bool gather = false, bool want_stage = fal
       p.cin_bytes = (uint32_t)cin_bytes;
       p.bblk_bytes = bblk;
       p.bres_bytes = bres_total;
+    } else {
+      p.hswz = 0;
     }
   }
   p.tw_shift = p.tw > 0 ? __builtin_ctz((unsigned)p.tw) : 0;
@@ -1407,6 +1459,14 @@ pmx_status build_maps(const pmx_conv_desc& d, const Plan& pl, const void* x, con
       st = encode(&maps->a[q], dt, 5, basep, dims, str, box, CU_TENSOR_MAP_SWIZZLE_NONE);
       if (st != PMX_OK) return st;
     }
+  } else if (p.mode == MODE_HALO && p.hswz) {
+    // pixel-major swizzled halo: dims {channels, W, H, B}, box {channels, 16, 18, 1}
+    cuuint64_t dims[4] = {(cuuint64_t)d.in_c, (cuuint64_t)d.in_w, (cuuint64_t)d.in_h, (cuuint64_t)d.batch};
+    cuuint64_t str[3] = {cs, cs * d.in_w, cs * d.in_w * d.in_h};
+    cuuint32_t box[4] = {(cuuint32_t)d.in_c, p.hw, p.hp / p.hw, 1};
+    st = encode(&maps->a[0], dt, 4, xb, dims, str, box,
+                p.cin_bytes == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B);
+    if (st != PMX_OK) return st;
   } else if (p.mode == MODE_HALO) {
     // [channel group][halo pixel][16 bytes]: dims {16B of channels, W, H, channel groups, B}
     const cuuint32_t cpg = 16 / esz;
