@@ -745,11 +745,11 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
             // the descriptor's base offset
             const uint32_t sbase = a_smem + s * p.a_bytes;
             constexpr uint32_t lay = CINB == 128 ? 2u : 4u;
-            const uint32_t hi0 = (uint32_t)(16 * CINB) >> 4 | (1u << 14) | (lay << 29);
+            const uint32_t hi0 = (uint32_t)(p.hw * CINB) >> 4 | (1u << 14) | (lay << 29);
 #pragma unroll
             for (int tap = 0; tap < 9; ++tap) {
               const int dy = tap / 3 - 1, dx = tap % 3 - 1;
-              const uint32_t st0 = sbase + (uint32_t)(((dy + 1) * 16 + dx + 1) * CINB);
+              const uint32_t st0 = sbase + (uint32_t)(((dy + 1) * (int)p.hw + dx + 1) * CINB);
 #pragma unroll
               for (int k = 0; k < CINB / 32; ++k) {
                 const int kb = k * 32;
@@ -1242,6 +1242,14 @@ bool halo_swz_enabled() {
   return on;
 }
 
+uint32_t halo_swz_width() {  // PMX_HSWZ_W: swizzled halo row width in pixels (10 or 16)
+  static const uint32_t v = [] {
+    const char* e = getenv("PMX_HSWZ_W");
+    return (e && atoi(e) == 10) ? 10u : 16u;
+  }();
+  return v;
+}
+
 bool estage_enabled() {
   static const bool on = [] {
     const char* e = getenv("PMX_ESTAGE");
@@ -1370,7 +1378,8 @@ Plan plan_for(const pmx_conv_desc& d, bool gather = false, bool want_stage = fal
       const char* e = getenv("PMX_HSWZ_BO");
       p.hswz_bo = e ? atoi(e) : 0;  // measured: the swizzle follows the absolute address
     }
-    const uint32_t hw = p.hswz ? 16 : 10, hp = p.stride == 1 ? (p.hswz ? 288u : 180u) : 561u;
+    const uint32_t swz_w = halo_swz_width();
+    const uint32_t hw = p.hswz ? swz_w : 10, hp = p.stride == 1 ? (p.hswz ? 18u * swz_w : 180u) : 561u;
     const uint32_t halo = hp * (uint32_t)cin_bytes;
     const uint32_t halo_al = (halo + 1023u) & ~1023u;
     const uint32_t bblk = (uint32_t)bn * kc_bytes;
