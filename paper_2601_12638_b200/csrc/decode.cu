@@ -67,6 +67,7 @@ __device__ __forceinline__ bool last_arrival(int* ctr, int n_ctas) {
 __global__ void __launch_bounds__(kThreads) topk_hist(const float* __restrict__ heads, int c_stride, int cls_off,
                                                       int n_anchors, int64_t ncand, int k, int* hist, int* arrive,
                                                       uint32_t* thresh) {
+  pdl_begin();
   __shared__ int h[kBins];
   __shared__ int sh[32];
   const int b = blockIdx.y;
@@ -161,6 +162,7 @@ __global__ void __launch_bounds__(kThreads) topk_select(
     const pmx_anchor_desc d, const float* __restrict__ heads, int c_stride, int cls_off, int box_off, int dir_off,
     int out_h, int out_w, const uint32_t* __restrict__ thresh, unsigned long long* cand, int* cnt, int* arrive,
     int32_t* topk_idx, float* topk_logit, float* boxes, int32_t* dir_label) {
+  pdl_begin();
   __shared__ unsigned long long s[kCap];
   __shared__ int sh_hist[256];
   __shared__ int sh_n, sh_sel[2];
@@ -302,11 +304,11 @@ pmx_status pmx_decode_topk(const pmx_anchor_desc* desc, int32_t batch, int32_t o
   PMX_REQUIRE(ws && ws_bytes >= w.bytes, "decode workspace too small");
   PMX_CUDA(cudaMemsetAsync(w.hist, 0, w.zero_bytes, stream));
   const int nch = (int)ceil_div(ncand, kChunk);
-  topk_hist<<<dim3(nch, batch), kThreads, 0, stream>>>(heads, head_c_stride, cls_off, d.n_anchors, ncand, d.k,
-                                                        w.hist, w.arrive, w.thresh);
-  topk_select<<<dim3(nch, batch), kThreads, 0, stream>>>(d, heads, head_c_stride, cls_off, box_off, dir_off, out_h,
-                                                          out_w, w.thresh, w.cand, w.cnt, w.arrive + batch, topk_idx,
-                                                          topk_logit, boxes, dir_label);
+  PMX_CUDA(launch_pdl(topk_hist, dim3(nch, batch), dim3(kThreads), 0, stream, heads, head_c_stride, cls_off,
+                      d.n_anchors, ncand, d.k, w.hist, w.arrive, w.thresh));
+  PMX_CUDA(launch_pdl(topk_select, dim3(nch, batch), dim3(kThreads), 0, stream, d, heads, head_c_stride, cls_off,
+                      box_off, dir_off, out_h, out_w, (const uint32_t*)w.thresh, w.cand, w.cnt, w.arrive + batch,
+                      topk_idx, topk_logit, boxes, dir_label));
   return check_launch("pmx_decode_topk");
 }
 

@@ -261,6 +261,7 @@ __device__ __forceinline__ void store2(const OutDev& o, int64_t pix, int c, floa
 
 template <int DT>
 __global__ void __launch_bounds__(kThreads, 2) pfn_points_kernel(const PfnArgs a, const Outs outs) {
+  pdl_begin();
   using R = Rec<DT>;
   using T = typename R::T;
   extern __shared__ __align__(16) uint8_t pfn_smem[];
@@ -501,7 +502,7 @@ pmx_status launch_dt(const PfnArgs& a, const Outs& outs, dim3 grid, cudaStream_t
     const dim3 g2((unsigned)ceil_div(a.pcap, kThreads), grid.y);  // 32 pillars per warp
     const size_t sm = pfn_points_smem<DT>();
     PMX_CUDA(cudaFuncSetAttribute(pfn_points_kernel<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    pfn_points_kernel<DT><<<g2, kThreads, sm, st>>>(a, outs);
+    PMX_CUDA(launch_pdl(pfn_points_kernel<DT>, g2, dim3(kThreads), sm, st, a, outs));
   } else {
     switch (a.d.n_features) {
 #define PMX_F_CASE(N) \

@@ -89,6 +89,7 @@ __device__ __forceinline__ int bin_cell(float x, float y, const pmx_grid g) {
 
 __global__ void bin_kernel(const float4* __restrict__ pts, const int64_t* __restrict__ offs, int64_t nmax,
                            const pmx_grid g, PillarWs w) {
+  pdl_begin();
   const int b = blockIdx.y;
   const int64_t base = offs[b];
   const int64_t n = offs[b + 1] - base;
@@ -104,6 +105,7 @@ __global__ void bin_kernel(const float4* __restrict__ pts, const int64_t* __rest
 
 __global__ void __launch_bounds__(kPtBlock) flag_kernel(const int64_t* __restrict__ offs, int64_t nmax,
                                                         const pmx_grid g, PillarWs w, int nb) {
+  pdl_begin();
   const int b = blockIdx.y;
   const int64_t n = offs[b + 1] - offs[b];
   const int64_t hw = (int64_t)g.grid_h * g.grid_w;
@@ -139,6 +141,7 @@ __device__ int block_incl_scan(int v, int* sh /*32*/) {
 
 __global__ void __launch_bounds__(1024) thresh_kernel(const int64_t* __restrict__ offs, int64_t nmax,
                                                       const pmx_grid g, PillarWs w, int nb) {
+  pdl_begin();
   __shared__ int sh[32];
   __shared__ int s_blk, s_need;
   const int b = blockIdx.x;
@@ -188,6 +191,7 @@ constexpr unsigned long long kLookPtsMask = (1ull << 40) - 1, kLookKeptMask = (1
 
 __global__ void __launch_bounds__(1024) emit_fused_kernel(const pmx_grid g, PillarWs w, int cb, int32_t pcap,
                                                           int32_t* coords, int32_t* counts, int32_t* n_pillars) {
+  pdl_begin();
   __shared__ int sh[32];
   __shared__ int s_blk;
   __shared__ unsigned long long s_prefix;
@@ -269,6 +273,7 @@ __global__ void __launch_bounds__(1024) emit_fused_kernel(const pmx_grid g, Pill
 
 __global__ void slot_kernel(const int64_t* __restrict__ offs, int64_t nmax, const pmx_grid g, PillarWs w,
                             int32_t pcap) {
+  pdl_begin();
   const int b = blockIdx.y;
   const int64_t n = offs[b + 1] - offs[b];
   const int64_t hw = (int64_t)g.grid_h * g.grid_w;
@@ -287,6 +292,7 @@ __global__ void slot_kernel(const int64_t* __restrict__ offs, int64_t nmax, cons
 // go to an overflow list handled warp-wide by select_kernel below.
 __global__ void __launch_bounds__(256) select_small_kernel(int64_t nmax, const pmx_grid g, PillarWs w, int32_t pcap,
                                                            const int32_t* __restrict__ n_pillars, int32_t* pt_idx) {
+  pdl_begin();
   const int b = blockIdx.y;
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n_pillars[b]) return;
@@ -318,6 +324,7 @@ __global__ void __launch_bounds__(256) select_small_kernel(int64_t nmax, const p
 __global__ void __launch_bounds__(256) select_small32_kernel(int64_t nmax, const pmx_grid g, PillarWs w,
                                                              int32_t pcap, const int32_t* __restrict__ n_pillars,
                                                              int32_t* pt_idx) {
+  pdl_begin();
   __shared__ int4 rows[8][32][8];  // [warp][pillar][16-byte chunk]
   const int b = blockIdx.y;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -358,6 +365,7 @@ __global__ void __launch_bounds__(256) select_small32_kernel(int64_t nmax, const
 __global__ void __launch_bounds__(256) select_kernel(const int64_t* __restrict__ offs, int64_t nmax,
                                                      const pmx_grid g, PillarWs w, int32_t pcap,
                                                      const int32_t* __restrict__ n_pillars, int32_t* pt_idx) {
+  pdl_begin();
   __shared__ int buf[8][32];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int n_items = *w.ovf_n;
@@ -518,19 +526,22 @@ pmx_status pmx_pillarize(const float* points, const int64_t* frame_offsets, int3
   PMX_CUDA(cudaMemsetAsync(w.look, 0, sizeof(unsigned long long) * batch * cb, stream));
   PMX_CUDA(cudaMemsetAsync(w.ticket, 0, sizeof(int32_t) * batch, stream));
   const int ptx = (int)std::min<int64_t>(ceil_div(nmax, 256), 4096);
-  bin_kernel<<<dim3(ptx, batch), 256, 0, stream>>>(reinterpret_cast<const float4*>(points), frame_offsets, nmax, g, w);
-  flag_kernel<<<dim3(nb, batch), kPtBlock, 0, stream>>>(frame_offsets, nmax, g, w, nb);
-  thresh_kernel<<<batch, 1024, 0, stream>>>(frame_offsets, nmax, g, w, nb);
-  emit_fused_kernel<<<dim3(cb, batch), 1024, 0, stream>>>(g, w, cb, pcap, coords, counts, n_pillars);
-  slot_kernel<<<dim3(ptx, batch), 256, 0, stream>>>(frame_offsets, nmax, g, w, pcap);
+  PMX_CUDA(launch_pdl(bin_kernel, dim3(ptx, batch), dim3(256), 0, stream, reinterpret_cast<const float4*>(points),
+                      frame_offsets, nmax, g, w));
+  PMX_CUDA(launch_pdl(flag_kernel, dim3(nb, batch), dim3(kPtBlock), 0, stream, frame_offsets, nmax, g, w, nb));
+  PMX_CUDA(launch_pdl(thresh_kernel, dim3(batch), dim3(1024), 0, stream, frame_offsets, nmax, g, w, nb));
+  PMX_CUDA(launch_pdl(emit_fused_kernel, dim3(cb, batch), dim3(1024), 0, stream, g, w, cb, pcap, coords, counts,
+                      n_pillars));
+  PMX_CUDA(launch_pdl(slot_kernel, dim3(ptx, batch), dim3(256), 0, stream, frame_offsets, nmax, g, w, pcap));
   if (g.max_points == 32)
-    select_small32_kernel<<<dim3((int)ceil_div(pcap, 256), batch), 256, 0, stream>>>(nmax, g, w, pcap, n_pillars,
-                                                                                      pt_idx);
+    PMX_CUDA(launch_pdl(select_small32_kernel, dim3((int)ceil_div(pcap, 256), batch), dim3(256), 0, stream, nmax, g,
+                        w, pcap, n_pillars, pt_idx));
   else
-    select_small_kernel<<<dim3((int)ceil_div(pcap, 256), batch), 256, 0, stream>>>(nmax, g, w, pcap, n_pillars,
-                                                                                    pt_idx);
+    PMX_CUDA(launch_pdl(select_small_kernel, dim3((int)ceil_div(pcap, 256), batch), dim3(256), 0, stream, nmax, g,
+                        w, pcap, n_pillars, pt_idx));
   // overflow pillars (> 32 points): one warp each, grid-stride over the device-side list
-  select_kernel<<<kNumSMs, 256, 0, stream>>>(frame_offsets, nmax, g, w, pcap, n_pillars, pt_idx);
+  PMX_CUDA(launch_pdl(select_kernel, dim3(kNumSMs), dim3(256), 0, stream, frame_offsets, nmax, g, w, pcap, n_pillars,
+                      pt_idx));
   return check_launch("pmx_pillarize");
 }
 

@@ -8,6 +8,7 @@
 
 #include <cstdio>
 #include <string>
+#include <utility>
 
 #include "pmx.h"
 
@@ -35,6 +36,34 @@ pmx_status check_launch(const char* what);
 inline int elem_size(int dtype) { return dtype == PMX_F32 ? 4 : (dtype == PMX_F16 ? 2 : 1); }
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 constexpr int kNumSMs = 148;
+
+// ---------------------------------------------------------------------------
+// programmatic dependent launch: kernels are launched with programmatic stream
+// serialization and start with pdl_begin() -- wait for the predecessor grid (its
+// writes visible), then let the successor grid start launching.  The successor's
+// launch and block scheduling overlap this kernel; no memory is touched before the
+// wait, so the ordering is the plain stream order.  (A no-op without the attribute.)
+
+__device__ __forceinline__ void pdl_begin() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 // ---------------------------------------------------------------------------
 // exact quantize: clip(rint(f64(x) / scale), -128, 127)   (pm/quant.py:98-103)
