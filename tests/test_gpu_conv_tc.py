@@ -33,7 +33,7 @@ CASES = [  # kind, cin, cout, k, stride, (h, w), batch
 ]
 
 
-def _run(lib, N, torch, desc, x, w, alpha, bias, outs_spec, mode):
+def _run(lib, N, torch, desc, x, w, alpha, bias, outs_spec, mode, observe=True):
     outs = []
     bufs = []
     for dt, scale in outs_spec:
@@ -48,7 +48,8 @@ def _run(lib, N, torch, desc, x, w, alpha, bias, outs_spec, mode):
     N.check(lib.pmx_minmax_init(keys.data_ptr(), 1, N.stream_ptr()))
     try:
         N.check(lib.pmx_conv(ctypes.byref(desc), x.data_ptr(), w.data_ptr(), None if alpha is None else alpha.data_ptr(),
-                             bias.data_ptr(), None, arr, n, keys.data_ptr(), None, 0, N.stream_ptr()), "conv")
+                             bias.data_ptr(), None, arr, n, keys.data_ptr() if observe else None, None, 0,
+                             N.stream_ptr()), "conv")
         torch.cuda.synchronize()
     finally:
         lib.pmx_set_conv_backend(0)
@@ -154,3 +155,41 @@ def test_tcgen05_single_int8_consumer(case, relu):
         assert int(c.min()) == 0
     else:
         assert int(c.min()) < 0
+
+
+PAIR_CASES = [  # the (int8, f16) consumer pair of a block's last conv: staged f16 stores
+    ("conv", 64, 64, 3, 1, (20, 18), 2),      # blocks.0.9 shape class (4 KB/warp staging)
+    ("conv", 64, 64, 3, 1, (248, 216), 1),    # blocks.0.9 full size
+    ("conv", 128, 128, 3, 1, (21, 13), 2),    # blocks.1.15 (1 KB/warp staging next to the halo)
+    ("conv", 128, 128, 3, 1, (124, 108), 1),  # blocks.1.15 full size
+    ("conv", 256, 256, 3, 1, (7, 9), 1),      # blocks.2.x class
+]
+
+
+@pytest.mark.parametrize("case", PAIR_CASES, ids=lambda c: f"{c[0]}{c[1]}x{c[2]}k{c[3]}s{c[4]}_{c[5][0]}x{c[5][1]}")
+@pytest.mark.parametrize("order", ["i8f16", "f16i8"])
+def test_tcgen05_int8_f16_pair(case, order):
+    """Two consumers (int8 codes + binary16), no observer: the staged-store epilogue
+    (and its small-staging mode) vs the SIMT kernel, bit for bit (int8 arithmetic)."""
+    import torch
+
+    from paper_2601_12638_b200 import _native as N
+
+    lib = N.load()
+    kind, cin, cout, k, s, (h, w), batch = case
+    rng = np.random.default_rng(cin * 5 + cout + h)
+    oh, ow = (h + 2 - k) // s + 1, (w + 2 - k) // s + 1
+    desc = N.ConvDesc(kind=N.PMX_CONV2D, in_dtype=N.PMX_I8, batch=batch, in_h=h, in_w=w, in_c=cin, in_c_stride=cin,
+                      in_c_offset=0, out_c=cout, k_h=k, k_w=k, stride_h=s, stride_w=s, pad_h=1, pad_w=1, out_h=oh,
+                      out_w=ow, relu=1)
+    x = torch.from_numpy(rng.integers(-128, 128, size=(batch, h, w, cin), dtype=np.int8)).cuda()
+    wt = torch.from_numpy(rng.integers(-128, 128, size=(cout, k * k * cin), dtype=np.int8)).cuda()
+    alpha = torch.from_numpy((rng.uniform(0.5, 2.0, cout) * 1e-4).astype(np.float32)).cuda()
+    bias = torch.from_numpy(rng.normal(scale=0.1, size=cout).astype(np.float32)).cuda()
+    spec = [(N.PMX_I8, 0.013), (N.PMX_F16, 0.0)]
+    if order == "f16i8":
+        spec = spec[::-1]
+    tc, _ = _run(lib, N, torch, desc, x, wt, alpha, bias, spec, 0, observe=False)
+    ref, _ = _run(lib, N, torch, desc, x, wt, alpha, bias, spec, 1, observe=False)
+    for a, b in zip(tc, ref):
+        assert torch.equal(a, b), (a.float() - b.float()).abs().max()
