@@ -236,12 +236,12 @@ def main():
     # i's graph, batch i's records come back D2H; every step pays its own copies
     pipe = pm.PipelinedEngine(eng)
     host_recs = [torch.empty(rec_dev.shape, dtype=rec_dev.dtype).pin_memory() for _ in range(2)]
-    pipe.run([(host_pts, host_offs)] * args.warmup, [host_recs[i % 2] for i in range(args.warmup)], D.pack_topk)
+    pipe.run([(host_pts, host_offs)] * args.warmup, [host_recs[i % 2] for i in range(args.warmup)])
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
     start.record()
-    pipe.run([(host_pts, host_offs)] * args.steps, [host_recs[i % 2] for i in range(args.steps)], D.pack_topk)
+    pipe.run([(host_pts, host_offs)] * args.steps, [host_recs[i % 2] for i in range(args.steps)])
     end.record()
     torch.cuda.synchronize()
     e2e_ms = D.max_over_ranks(start.elapsed_time(end) / args.steps, device=dev)

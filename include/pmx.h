@@ -297,6 +297,14 @@ pmx_status pmx_decode_topk(const pmx_anchor_desc* desc, int32_t batch, int32_t o
                            float* topk_logit, float* boxes, int32_t* dir_label, void* ws,
                            size_t ws_bytes, pmx_stream_t stream);
 
+/* Fixed-size per-frame top-k records for the host / the NCCL gather:
+ * records [B, k, 10] f32 = (idx, logit, box[7], dir) with idx and dir as f32
+ * (exact below 2^24).  Same layout as paper_2601_12638_b200.distributed.pack_topk;
+ * one kernel inside the captured graph instead of four torch ops after it. */
+pmx_status pmx_pack_topk_records(int32_t batch, int32_t k, const int32_t* topk_idx,
+                                 const float* topk_logit, const float* boxes,
+                                 const int32_t* dir_label, float* records, pmx_stream_t stream);
+
 /* ------------------------------------------------------------------------
  * K12 sensitivity-sweep error (BASELINE config 5; SPEC.md:364-372 sweep with the
  * head-output error as the score): out2[0] += sum((a - b)^2), out2[1] += sum(b^2)

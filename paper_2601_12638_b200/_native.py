@@ -91,6 +91,7 @@ SIGNATURES = {
     "pmx_decode_workspace": (SZ, [C.POINTER(AnchorDesc), I32, I32, I32]),
     "pmx_decode_topk": (I32, [C.POINTER(AnchorDesc), I32, I32, I32, P, I32, I32, I32, I32, P, P, P, P, P, SZ,
                               P]),
+    "pmx_pack_topk_records": (I32, [I32, I32, P, P, P, P, P, P]),
     "pmx_zero": (I32, [P, SZ, P]),
     "pmx_sq_err": (I32, [P, P, I64, P, P, P]),
 }

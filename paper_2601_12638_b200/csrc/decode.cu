@@ -243,6 +243,19 @@ __global__ void __launch_bounds__(kThreads) topk_select(
                dir_label);
 }
 
+__global__ void pack_records_kernel(int n, const int32_t* __restrict__ idx, const float* __restrict__ logit,
+                                    const float* __restrict__ boxes, const int32_t* __restrict__ dir, float* rec) {
+  pdl_begin();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  float* r = rec + (int64_t)i * 10;
+  r[0] = (float)idx[i];
+  r[1] = logit[i];
+#pragma unroll
+  for (int j = 0; j < 7; ++j) r[2 + j] = boxes[(int64_t)i * 7 + j];
+  r[9] = (float)dir[i];
+}
+
 struct DecodeWs {
   unsigned long long* cand;
   int* hist;     // [B, kBins]
@@ -310,6 +323,17 @@ pmx_status pmx_decode_topk(const pmx_anchor_desc* desc, int32_t batch, int32_t o
                       box_off, dir_off, out_h, out_w, (const uint32_t*)w.thresh, w.cand, w.cnt, w.arrive + batch,
                       topk_idx, topk_logit, boxes, dir_label));
   return check_launch("pmx_decode_topk");
+}
+
+pmx_status pmx_pack_topk_records(int32_t batch, int32_t k, const int32_t* topk_idx, const float* topk_logit,
+                                 const float* boxes, const int32_t* dir_label, float* records, pmx_stream_t stream) {
+  PMX_REQUIRE(batch >= 0 && k >= 0, "negative extent");
+  PMX_REQUIRE((topk_idx && topk_logit && boxes && dir_label && records) || batch * k == 0, "NULL operand");
+  const int n = batch * k;
+  if (n == 0) return PMX_OK;
+  PMX_CUDA(launch_pdl(pack_records_kernel, dim3((unsigned)ceil_div(n, 256)), dim3(256), 0, stream, n, topk_idx,
+                      topk_logit, boxes, dir_label, records));
+  return check_launch("pmx_pack_topk_records");
 }
 
 }  // extern "C"

@@ -426,6 +426,8 @@ class CompiledGraph:
             self.topk_logit = torch.empty((B, a.k), dtype=torch.float32, device="cuda")
             self.topk_boxes = torch.empty((B, a.k, 7), dtype=torch.float32, device="cuda")
             self.topk_dir = torch.empty((B, a.k), dtype=torch.int32, device="cuda")
+            # fixed-size records [B, k, 10] (distributed.pack_topk layout), written in the graph
+            self.records = torch.empty((B, a.k, 10), dtype=torch.float32, device="cuda")
 
     # ---------------- weights (one-time prep on the device)
 
@@ -702,6 +704,10 @@ class CompiledGraph:
             ctypes.byref(d), B, H, W, self.heads_cat.data_ptr(), ctot, 0, A, 8 * A, self.topk_idx.data_ptr(),
             self.topk_logit.data_ptr(), self.topk_boxes.data_ptr(), self.topk_dir.data_ptr(), ws.data_ptr(),
             ws_bytes, s), "decode_topk")))
+        # self.records is looked up at launch time (PipelinedEngine captures one buffer per slot)
+        self.ops.append(("records", lambda s: N.check(lib.pmx_pack_topk_records(
+            B, a.k, self.topk_idx.data_ptr(), self.topk_logit.data_ptr(), self.topk_boxes.data_ptr(),
+            self.topk_dir.data_ptr(), self.records.data_ptr(), s), "pack_topk_records")))
 
     # ---------------- execution
 
@@ -763,7 +769,7 @@ class CompiledGraph:
         n = 0
         for name, _ in self.ops:
             if name == "pillarize":
-                n += 9  # bin, flag, thresh, cellcount, cellscan, emit, slot, select_small, select
+                n += 7  # bin, flag, thresh, emit (single pass), slot, select_small, select
             elif name == "decode":
                 n += 2  # topk_hist (+ threshold), topk_select (+ sort, decode)
             else:

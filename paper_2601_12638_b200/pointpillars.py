@@ -258,13 +258,20 @@ class PipelinedEngine:
 
         self.eng = eng
         cg = eng.cg
-        # slot 1 starts as a copy of slot 0: capture() warms up on whatever the slot holds
-        self.slots = [(cg.points, cg.offsets), (cg.points.clone(), cg.offsets.clone())]
+        # slot 1 starts as a copy of slot 0: capture() warms up on whatever the slot holds;
+        # each slot's graph also writes its own top-k records buffer (read back D2H)
+        rec0 = getattr(cg, "records", None)
+        self.slots = [(cg.points, cg.offsets, rec0),
+                      (cg.points.clone(), cg.offsets.clone(), None if rec0 is None else rec0.clone())]
         self.graphs = []
-        for pts, offs in self.slots:
+        for pts, offs, rec in self.slots:
             cg.points, cg.offsets = pts, offs
+            if rec is not None:
+                cg.records = rec
             self.graphs.append(cg.capture())
-        cg.points, cg.offsets = self.slots[0]
+        cg.points, cg.offsets = self.slots[0][:2]
+        if rec0 is not None:
+            cg.records = rec0
         cg.graph_exec = self.graphs[0]
         self.h2d = torch.cuda.Stream()
         self.d2h = torch.cuda.Stream()
@@ -277,7 +284,7 @@ class PipelinedEngine:
         import torch
 
         slot = i % 2
-        pts, offs = self.slots[slot]
+        pts, offs, _ = self.slots[slot]
         with torch.cuda.stream(self.h2d):
             if i >= 2:
                 self.h2d.wait_event(self.done[slot])  # batch i-2 finished reading this slot
@@ -285,9 +292,10 @@ class PipelinedEngine:
             offs.copy_(host_offsets, non_blocking=True)
             self.copied[slot].record(self.h2d)
 
-    def run(self, batches, host_out, pack):
+    def run(self, batches, host_out, pack=None):
         """batches: list of (pinned points [N, 4] f32, pinned offsets [B + 1] i64);
-        host_out: list of pinned tensors receiving pack(topk) per batch (same length)."""
+        host_out: list of pinned tensors receiving each batch's top-k records [B, k, 10]
+        (written inside the graph), or pack(topk) when a pack function is given."""
         import torch
 
         comp = torch.cuda.current_stream()
@@ -301,7 +309,7 @@ class PipelinedEngine:
                 self._upload(i + 1, *batches[i + 1])
             comp.wait_event(self.copied[slot])
             self.graphs[slot].replay()
-            rec = pack(self.eng.topk())
+            rec = pack(self.eng.topk()) if pack is not None else self.slots[slot][2]
             self.done[slot].record(comp)
             with torch.cuda.stream(self.d2h):
                 self.d2h.wait_event(self.done[slot])

@@ -288,6 +288,8 @@ def test_pipelined_engine_matches_sequential(pm):
         e.load_points(fr)
         e.run()
         want.append(D.pack_topk(e.topk()).cpu())
+        # the in-graph records op (pmx_pack_topk_records) == the torch packing, bit for bit
+        assert torch.equal(e.cg.records.cpu(), want[-1])
     eng = pm.PointPillarsEngine(graph, pm.MIXED_PLAN_LABEL, stats, cfg, batch=2, max_points_per_frame=5000)
     eng.load_points(batches_np[0])
     pipe = pm.PipelinedEngine(eng)
@@ -300,4 +302,10 @@ def test_pipelined_engine_matches_sequential(pm):
     pipe.run(batches, outs, D.pack_topk)
     torch.cuda.synchronize()
     for o, w in zip(outs, want):
+        assert torch.equal(o, w)
+    # default: the records each slot's graph wrote, read back without extra kernels
+    outs2 = [torch.empty_like(w).pin_memory() for w in want]
+    pipe.run(batches, outs2)
+    torch.cuda.synchronize()
+    for o, w in zip(outs2, want):
         assert torch.equal(o, w)
