@@ -528,18 +528,25 @@ __device__ __forceinline__ void gather_producer(const TcParams& p, uint32_t a_sm
   if (blockIdx.x < total) load_map(blockIdx.x, mcur);
   if (blockIdx.x + (int)gridDim.x < total) load_map(blockIdx.x + gridDim.x, mnext);
   uint32_t s = 0, ph = 0;
+  int it = 0;  // trace index
+  (void)it;
   for (int t = blockIdx.x; t < total; t += gridDim.x) {
     const int tb = (int)fdiv(fdiv((uint32_t)t, p.fd_tx), p.fd_ty);
     const char* fb = feats + (int64_t)tb * p.g_pcap * p.g_row_bytes;
+    if (gt == 0) PMX_TRACE(0, it);
     mbar_wait(empty(s), ph ^ 1);
+    if (gt == 0) PMX_TRACE(10, it);
     const uint32_t slot = a_smem + s * p.a_bytes;
     const uint32_t old = (uint32_t)(clr >> (kPixPerThr * s)) & ((1u << kPixPerThr) - 1);
     uint32_t now = 0;
 #pragma unroll
     for (int j = 0; j < kPixPerThr; ++j) {
-      if ((old >> j) & 1)
+      // a pixel the stage's previous tile filled and this one leaves empty: zero it
+      // (st.shared: no L1TEX request; occupied pixels are overwritten by the copies)
+      if (((old >> j) & 1) && mcur[j] == 0)
         for (int g = 0; g < G; ++g)
-          cp_async_zero16(slot + dst0[j] + g * gstep[j], feats);
+          asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(slot + dst0[j] + g * gstep[j]), "r"(0)
+                       : "memory");
       if (mcur[j] != 0) {
         // occupied pixel: its feature row (G x 16 bytes) straight into the stage
         const char* src = fb + (int64_t)(mcur[j] - 1) * p.g_row_bytes;
@@ -551,8 +558,12 @@ __device__ __forceinline__ void gather_producer(const TcParams& p, uint32_t a_sm
       }
     }
     clr = (clr & ~((uint64_t)((1u << kPixPerThr) - 1) << (kPixPerThr * s))) | ((uint64_t)now << (kPixPerThr * s));
-    // the stage's full barrier counts this thread once its copies have landed
+    // two arrivals per thread on the stage's full barrier: a release arrive ordering its
+    // zero fills, the cp.async arrive once its copies have landed
+    mbar_arrive(full(s));
     asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(full(s)) : "memory");
+    if (gt == 0) PMX_TRACE(1, it);
+    ++it;
 #pragma unroll
     for (int j = 0; j < kPixPerThr; ++j) mcur[j] = mnext[j];
     const int tn2 = t + 2 * (int)gridDim.x;
@@ -595,7 +606,7 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
   if (threadIdx.x == 0) {
     PMX_TRACE(8, 0);
     for (int s = 0; s < p.stages; ++s) {
-      mbar_init(full(s), GATHER ? 32 * kGatherWarps : 1);  // TMA: expect_tx; gather: one cp.async arrive per thread
+      mbar_init(full(s), GATHER ? 2 * 32 * kGatherWarps : 1);  // TMA: expect_tx; gather: 2 arrivals per thread
       mbar_init(empty(s), 1);
     }
     for (int a = 0; a < p.nacc; ++a) {

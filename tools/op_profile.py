@@ -73,10 +73,10 @@ def main():
             if not t[:8, i].any() and not t[9, i]:
                 break
             print(f"{i:4d} " + " ".join(f"{(t[e, i] - t0) if t[e, i] else -1:12d}" for e in (0, 1, 9, 2, 3, 4, 5, 6, 7)))
-        if t[10:14].any():
-            print("gather producer: iter_start, built, empty_ok, B1, stored, arrived")
+        if t[10].any():
+            print("gather producer (thread 0): iter_start, empty_ok, arrived")
             for i in range(32):
-                print(f"{i:4d} " + " ".join(f"{(t[e, i] - t0) if t[e, i] else -1:10d}" for e in (0, 10, 1, 11, 12, 13)))
+                print(f"{i:4d} " + " ".join(f"{(t[e, i] - t0) if t[e, i] else -1:10d}" for e in (0, 10, 1)))
         return
     torch.cuda.profiler.start()
     fn(N.stream_ptr())
