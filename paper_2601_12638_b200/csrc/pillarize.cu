@@ -229,26 +229,32 @@ __global__ void __launch_bounds__(1024) emit_fused_kernel(const pmx_grid g, Pill
   const int pts_tot = sh[31];
   a -= kept;
   p -= pts;
-  if (threadIdx.x == 0) {
+  if (threadIdx.x < 32) {
+    // warp-wide decoupled look-back: 32 predecessors per round (nearest first in lane
+    // order); stop at the nearest one that already holds its inclusive prefix
+    const int lane = threadIdx.x;
     unsigned long long* look = w.look + (int64_t)b * cb;
     const unsigned long long agg = ((unsigned long long)kept_tot << 40) | (unsigned long long)pts_tot;
+    if (lane == 0) atomicExch(look + blk, (blk == 0 ? kLookInc : kLookAgg) | agg);
     unsigned long long excl = 0;
-    if (blk == 0) {
-      atomicExch(look + blk, kLookInc | agg);
-    } else {
-      atomicExch(look + blk, kLookAgg | agg);
-      for (int j = blk - 1; j >= 0; --j) {
-        unsigned long long v;
-        do {
-          v = atomicAdd(look + j, 0ull);  // L2-coherent read
-        } while ((v >> 62) == 0);
-        excl += v & ~(3ull << 62);
-        if ((v >> 62) == 2) break;
+    for (int j = blk - 1; j >= 0; j -= 32) {
+      const int jj = j - lane;
+      unsigned long long v = jj >= 0 ? atomicAdd(look + jj, 0ull) : kLookInc;  // before block 0: inclusive 0
+      while (__any_sync(0xffffffffu, (v >> 62) == 0)) {
+        if ((v >> 62) == 0) v = atomicAdd(look + jj, 0ull);
       }
-      atomicExch(look + blk, kLookInc | (excl + agg));
+      const unsigned incl = __ballot_sync(0xffffffffu, (v >> 62) == 2);
+      const int stop = incl ? __ffs(incl) - 1 : 31;
+      unsigned long long x = lane <= stop ? (v & ~(3ull << 62)) : 0ull;
+      for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+      excl += __shfl_sync(0xffffffffu, x, 0);
+      if (incl) break;
     }
-    s_prefix = excl;
-    if (blk == cb - 1) n_pillars[b] = (int)(((excl + agg) >> 40) & kLookKeptMask);
+    if (lane == 0) {
+      if (blk > 0) atomicExch(look + blk, kLookInc | (excl + agg));
+      s_prefix = excl;
+      if (blk == cb - 1) n_pillars[b] = (int)(((excl + agg) >> 40) & kLookKeptMask);
+    }
   }
   __syncthreads();
   a += (int)((s_prefix >> 40) & kLookKeptMask);
