@@ -72,6 +72,29 @@ size_t carve(const pmx_grid* g, int32_t B, int64_t nmax, int32_t pcap, void* bas
   return off;
 }
 
+// first = INT_MAX-ish (0x7f7f7f7f, as the memset it replaces), cnt = fill = 0,
+// look-back words, tickets and the overflow counter = 0
+__global__ void init_ws_kernel(PillarWs w, int64_t n_cells, int64_t n_fill, int64_t n_look, int batch) {
+  pdl_begin();
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nt = (int64_t)gridDim.x * blockDim.x;
+  const int4 f4 = make_int4(0x7f7f7f7f, 0x7f7f7f7f, 0x7f7f7f7f, 0x7f7f7f7f), z4 = make_int4(0, 0, 0, 0);
+  if ((n_cells & 3) == 0) {
+    for (int64_t i = tid; i < n_cells / 4; i += nt) {
+      reinterpret_cast<int4*>(w.first)[i] = f4;
+      reinterpret_cast<int4*>(w.cnt)[i] = z4;
+    }
+  } else {
+    for (int64_t i = tid; i < n_cells; i += nt) {
+      w.first[i] = 0x7f7f7f7f;
+      w.cnt[i] = 0;
+    }
+  }
+  for (int64_t i = tid; i < n_fill; i += nt) w.fill[i] = 0;
+  for (int64_t i = tid; i < n_look; i += nt) w.look[i] = 0ull;
+  for (int64_t i = tid; i < batch; i += nt) w.ticket[i] = 0;
+  if (tid == 0) *w.ovf_n = 0;
+}
+
 __device__ __forceinline__ int bin_cell(float x, float y, const pmx_grid g) {
   // pm/scenes.py:177-178: (f32(p) - origin) / cell in IEEE f32, astype(int64) truncates, clip
   float fy = __fdiv_rn(__fsub_rn(y, g.y_min), g.cell_h);
@@ -525,12 +548,13 @@ pmx_status pmx_pillarize(const float* points, const int64_t* frame_offsets, int3
   const int64_t nmax = max_points_per_frame > 0 ? max_points_per_frame : 1;
   const int nb = (int)ceil_div(nmax, kPtBlock);
   const int cb = (int)ceil_div(hw, kCellBlock);
-  PMX_CUDA(cudaMemsetAsync(w.first, 0x7f, sizeof(int32_t) * batch * hw, stream));
-  PMX_CUDA(cudaMemsetAsync(w.cnt, 0, sizeof(int32_t) * batch * hw, stream));
-  PMX_CUDA(cudaMemsetAsync(w.fill, 0, sizeof(int32_t) * batch * pcap, stream));
-  PMX_CUDA(cudaMemsetAsync(w.ovf_n, 0, sizeof(int32_t), stream));
-  PMX_CUDA(cudaMemsetAsync(w.look, 0, sizeof(unsigned long long) * batch * cb, stream));
-  PMX_CUDA(cudaMemsetAsync(w.ticket, 0, sizeof(int32_t) * batch, stream));
+  // one kernel initialises every per-call workspace array (six memset nodes before)
+  {
+    const int64_t n4 = batch * hw;  // first / cnt (int4 when hw % 4 == 0)
+    const int blocks = (int)std::min<int64_t>(ceil_div(n4, 256 * 4), 148 * 8);
+    PMX_CUDA(launch_pdl(init_ws_kernel, dim3(blocks), dim3(256), 0, stream, w, n4, (int64_t)batch * pcap,
+                        (int64_t)batch * cb, batch));
+  }
   const int ptx = (int)std::min<int64_t>(ceil_div(nmax, 256), 4096);
   PMX_CUDA(launch_pdl(bin_kernel, dim3(ptx, batch), dim3(256), 0, stream, reinterpret_cast<const float4*>(points),
                       frame_offsets, nmax, g, w));
