@@ -1,19 +1,25 @@
 // tcgen05 implicit-GEMM conv / deconv / 1x1 for sm_100a (K6, K7, K9, K10).
 //
 // Persistent (grid <= 148, one CTA per SM), warp-specialised, mbarrier-pipelined;
-// every role walks the same static tile sequence (tile = 128 output pixels x BN):
-//   warp 0 (1 thread)  TMA producer: per K-block, one box of the A operand (the
-//                      input shifted per 3x3 tap -- implicit im2col, padding by TMA
-//                      out-of-bounds zero fill) and one box of B (weights); in HALO
-//                      mode one halo box per tile and resident weights instead;
-//   warp 1 (1 thread)  TMEM allocator + MMA issuer: tcgen05.mma kind::i8 (s8 x s8 ->
-//                      s32) or kind::f16 (f16 x f16 -> f32) into one of two TMEM
-//                      accumulators; tcgen05.commit frees the stage / signals the
-//                      epilogue;
-//   warps 2-17         epilogue (4 per TMEM lane quarter): tcgen05.ld (thread =
-//                      output pixel row), scale + bias (+ unfolded BN) + ReLU, exact
-//                      requantisation to every consumer format, vectorised NHWC
-//                      stores (concat slices, deconv pixel shuffle).
+// every role walks the same static tile sequence (tile = 128 output pixels x BN).
+// The sub-partition scheduler favours high warp ids, so the single-thread roles
+// sit at the top:
+//   warps 0-15          epilogue (4 per TMEM lane quarter, warp & 3): tcgen05.ld
+//                       (thread = output pixel row), scale + bias (+ unfolded BN) +
+//                       ReLU, exact requantisation to every consumer format; NHWC
+//                       stores, staged through shared memory for wide int8 rows and
+//                       for the f16 half of an (int8, f16) consumer pair;
+//   warp 16 (1 thread)  TMA producer: per K-block, one box of the A operand (the
+//                       input shifted per 3x3 tap -- implicit im2col, padding by TMA
+//                       out-of-bounds zero fill) and one box of B (weights); in HALO
+//                       mode one halo box per tile (stride 1: a swizzled
+//                       pixel-major 16 x 18 halo) and resident weights instead;
+//                       GATHER (first conv): warps 16, 18, 19 fill the halo from
+//                       pillar rows with cp.async;
+//   warp 17 (1 thread)  TMEM allocator + MMA issuer: tcgen05.mma kind::i8 (s8 x s8 ->
+//                       s32) or kind::f16 (f16 x f16 -> f32) into 2-8 TMEM
+//                       accumulators; tcgen05.commit frees the stage / signals the
+//                       epilogue.
 // Stride-2 3x3 convs read the input through four parity-split tensor maps
 // (x[2i+p] -> map p at i), so every tap is a plain tiled box.  Launched with
 // programmatic dependent launch: the prologue overlaps the previous layer's tail.
