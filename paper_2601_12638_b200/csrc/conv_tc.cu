@@ -1095,20 +1095,24 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
                          : "memory");
           }
           __syncwarp();
-          if (live) {
+          {
+            // (converged: shuffles unconditional, one shuffle per row -- ~0 marks an
+            // invalid row; the output base is re-read from the parameter bank)
+            const uint32_t mp = (valid && live) ? mypix : 0xffffffffu;
+            int8_t* const obase = reinterpret_cast<int8_t*>(outs.o[0].ptr) + outs.o[0].c_offset + cob0;
+            const uint32_t ocs = (uint32_t)outs.o[0].c_stride;
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
               const int r = 8 * j + (lane >> 2);
               const uint32_t cc = (uint32_t)lane & 3u;
-              const uint32_t rp = __shfl_sync(0xffffffffu, mypix, r);
-              const int rv = __shfl_sync(0xffffffffu, (int)valid, r);
+              const uint32_t rp = __shfl_sync(0xffffffffu, mp, r);
               uint4 w;
               const uint32_t la = wstage + (uint32_t)r * 64u + ((cc ^ (((uint32_t)r >> 1) & 3u)) << 4);
               asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
                            : "=r"(w.x), "=r"(w.y), "=r"(w.z), "=r"(w.w)
                            : "r"(la)
                            : "memory");
-              if (rv) *reinterpret_cast<uint4*>(o_ptr + (size_t)rp * o_cs + cob0 + 16 * cc) = w;
+              if (rp != 0xffffffffu) *reinterpret_cast<uint4*>(obase + (size_t)rp * ocs + 16 * cc) = w;
             }
           }
           __syncwarp();
