@@ -984,19 +984,20 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
                 sts_f16(wstage + (uint32_t)lane * 32u + (sw << 4), wstage + (uint32_t)lane * 32u + ((1u ^ sw) << 4), y);
               }
               __syncwarp();
-              if (live) {
+              {
+                const uint32_t mp = (valid && live) ? pix_in : 0xffffffffu;
 #pragma unroll
                 for (int j = 0; j < 2; ++j) {
                   const int r = 16 * j + (lane >> 1);
                   const uint32_t sl = (uint32_t)lane & 1u;
-                  const uint32_t rp = __shfl_sync(0xffffffffu, pix_in, r);
-                  const int rv = __shfl_sync(0xffffffffu, (int)valid, r);
+                  const uint32_t rp = __shfl_sync(0xffffffffu, mp, r);
                   uint4 w;
                   asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
                                : "=r"(w.x), "=r"(w.y), "=r"(w.z), "=r"(w.w)
                                : "r"(wstage + (uint32_t)r * 32u + ((sl ^ (((uint32_t)r >> 2) & 1u)) << 4))
                                : "memory");
-                  if (rv) *reinterpret_cast<uint4*>(ph + (size_t)rp * csh + nbase0 + 16 * k + 8 * sl) = w;
+                  if (rp != 0xffffffffu)
+                    *reinterpret_cast<uint4*>(ph + (size_t)rp * csh + nbase0 + 16 * k + 8 * sl) = w;
                 }
               }
               __syncwarp();
@@ -1017,19 +1018,19 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
               sts_f16(rb + (((2u * k) ^ sw) << 4), rb + (((2u * k + 1u) ^ sw) << 4), y);
             }
             __syncwarp();
-            if (live) {
+            {
+              const uint32_t mp = (valid && live) ? pix_in : 0xffffffffu;
 #pragma unroll
               for (int j = 0; j < 8; ++j) {
                 const int r = 4 * j + (lane >> 3);
                 const uint32_t sl = (uint32_t)lane & 7u;
-                const uint32_t rp = __shfl_sync(0xffffffffu, pix_in, r);
-                const int rv = __shfl_sync(0xffffffffu, (int)valid, r);
+                const uint32_t rp = __shfl_sync(0xffffffffu, mp, r);
                 uint4 w;
                 asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
                              : "=r"(w.x), "=r"(w.y), "=r"(w.z), "=r"(w.w)
                              : "r"(wstage + (uint32_t)r * 128u + ((sl ^ ((uint32_t)r & 7u)) << 4))
                              : "memory");
-                if (rv) *reinterpret_cast<uint4*>(ph + (size_t)rp * csh + nbase0 + 8 * sl) = w;
+                if (rp != 0xffffffffu) *reinterpret_cast<uint4*>(ph + (size_t)rp * csh + nbase0 + 8 * sl) = w;
               }
             }
             __syncwarp();
