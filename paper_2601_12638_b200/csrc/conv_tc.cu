@@ -1187,7 +1187,9 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
 #if defined(PMX_ABLATE) && PMX_ABLATE == 2
             if ((code.x & code.y & code.z & code.w) == 0x7f7f7f7fu)
 #endif
-            *reinterpret_cast<uint4*>(o_ptr + (size_t)pix * o_cs + cobase) = code;
+            // (output base / stride from the parameter bank at the store: never spilled)
+            *reinterpret_cast<uint4*>(reinterpret_cast<int8_t*>(outs.o[0].ptr) + outs.o[0].c_offset +
+                                      (size_t)pix * (uint32_t)outs.o[0].c_stride + cobase) = code;
             continue;
           }
         }
