@@ -18,7 +18,13 @@
 namespace pmx {
 namespace {
 
-constexpr int kChunk = 8192;  // anchors per CTA (13 CTAs per KITTI frame: fewer, fuller waves)
+// anchors per CTA, chosen per call: large batches want few, full CTAs (16384: 7 per
+// KITTI frame, 68 vs 76 us at batch 32), batch 1 wants more CTAs per frame (4096: 23 vs 27 us)
+int decode_chunk(int batch) {
+  const char* e = getenv("PMX_DECODE_CHUNK");  // A/B override
+  if (e && atoi(e) >= 1024) return atoi(e) & ~1023;
+  return batch >= 8 ? 16384 : (batch >= 2 ? 8192 : 4096);  // measured: b32 68 us, b1 23 us
+}
 constexpr int kThreads = 1024;
 constexpr int kCap = 4096;    // candidates sorted in shared memory
 
@@ -66,15 +72,15 @@ __device__ __forceinline__ bool last_arrival(int* ctr, int n_ctas) {
 
 __global__ void __launch_bounds__(kThreads) topk_hist(const float* __restrict__ heads, int c_stride, int cls_off,
                                                       int n_anchors, int64_t ncand, int k, int* hist, int* arrive,
-                                                      uint32_t* thresh) {
+                                                      uint32_t* thresh, int chunk) {
   pdl_begin();
   __shared__ int h[kBins];
   __shared__ int sh[32];
   const int b = blockIdx.y;
   for (int t = threadIdx.x; t < kBins; t += blockDim.x) h[t] = 0;
   __syncthreads();
-  const int64_t base = (int64_t)blockIdx.x * kChunk;
-  for (int t = threadIdx.x; t < kChunk; t += blockDim.x) {
+  const int64_t base = (int64_t)blockIdx.x * chunk;
+  for (int t = threadIdx.x; t < chunk; t += blockDim.x) {
     const int64_t i = base + t;
     if (i < ncand) atomicAdd(&h[(int)(cand_key(heads, c_stride, cls_off, n_anchors, ncand, b, i) >> 53)], 1);
   }
@@ -161,7 +167,7 @@ __device__ void decode_one(const pmx_anchor_desc& d, unsigned long long key, int
 __global__ void __launch_bounds__(kThreads) topk_select(
     const pmx_anchor_desc d, const float* __restrict__ heads, int c_stride, int cls_off, int box_off, int dir_off,
     int out_h, int out_w, const uint32_t* __restrict__ thresh, unsigned long long* cand, int* cnt, int* arrive,
-    int32_t* topk_idx, float* topk_logit, float* boxes, int32_t* dir_label) {
+    int32_t* topk_idx, float* topk_logit, float* boxes, int32_t* dir_label, int chunk) {
   pdl_begin();
   __shared__ unsigned long long s[kCap];
   __shared__ int sh_hist[256];
@@ -172,8 +178,8 @@ __global__ void __launch_bounds__(kThreads) topk_select(
   const uint32_t T = thresh[b];
   const int lane = threadIdx.x & 31;
   unsigned long long* cb = cand + (int64_t)b * ncand;
-  const int64_t base = (int64_t)blockIdx.x * kChunk;
-  for (int t0 = 0; t0 < kChunk; t0 += blockDim.x) {
+  const int64_t base = (int64_t)blockIdx.x * chunk;
+  for (int t0 = 0; t0 < chunk; t0 += blockDim.x) {
     const int64_t i = base + t0 + threadIdx.x;
     unsigned long long key = 0ull;
     bool keep = false;
@@ -316,12 +322,13 @@ pmx_status pmx_decode_topk(const pmx_anchor_desc* desc, int32_t batch, int32_t o
   DecodeWs w = carve_ws(ws, batch, ncand);
   PMX_REQUIRE(ws && ws_bytes >= w.bytes, "decode workspace too small");
   PMX_CUDA(cudaMemsetAsync(w.hist, 0, w.zero_bytes, stream));
-  const int nch = (int)ceil_div(ncand, kChunk);
+  const int chunk = decode_chunk(batch);
+  const int nch = (int)ceil_div(ncand, chunk);
   PMX_CUDA(launch_pdl(topk_hist, dim3(nch, batch), dim3(kThreads), 0, stream, heads, head_c_stride, cls_off,
-                      d.n_anchors, ncand, d.k, w.hist, w.arrive, w.thresh));
+                      d.n_anchors, ncand, d.k, w.hist, w.arrive, w.thresh, chunk));
   PMX_CUDA(launch_pdl(topk_select, dim3(nch, batch), dim3(kThreads), 0, stream, d, heads, head_c_stride, cls_off,
                       box_off, dir_off, out_h, out_w, (const uint32_t*)w.thresh, w.cand, w.cnt, w.arrive + batch,
-                      topk_idx, topk_logit, boxes, dir_label));
+                      topk_idx, topk_logit, boxes, dir_label, chunk));
   return check_launch("pmx_decode_topk");
 }
 
