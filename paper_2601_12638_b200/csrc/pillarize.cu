@@ -74,7 +74,8 @@ size_t carve(const pmx_grid* g, int32_t B, int64_t nmax, int32_t pcap, void* bas
 
 // first = INT_MAX-ish (0x7f7f7f7f, as the memset it replaces), cnt = fill = 0,
 // look-back words, tickets and the overflow counter = 0
-__global__ void init_ws_kernel(PillarWs w, int64_t n_cells, int64_t n_fill, int64_t n_look, int batch) {
+__global__ void init_ws_kernel(PillarWs w, int64_t n_cells, int64_t n_fill, int64_t n_look, int batch,
+                               int64_t n_ptblk) {
   pdl_begin();
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nt = (int64_t)gridDim.x * blockDim.x;
   const int4 f4 = make_int4(0x7f7f7f7f, 0x7f7f7f7f, 0x7f7f7f7f, 0x7f7f7f7f), z4 = make_int4(0, 0, 0, 0);
@@ -92,6 +93,7 @@ __global__ void init_ws_kernel(PillarWs w, int64_t n_cells, int64_t n_fill, int6
   for (int64_t i = tid; i < n_fill; i += nt) w.fill[i] = 0;
   for (int64_t i = tid; i < n_look; i += nt) w.look[i] = 0ull;
   for (int64_t i = tid; i < batch; i += nt) w.ticket[i] = 0;
+  for (int64_t i = tid; i < n_ptblk; i += nt) w.ptblk[i] = 0;
   if (tid == 0) *w.ovf_n = 0;
 }
 
@@ -137,6 +139,34 @@ __global__ void __launch_bounds__(kPtBlock) flag_kernel(const int64_t* __restric
   if (i < n) flag = w.first[b * hw + w.cell[b * nmax + i]] == (int)i;
   int c = __syncthreads_count(flag);
   if (threadIdx.x == 0) w.ptblk[b * nb + blockIdx.x] = c;
+}
+
+// Same counts per cell instead of per point: every occupied cell adds 1 to the
+// 1024-point block holding its first point (shared-memory histogram per CTA, then one
+// atomic per non-empty bin) -- a coalesced pass over first[] instead of a random
+// first[cell[i]] read per point.  ptblk is zeroed by init_ws_kernel.
+__global__ void __launch_bounds__(1024) firsthist_kernel(const pmx_grid g, PillarWs w, int nb) {
+  pdl_begin();
+  extern __shared__ int h[];  // [nb]
+  const int b = blockIdx.y;
+  const int64_t hw = (int64_t)g.grid_h * g.grid_w;
+  for (int t = threadIdx.x; t < nb; t += blockDim.x) h[t] = 0;
+  __syncthreads();
+  const int64_t c0 = (int64_t)blockIdx.x * kCellBlock + threadIdx.x * kCellPerThr;
+  int f[kCellPerThr];
+  if ((hw & 3) == 0 && c0 + kCellPerThr <= hw) {
+    const int4 f4 = __ldg(reinterpret_cast<const int4*>(w.first + b * hw + c0));
+    f[0] = f4.x; f[1] = f4.y; f[2] = f4.z; f[3] = f4.w;
+  } else {
+#pragma unroll
+    for (int j = 0; j < kCellPerThr; ++j) f[j] = c0 + j < hw ? w.first[b * hw + c0 + j] : 0x7f7f7f7f;
+  }
+#pragma unroll
+  for (int j = 0; j < kCellPerThr; ++j)
+    if (f[j] != 0x7f7f7f7f) atomicAdd(&h[f[j] / kPtBlock], 1);
+  __syncthreads();
+  for (int t = threadIdx.x; t < nb; t += blockDim.x)
+    if (h[t]) atomicAdd(w.ptblk + (int64_t)b * nb + t, h[t]);
 }
 
 // inclusive block scan of one int per thread (blockDim.x == 1024)
@@ -553,12 +583,17 @@ pmx_status pmx_pillarize(const float* points, const int64_t* frame_offsets, int3
     const int64_t n4 = batch * hw;  // first / cnt (int4 when hw % 4 == 0)
     const int blocks = (int)std::min<int64_t>(ceil_div(n4, 256 * 4), 148 * 8);
     PMX_CUDA(launch_pdl(init_ws_kernel, dim3(blocks), dim3(256), 0, stream, w, n4, (int64_t)batch * pcap,
-                        (int64_t)batch * cb, batch));
+                        (int64_t)batch * cb, batch, (int64_t)batch * nb));
   }
   const int ptx = (int)std::min<int64_t>(ceil_div(nmax, 256), 4096);
   PMX_CUDA(launch_pdl(bin_kernel, dim3(ptx, batch), dim3(256), 0, stream, reinterpret_cast<const float4*>(points),
                       frame_offsets, nmax, g, w));
-  PMX_CUDA(launch_pdl(flag_kernel, dim3(nb, batch), dim3(kPtBlock), 0, stream, frame_offsets, nmax, g, w, nb));
+  if (nb <= 16384) {  // the per-frame bins fit in shared memory
+    PMX_CUDA(cudaFuncSetAttribute(firsthist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, nb * 4));
+    PMX_CUDA(launch_pdl(firsthist_kernel, dim3(cb, batch), dim3(1024), (size_t)nb * 4, stream, g, w, nb));
+  } else {
+    PMX_CUDA(launch_pdl(flag_kernel, dim3(nb, batch), dim3(kPtBlock), 0, stream, frame_offsets, nmax, g, w, nb));
+  }
   PMX_CUDA(launch_pdl(thresh_kernel, dim3(batch), dim3(1024), 0, stream, frame_offsets, nmax, g, w, nb));
   PMX_CUDA(launch_pdl(emit_fused_kernel, dim3(cb, batch), dim3(1024), 0, stream, g, w, cb, pcap, coords, counts,
                       n_pillars));
