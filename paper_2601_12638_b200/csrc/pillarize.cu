@@ -192,6 +192,32 @@ __device__ int block_incl_scan(int v, int* sh /*32*/) {
   return v;
 }
 
+// the same for a (kept, points) pair packed as kept << 40 | points in 64 bits: one scan
+// (and three barriers) instead of two; returns the inclusive pair, *total = block sum
+__device__ unsigned long long block_incl_scan2(unsigned long long v, unsigned long long* sh /*32*/,
+                                               unsigned long long* total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long t = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += t;
+  }
+  if (lane == 31) sh[wid] = v;
+  __syncthreads();
+  if (wid == 0) {
+    unsigned long long x = sh[lane];
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long t = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += t;
+    }
+    sh[lane] = x;
+  }
+  __syncthreads();
+  if (wid > 0) v += sh[wid - 1];
+  *total = sh[31];
+  __syncthreads();
+  return v;
+}
+
 __global__ void __launch_bounds__(1024) thresh_kernel(const int64_t* __restrict__ offs, int64_t nmax,
                                                       const pmx_grid g, PillarWs w, int nb) {
   pdl_begin();
@@ -245,7 +271,7 @@ constexpr unsigned long long kLookPtsMask = (1ull << 40) - 1, kLookKeptMask = (1
 __global__ void __launch_bounds__(1024) emit_fused_kernel(const pmx_grid g, PillarWs w, int cb, int32_t pcap,
                                                           int32_t* coords, int32_t* counts, int32_t* n_pillars) {
   pdl_begin();
-  __shared__ int sh[32];
+  __shared__ unsigned long long sh2[32];
   __shared__ int s_blk;
   __shared__ unsigned long long s_prefix;
   const int b = blockIdx.y;
@@ -275,13 +301,12 @@ __global__ void __launch_bounds__(1024) emit_fused_kernel(const pmx_grid g, Pill
     kept += keep[j];
     pts += keep[j] ? n[j] : 0;
   }
-  int a = block_incl_scan(kept, sh);
-  const int kept_tot = sh[31];
-  __syncthreads();
-  int p = block_incl_scan(pts, sh);
-  const int pts_tot = sh[31];
-  a -= kept;
-  p -= pts;
+  unsigned long long tot2;
+  const unsigned long long mine = ((unsigned long long)kept << 40) | (unsigned long long)pts;
+  const unsigned long long incl = block_incl_scan2(mine, sh2, &tot2);
+  const int kept_tot = (int)(tot2 >> 40), pts_tot = (int)(tot2 & kLookPtsMask);
+  int a = (int)((incl - mine) >> 40);
+  int p = (int)((incl - mine) & kLookPtsMask);
   if (threadIdx.x < 32) {
     // warp-wide decoupled look-back: 32 predecessors per round (nearest first in lane
     // order); stop at the nearest one that already holds its inclusive prefix
