@@ -243,22 +243,6 @@ constexpr size_t pfn_points_smem() {
   return (size_t)(kThreads / 32) * 32 * kSlots * Rec<DT>::BYTES + (size_t)(kThreads / 32) * 32 * 6 * 4;
 }
 
-__device__ __forceinline__ void store2(const OutDev& o, int64_t pix, int c, float y0, float y1, bool two) {
-  const int64_t off = pix * o.c_stride + o.c_offset + c;
-  if (o.dtype == PMX_F16 && two && (off & 1) == 0) {
-    const __half2 h = __halves2half2(f16_sat(y0), f16_sat(y1));
-    *reinterpret_cast<__half2*>(reinterpret_cast<__half*>(o.ptr) + off) = h;
-  } else if (o.dtype == PMX_I8 && two && (off & 1) == 0) {
-    const int a = quantize_exact(y0, o.scale, o.inv), b = quantize_exact(y1, o.scale, o.inv);
-    *reinterpret_cast<uint16_t*>(reinterpret_cast<int8_t*>(o.ptr) + off) = (uint16_t)((a & 0xff) | ((b & 0xff) << 8));
-  } else if (o.dtype == PMX_F32 && two && (off & 1) == 0) {
-    *reinterpret_cast<float2*>(reinterpret_cast<float*>(o.ptr) + off) = make_float2(y0, y1);
-  } else {
-    store_one(o, pix, c, y0);
-    if (two) store_one(o, pix, c + 1, y1);
-  }
-}
-
 template <int DT>
 __global__ void __launch_bounds__(kThreads, 2) pfn_points_kernel(const PfnArgs a, const Outs outs) {
   pdl_begin();
