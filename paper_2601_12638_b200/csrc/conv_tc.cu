@@ -51,20 +51,6 @@ __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
 }
 
-// try_wait with a suspend-time hint: a waiting warp sleeps (NANOSLEEP.SYNCS, woken by
-// the barrier's phase flip) instead of spinning on issue slots the epilogue needs
-__device__ __forceinline__ bool mbar_try_sleep(uint32_t bar, uint32_t parity) {
-  uint32_t ok;
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
-      "selp.u32 %0, 1, 0, p;\n\t}"
-      : "=r"(ok)
-      : "r"(bar), "r"(parity), "r"(1000000u)
-      : "memory");
-  return ok != 0;
-}
-
 // plain try_wait loop (no suspend-time hint) for the MMA issuer: it must resume the
 // moment an operand stage or accumulator frees up
 __device__ __forceinline__ void mbar_spin(uint32_t bar, uint32_t parity) {
@@ -92,15 +78,6 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
           dst),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
-      : "memory");
-}
-
-__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2,
-                                            uint32_t bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
-          dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
       : "memory");
 }
 
@@ -455,7 +432,6 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
 // Replaces the canvas write of pm/tensor_ops.py:138-160 + the conv's canvas read.
 template <int HS>
 struct GatherGeom {
-  static constexpr int NPL = HS == 2 ? 4 : 1;
   static constexpr int HPX_TOTAL = HS == 2 ? 561 : 180;
 };
 
@@ -875,8 +851,6 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
     float lo = __int_as_float(0x7f800000), hi = -lo;
     const float qlo = p.relu ? 0.0f : -128.0f;
     // OUTK 1 fast path: consumer parameters in registers, kernel-uniform eligibility
-    int8_t* const o_ptr = reinterpret_cast<int8_t*>(outs.o[0].ptr) + outs.o[0].c_offset;
-    const int64_t o_cs = outs.o[0].c_stride;
     const double o_scale = outs.o[0].scale;
     const float o_inv = outs.o[0].inv;
     const bool fast = OUTK == 1 && !p.bn_post && !p.keys && (p.n_gemm % 16) == 0;
@@ -1154,7 +1128,8 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
 #if defined(PMX_ABLATE) && PMX_ABLATE == 1
             continue;
 #elif defined(PMX_ABLATE) && PMX_ABLATE == 3
-            *reinterpret_cast<uint4*>(o_ptr + (size_t)pix * o_cs + cobase) = make_uint4(v[0], v[5], v[10], v[15]);
+            *reinterpret_cast<uint4*>(reinterpret_cast<int8_t*>(outs.o[0].ptr) + outs.o[0].c_offset +
+                                      (size_t)pix * (uint32_t)outs.o[0].c_stride + cobase) = make_uint4(v[0], v[5], v[10], v[15]);
             continue;
 #endif
             float y[16];
