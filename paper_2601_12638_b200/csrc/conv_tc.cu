@@ -932,7 +932,11 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
 #pragma unroll
               for (int j = 0; j < 16; ++j) y[j] = fmaxf(y[j], 0.f);
             }
-            *reinterpret_cast<uint4*>(p8 + (size_t)pix_in * cs8 + cobase) = quant16(y, sc8, inv8);
+            // clamp-free fast quantizer (y is already ReLU'd when relu is set); ties,
+            // saturation and NaN take the exact path
+            uint4 code8;
+            if (!quant16_noclamp<false>(y, inv8, code8)) code8 = quant16(y, sc8, inv8);
+            *reinterpret_cast<uint4*>(p8 + (size_t)pix_in * cs8 + cobase) = code8;
           };
           auto sts_f16 = [&](uint32_t a0, uint32_t a1, const float (&y)[16]) {
             asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a0), "r"(f16x2_sat(y[0], y[1])),
