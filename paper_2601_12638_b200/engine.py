@@ -769,7 +769,7 @@ class CompiledGraph:
         n = 0
         for name, _ in self.ops:
             if name == "pillarize":
-                n += 7  # bin, flag, thresh, emit (single pass), slot, select_small, select
+                n += 8  # init, bin, first-seen histogram, thresh, emit (single pass), slot, select (x2)
             elif name == "decode":
                 n += 2  # topk_hist (+ threshold), topk_select (+ sort, decode)
             else:
