@@ -309,3 +309,33 @@ def test_pipelined_engine_matches_sequential(pm):
     torch.cuda.synchronize()
     for o, w in zip(outs2, want):
         assert torch.equal(o, w)
+
+
+def test_int8_plan_tcgen05_equals_simt_end_to_end(pm):
+    """All-INT8 plan, two full-size KITTI frames: every conv through the tcgen05 kernels
+    (swizzled halos, cp.async gather, staged stores, fused heads) vs every conv through
+    the SIMT kernels (dense canvas, no gather).  Integer arithmetic end to end, so the
+    head maps and the top-k must be identical bit for bit."""
+    import torch
+
+    from paper_2601_12638_b200 import _native as N
+
+    lib = N.load()
+    cfg = pm.PointPillarsConfig(max_pillars=16000)
+    graph = pm.build_pointpillars(cfg, seed=11)
+    frames = [pm.make_frame(120000, 70 + i, cfg) for i in range(2)]
+    stats = pm.calibrate_frames(graph, [pm.make_frame(120000, 80, cfg, 0.01)], cfg)
+    got = {}
+    for mode in (0, 1):
+        lib.pmx_set_conv_backend(mode)
+        try:
+            e = pm.PointPillarsEngine(graph, "INT8", stats, cfg, batch=2, max_points_per_frame=120000)
+            e.load_points(frames)
+            e.run()
+            torch.cuda.synchronize()
+            got[mode] = ({k: v.clone() for k, v in e.heads().items()}, e.topk()["idx"].clone())
+        finally:
+            lib.pmx_set_conv_backend(0)
+    for name in got[0][0]:
+        assert torch.equal(got[0][0][name], got[1][0][name]), name
+    assert torch.equal(got[0][1], got[1][1])
