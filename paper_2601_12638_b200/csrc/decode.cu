@@ -72,7 +72,7 @@ __device__ __forceinline__ bool last_arrival(int* ctr, int n_ctas) {
 
 __global__ void __launch_bounds__(kThreads) topk_hist(const float* __restrict__ heads, int c_stride, int cls_off,
                                                       int n_anchors, int64_t ncand, int k, int* hist, int* arrive,
-                                                      uint32_t* thresh, int chunk) {
+                                                      uint32_t* thresh, int chunk, unsigned long long* keys) {
   pdl_begin();
   __shared__ int h[kBins];
   __shared__ int sh[32];
@@ -80,9 +80,15 @@ __global__ void __launch_bounds__(kThreads) topk_hist(const float* __restrict__ 
   for (int t = threadIdx.x; t < kBins; t += blockDim.x) h[t] = 0;
   __syncthreads();
   const int64_t base = (int64_t)blockIdx.x * chunk;
+  unsigned long long* kb = keys + (int64_t)b * ncand;
   for (int t = threadIdx.x; t < chunk; t += blockDim.x) {
     const int64_t i = base + t;
-    if (i < ncand) atomicAdd(&h[(int)(cand_key(heads, c_stride, cls_off, n_anchors, ncand, b, i) >> 53)], 1);
+    if (i < ncand) {
+      // the key goes to a dense array: pass 2 reads 8 bytes per anchor, not the heads rows
+      const unsigned long long key = cand_key(heads, c_stride, cls_off, n_anchors, ncand, b, i);
+      kb[i] = key;
+      atomicAdd(&h[(int)(key >> 53)], 1);
+    }
   }
   __syncthreads();
   int* hb = hist + (int64_t)b * kBins;
@@ -167,7 +173,8 @@ __device__ void decode_one(const pmx_anchor_desc& d, unsigned long long key, int
 __global__ void __launch_bounds__(kThreads) topk_select(
     const pmx_anchor_desc d, const float* __restrict__ heads, int c_stride, int cls_off, int box_off, int dir_off,
     int out_h, int out_w, const uint32_t* __restrict__ thresh, unsigned long long* cand, int* cnt, int* arrive,
-    int32_t* topk_idx, float* topk_logit, float* boxes, int32_t* dir_label, int chunk) {
+    int32_t* topk_idx, float* topk_logit, float* boxes, int32_t* dir_label, int chunk,
+    const unsigned long long* __restrict__ keys) {
   pdl_begin();
   __shared__ unsigned long long s[kCap];
   __shared__ int sh_hist[256];
@@ -184,7 +191,7 @@ __global__ void __launch_bounds__(kThreads) topk_select(
     unsigned long long key = 0ull;
     bool keep = false;
     if (i < ncand) {
-      key = cand_key(heads, c_stride, cls_off, n_anchors, ncand, b, i);
+      key = __ldcs(keys + (int64_t)b * ncand + i);  // written by pass 1 (streaming: read once)
       keep = (uint32_t)(key >> 32) >= T;
     }
     const unsigned m = __ballot_sync(0xffffffffu, keep);
@@ -264,6 +271,7 @@ __global__ void pack_records_kernel(int n, const int32_t* __restrict__ idx, cons
 
 struct DecodeWs {
   unsigned long long* cand;
+  unsigned long long* keys;  // [B, ncand] every anchor's key (pass 1 -> pass 2)
   int* hist;     // [B, kBins]
   int* cnt;      // [B]
   int* arrive;   // [2, B]
@@ -282,6 +290,7 @@ DecodeWs carve_ws(void* base, int32_t batch, int64_t ncand) {
     return r;
   };
   w.cand = (unsigned long long*)take(sizeof(unsigned long long) * batch * ncand);
+  w.keys = (unsigned long long*)take(sizeof(unsigned long long) * batch * ncand);
   const size_t z0 = off;
   w.hist = (int*)take(sizeof(int) * batch * kBins);
   w.cnt = (int*)take(sizeof(int) * batch);
@@ -325,10 +334,10 @@ pmx_status pmx_decode_topk(const pmx_anchor_desc* desc, int32_t batch, int32_t o
   const int chunk = decode_chunk(batch);
   const int nch = (int)ceil_div(ncand, chunk);
   PMX_CUDA(launch_pdl(topk_hist, dim3(nch, batch), dim3(kThreads), 0, stream, heads, head_c_stride, cls_off,
-                      d.n_anchors, ncand, d.k, w.hist, w.arrive, w.thresh, chunk));
+                      d.n_anchors, ncand, d.k, w.hist, w.arrive, w.thresh, chunk, w.keys));
   PMX_CUDA(launch_pdl(topk_select, dim3(nch, batch), dim3(kThreads), 0, stream, d, heads, head_c_stride, cls_off,
                       box_off, dir_off, out_h, out_w, (const uint32_t*)w.thresh, w.cand, w.cnt, w.arrive + batch,
-                      topk_idx, topk_logit, boxes, dir_label, chunk));
+                      topk_idx, topk_logit, boxes, dir_label, chunk, (const unsigned long long*)w.keys));
   return check_launch("pmx_decode_topk");
 }
 
