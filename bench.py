@@ -38,6 +38,14 @@ MAX_PILLARS = 16000
 CALIB_FRAMES = 2
 
 
+def torch_dist_done():
+    import torch.distributed as dist
+
+    if dist.is_initialized():
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 def _peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -109,7 +117,7 @@ def cpu_reference_frame(pm, O, graph, stats, cfg, frame, plan):
     return heads
 
 
-def run_reference(args, rank):
+def run_reference(args, rank, world):
     """--impl reference: the reference's CPU algorithm (oracle port of pillarmix) on host cores."""
     if rank != 0:
         return
@@ -131,7 +139,7 @@ def run_reference(args, rank):
     dt = time.perf_counter() - t0
     fps = args.steps / dt
     line = {
-        "impl": "reference", "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": args.gpus,
+        "impl": "reference", "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "int8/fp16 (fake-quant f32 numpy)", "data": "synthetic",
         "config": {"workload": "C4 frames (60k-150k pts), mixed plan " + pm.MIXED_PLAN_LABEL + ", 1 frame per step",
@@ -141,6 +149,26 @@ def run_reference(args, rank):
         "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def launch_check(args, D):
+    """Every rank joins the process group (NCCL with GPUs, gloo without), the ranks agree
+    on the world size and the max over ranks; rank 0 prints one JSON line."""
+    import torch
+
+    backend = "nccl" if torch.cuda.is_available() else "gloo"
+    rank, world, local = D.init_from_env(backend)
+    dev = None
+    if backend == "nccl":
+        torch.cuda.set_device(local)
+        dev = torch.device("cuda", local)
+    mx = D.max_over_ranks(float(rank), device=dev)
+    ranks = D.gather_scalars([rank], device=dev).ravel().astype(int).tolist()
+    if rank == 0:
+        print(json.dumps({"launch_check": True, "n_gpus": world, "backend": backend, "max_rank": mx,
+                          "ranks": ranks}), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
 
 
 def b1_latency(pm, graph, stats, cfg, plan, n_points, seed, reps=200):
@@ -173,13 +201,26 @@ def main():
     ap.add_argument("--batch", type=int, default=BATCH)
     ap.add_argument("--no-latency", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--launch-check", action="store_true",
+                    help="only start the ranks, agree on the world size and exit (tests the multi-rank launch)")
     args = ap.parse_args()
 
     from paper_2601_12638_b200 import distributed as D
 
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # no outer torchrun: start one rank per GPU ourselves (127.0.0.1, free port)
+        sys.exit(D.spawn_ranks(str(Path(__file__).resolve()), args.gpus, sys.argv[1:]))
+    world_env = int(os.environ.get("WORLD_SIZE", "1"))
+    if world_env != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world_env} ranks were launched")
+    if args.launch_check:
+        launch_check(args, D)
+        return
     rank, world, local = D.init_from_env("nccl" if args.impl == "ours" else "gloo")
     if args.impl == "reference":
-        run_reference(args, rank)
+        run_reference(args, rank, world)
+        if world > 1:
+            torch_dist_done()
         return
     import torch
 

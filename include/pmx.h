@@ -252,9 +252,10 @@ pmx_status pmx_conv_gather(const pmx_conv_desc* desc, const void* feats, const i
                            uint32_t* out_keys, pmx_stream_t stream);
 
 /* Force a backend for testing: 0 = automatic, 1 = SIMT reference kernel only,
- * 2 = tcgen05 without the halo variant. */
+ * 2 = tcgen05 without the halo variant.  Thread-local: applies to later calls made
+ * by the calling thread only (no process-wide state). */
 void pmx_set_conv_backend(int32_t mode);
-/* Debug: when non-NULL, tcgen05 conv launches record per-role clock64 stamps of
+/* Debug (thread-local, like pmx_set_conv_backend): when non-NULL, tcgen05 conv launches record per-role clock64 stamps of
  * CTA 0 into buf[10][64]: rows 0-7 producer/MMA/epilogue hand-offs per tile, row 8
  * = kernel entry, setup done, resident weights landed, teardown; row 9 = MMA loop top. */
 void pmx_debug_trace(unsigned long long* buf);
@@ -309,10 +310,12 @@ pmx_status pmx_pack_topk_records(int32_t batch, int32_t k, const int32_t* topk_i
  * K12 sensitivity-sweep error (BASELINE config 5; SPEC.md:364-372 sweep with the
  * head-output error as the score): out2[0] += sum((a - b)^2), out2[1] += sum(b^2)
  * over n f32 values, accumulated in f64 in a fixed order (deterministic:
- * per-block partials, then one ordered reduction).  ws: >= 2 * 1184 doubles.
+ * a fixed number of per-block partials, then one ordered reduction).
+ * ws: device scratch of ws_bytes >= pmx_sq_err_workspace() (checked).
  * ---------------------------------------------------------------------- */
+size_t pmx_sq_err_workspace(void);
 pmx_status pmx_sq_err(const float* a, const float* b, int64_t n, double* out2, double* ws,
-                      pmx_stream_t stream);
+                      size_t ws_bytes, pmx_stream_t stream);
 
 #ifdef __cplusplus
 }

@@ -93,7 +93,8 @@ SIGNATURES = {
                               P]),
     "pmx_pack_topk_records": (I32, [I32, I32, P, P, P, P, P, P]),
     "pmx_zero": (I32, [P, SZ, P]),
-    "pmx_sq_err": (I32, [P, P, I64, P, P, P]),
+    "pmx_sq_err_workspace": (SZ, []),
+    "pmx_sq_err": (I32, [P, P, I64, P, P, SZ, P]),
 }
 
 _LIB = None

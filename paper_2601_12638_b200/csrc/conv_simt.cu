@@ -18,7 +18,9 @@ size_t conv_tc_workspace(const pmx_conv_desc& d);
 bool conv_tc_gather_ok(const pmx_conv_desc& d);
 const char* conv_tc_backend(int dtype, int kind);
 
-int g_conv_backend_mode = 0;
+// backend override of the CALLING thread (tests): thread-local, so concurrent callers on
+// other threads are unaffected and the library holds no shared mutable state
+thread_local int g_conv_backend_mode = 0;
 
 namespace {
 

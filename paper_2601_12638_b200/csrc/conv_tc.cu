@@ -32,8 +32,8 @@
 
 namespace pmx {
 
-extern int g_conv_backend_mode;
-unsigned long long* g_trace = nullptr;  // pmx_debug_trace
+extern thread_local int g_conv_backend_mode;  // per calling thread (test override)
+thread_local unsigned long long* g_trace = nullptr;  // pmx_debug_trace (per calling thread)
 
 namespace {
 
@@ -1337,11 +1337,11 @@ Plan plan_for(const pmx_conv_desc& d, bool gather = false, bool want_stage = fal
   }
   // small M (batch-1 blocks.2: 27 M tiles): split N while the tile count still fits
   // one wave -- each CTA then streams a quarter of the weights and issues N=64 MMAs
-  while (bn > 64 && bn % 32 == 0 && (int64_t)p.m_tiles * ceil_div(p.n_gemm, bn / 2) <= kNumSMs) bn /= 2;
+  while (bn > 64 && bn % 32 == 0 && (int64_t)p.m_tiles * ceil_div(p.n_gemm, bn / 2) <= num_sms()) bn /= 2;
   p.bn = bn;
   p.n_tiles = (int)ceil_div(p.n_gemm, bn);
   const int64_t tiles = (int64_t)p.m_tiles * p.n_tiles;
-  pl.grid_x = (int)(tiles < kNumSMs ? tiles : kNumSMs);
+  pl.grid_x = (int)(tiles < num_sms() ? tiles : num_sms());
   pl.grid_y = 1;
   // warp-transposed int8 stores: every epilogue warp owns exactly 4 chunks (64
   // channels) of a tile, groups never straddle a deconv tap
@@ -1410,7 +1410,7 @@ Plan plan_for(const pmx_conv_desc& d, bool gather = false, bool want_stage = fal
       p.tiles_y = (int)ceil_div(d.out_h, 16);
       p.m_tiles = d.batch * p.tiles_x * p.tiles_y;
       const int64_t t2 = (int64_t)p.m_tiles;
-      pl.grid_x = (int)(t2 < kNumSMs ? t2 : kNumSMs);
+      pl.grid_x = (int)(t2 < num_sms() ? t2 : num_sms());
       p.a_bytes = halo_al;
       p.b_bytes = 0;
       int hs = (int)((budget - bres_total) / halo_al);

@@ -606,7 +606,7 @@ pmx_status pmx_pillarize(const float* points, const int64_t* frame_offsets, int3
   // one kernel initialises every per-call workspace array (six memset nodes before)
   {
     const int64_t n4 = batch * hw;  // first / cnt (int4 when hw % 4 == 0)
-    const int blocks = (int)std::min<int64_t>(ceil_div(n4, 256 * 4), 148 * 8);
+    const int blocks = (int)std::min<int64_t>(ceil_div(n4, 256 * 4), (int64_t)num_sms() * 8);
     PMX_CUDA(launch_pdl(init_ws_kernel, dim3(blocks), dim3(256), 0, stream, w, n4, (int64_t)batch * pcap,
                         (int64_t)batch * cb, batch, (int64_t)batch * nb));
   }
@@ -630,7 +630,7 @@ pmx_status pmx_pillarize(const float* points, const int64_t* frame_offsets, int3
     PMX_CUDA(launch_pdl(select_small_kernel, dim3((int)ceil_div(pcap, 256), batch), dim3(256), 0, stream, nmax, g,
                         w, pcap, n_pillars, pt_idx));
   // overflow pillars (> 32 points): one warp each, grid-stride over the device-side list
-  PMX_CUDA(launch_pdl(select_kernel, dim3(kNumSMs), dim3(256), 0, stream, frame_offsets, nmax, g, w, pcap, n_pillars,
+  PMX_CUDA(launch_pdl(select_kernel, dim3(num_sms()), dim3(256), 0, stream, frame_offsets, nmax, g, w, pcap, n_pillars,
                       pt_idx));
   return check_launch("pmx_pillarize");
 }

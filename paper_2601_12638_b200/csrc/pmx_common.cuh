@@ -35,7 +35,9 @@ pmx_status check_launch(const char* what);
 
 inline int elem_size(int dtype) { return dtype == PMX_F32 ? 4 : (dtype == PMX_F16 ? 2 : 1); }
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
-constexpr int kNumSMs = 148;
+// SM count of the current device (queried once per device, cached): persistent grids
+// are sized from it, never from a compile-time constant (other SKUs, MIG slices)
+int num_sms();
 
 // ---------------------------------------------------------------------------
 // programmatic dependent launch: kernels are launched with programmatic stream

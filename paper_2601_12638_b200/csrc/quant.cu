@@ -1,6 +1,8 @@
 // K1 quantize / fake_quant / fp16_roundtrip, K2 min/max observers, error plumbing,
 // nearest 2x upsample.  All HBM-bound elementwise kernels: grid-stride loops over
 // 4-element vectors, grid sized to a multiple of the 148 SMs.
+#include <mutex>
+
 #include "pmx_common.cuh"
 
 namespace pmx {
@@ -8,6 +10,18 @@ namespace pmx {
 static thread_local std::string g_last_error;
 
 void set_error(const std::string& msg) { g_last_error = msg; }
+
+int num_sms() {
+  static std::once_flag once[64];
+  static int count[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+  std::call_once(once[dev], [dev] {
+    int n = 0;
+    count[dev] = cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && n > 0 ? n : 148;
+  });
+  return count[dev];
+}
 
 pmx_status fail(pmx_status code, const std::string& msg) {
   g_last_error = msg;
@@ -35,7 +49,7 @@ pmx_status validate_outs(const pmx_out* outs, int n, int c_needed) {
 
 static int grid_for(int64_t n, int threads) {
   int64_t blocks = ceil_div(n, threads);
-  int64_t cap = (int64_t)kNumSMs * 16;
+  int64_t cap = (int64_t)num_sms() * 16;
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
   return (int)blocks;
@@ -181,7 +195,9 @@ __global__ void __launch_bounds__(256) cast_out_kernel(const float* __restrict__
   if (keys) block_minmax_commit<256>(lo, hi, keys);
 }
 
-constexpr int kErrBlocks = 8 * kNumSMs;
+// fixed partial count (not tied to the SM count): the f64 reduction order, and so the
+// result, is the same on every device
+constexpr int kErrBlocks = 1184;
 
 __global__ void __launch_bounds__(256) sq_err_partial(const float* __restrict__ a, const float* __restrict__ b,
                                                       int64_t n, double* part) {
@@ -330,10 +346,14 @@ pmx_status pmx_minmax(const void* x, int64_t n, int32_t dtype, uint32_t* keys, p
   return check_launch("pmx_minmax");
 }
 
-pmx_status pmx_sq_err(const float* a, const float* b, int64_t n, double* out2, double* ws, pmx_stream_t stream) {
+size_t pmx_sq_err_workspace(void) { return 2 * sizeof(double) * kErrBlocks; }
+
+pmx_status pmx_sq_err(const float* a, const float* b, int64_t n, double* out2, double* ws, size_t ws_bytes,
+                      pmx_stream_t stream) {
   PMX_REQUIRE(n >= 0, "negative length");
   if (n == 0) return PMX_OK;
   PMX_REQUIRE(a && b && out2 && ws, "NULL operand");
+  PMX_REQUIRE(ws_bytes >= pmx_sq_err_workspace(), "pmx_sq_err workspace too small (see pmx_sq_err_workspace)");
   sq_err_partial<<<kErrBlocks, 256, 0, stream>>>(a, b, n, ws);
   sq_err_final<<<1, 32, 0, stream>>>(ws, kErrBlocks, out2);
   return check_launch("pmx_sq_err");

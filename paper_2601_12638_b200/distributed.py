@@ -13,7 +13,7 @@ import os
 
 import numpy as np
 
-__all__ = ["init_from_env", "shard_range", "shard_round_robin", "pack_topk", "gather_records", "max_over_ranks",
+__all__ = ["init_from_env", "free_port", "spawn_ranks", "shard_range", "shard_round_robin", "pack_topk", "gather_records", "max_over_ranks",
            "gather_scalars"]
 
 RECORD = 10  # per detection: idx, logit, x, y, z, w, l, h, yaw, dir
@@ -29,11 +29,33 @@ def init_from_env(backend: str | None = None):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1 and not dist.is_initialized():
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29531")
         backend = backend or ("nccl" if torch.cuda.is_available() else "gloo")
         if backend == "nccl":
             torch.cuda.set_device(local)
         dist.init_process_group(backend=backend, rank=rank, world_size=world)
     return rank, world, local
+
+
+def free_port() -> int:
+    """An unused TCP port on 127.0.0.1 (rendezvous for spawned ranks)."""
+    import socket
+
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def spawn_ranks(script: str, n: int, argv: list[str]) -> int:
+    """Re-run ``script argv`` as ``n`` ranks under torch.distributed.run (one process per
+    GPU, rendezvous on 127.0.0.1 at a free port) and return the launcher's exit code.
+    Used when a multi-GPU run is requested without an outer torchrun."""
+    import subprocess
+    import sys
+
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}", script, *argv]
+    return subprocess.call(cmd)
 
 
 def shard_range(n_items: int, rank: int, world: int) -> range:

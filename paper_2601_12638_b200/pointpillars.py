@@ -308,6 +308,10 @@ class PipelinedEngine:
             if i + 1 < n:
                 self._upload(i + 1, *batches[i + 1])
             comp.wait_event(self.copied[slot])
+            if i >= 2:
+                # batch i-2's D2H copy (d2h stream) must have finished reading this slot's
+                # records buffer before the graph rewrites it
+                comp.wait_event(self.fetched[slot])
             self.graphs[slot].replay()
             rec = pack(self.eng.topk()) if pack is not None else self.slots[slot][2]
             self.done[slot].record(comp)

@@ -36,8 +36,15 @@ class SensitivityRecord:
     rank: int
 
 
+def sq_err_workspace(lib):
+    import torch
+
+    return torch.empty(lib.pmx_sq_err_workspace() // 8, dtype=torch.float64, device="cuda")
+
+
 def _sq_err(lib, a, b, acc, ws):
-    N.check(lib.pmx_sq_err(a.data_ptr(), b.data_ptr(), a.numel(), acc.data_ptr(), ws.data_ptr(), N.stream_ptr()),
+    N.check(lib.pmx_sq_err(a.data_ptr(), b.data_ptr(), a.numel(), acc.data_ptr(), ws.data_ptr(),
+                           ws.numel() * ws.element_size(), N.stream_ptr()),
             "sq_err")
 
 
@@ -71,7 +78,7 @@ def plan_errors(graph, stats, frames, plans, ref, cfg: PointPillarsConfig, batch
 
     lib = N.require_cuda()
     nmax = max(len(f) for f in frames)
-    ws = torch.empty(2 * 8 * 148, dtype=torch.float64, device="cuda")
+    ws = sq_err_workspace(lib)
     res = []
     for plan in plans:
         eng = PointPillarsEngine(graph, plan, stats, cfg, batch=batch, max_points_per_frame=nmax)

@@ -91,3 +91,33 @@ def test_two_rank_sweep_sharding():
     assert s0 == list(range(0, 23, 2)) and s1 == list(range(1, 23, 2))
     want = [[j + 1.0, 10.0 * (j + 1)] for j in range(23)]
     assert t0 == t1 == want
+
+
+def test_bench_spawns_ranks_itself():
+    """`bench.py --gpus 2` without an outer torchrun launches its own two ranks (torchrun
+    re-exec, 127.0.0.1, free port); here they rendezvous over gloo on the CPU."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parent.parent
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_PORT")}
+    r = subprocess.run([sys.executable, str(root / "bench.py"), "--gpus", "2", "--launch-check"], env=env,
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [json.loads(ln) for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    assert lines[0]["n_gpus"] == 2 and lines[0]["max_rank"] == 1.0 and lines[0]["ranks"] == [0, 1]
+
+
+def test_bench_rejects_mismatched_world():
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parent.parent
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    r = subprocess.run([sys.executable, str(root / "bench.py"), "--gpus", "2", "--launch-check"], env=env,
+                       capture_output=True, text=True, timeout=120)
+    assert r.returncode != 0 and "WORLD_SIZE=1" in r.stderr

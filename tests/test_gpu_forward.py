@@ -311,6 +311,34 @@ def test_pipelined_engine_matches_sequential(pm):
         assert torch.equal(o, w)
 
 
+def test_pipelined_engine_batch1_many_distinct_frames(pm):
+    """Batch 1 (short graphs) over many distinct frames: every slot's records buffer is
+    rewritten only after the previous D2H copy of that slot finished (no WAR race)."""
+    import torch
+
+    from paper_2601_12638_b200 import distributed as D
+
+    cfg = pm.PointPillarsConfig.small(max_pillars=1500)
+    graph = pm.build_pointpillars(cfg, seed=5)
+    stats = pm.calibrate_frames(graph, [pm.make_frame(3000, 600 + i, cfg) for i in range(2)], cfg)
+    frames = [pm.make_frame(1500 + 37 * j, 700 + j, cfg) for j in range(24)]
+    eng = pm.PointPillarsEngine(graph, pm.MIXED_PLAN_LABEL, stats, cfg, batch=1, max_points_per_frame=3000)
+    want = []
+    for f in frames:
+        eng.load_points([f])
+        eng.run()
+        want.append(D.pack_topk(eng.topk()).cpu())
+    pipe = pm.PipelinedEngine(eng)
+    batches = [(torch.from_numpy(f).pin_memory(), torch.from_numpy(np.array([0, len(f)], np.int64)).pin_memory())
+               for f in frames]
+    for _ in range(3):
+        outs = [torch.empty_like(w).pin_memory() for w in want]
+        pipe.run(batches, outs)
+        torch.cuda.synchronize()
+        for j, (o, w) in enumerate(zip(outs, want)):
+            assert torch.equal(o, w), j
+
+
 def test_int8_plan_tcgen05_equals_simt_end_to_end(pm):
     """All-INT8 plan, two full-size KITTI frames: every conv through the tcgen05 kernels
     (swizzled halos, cp.async gather, staged stores, fused heads) vs every conv through

@@ -20,7 +20,7 @@ def test_sq_err_matches_f64(pm, n):
     import torch
 
     from paper_2601_12638_b200 import _native as N
-    from paper_2601_12638_b200.sweep import _sq_err
+    from paper_2601_12638_b200.sweep import _sq_err, sq_err_workspace
 
     lib = N.require_cuda()
     rng = np.random.default_rng(n)
@@ -28,7 +28,7 @@ def test_sq_err_matches_f64(pm, n):
     b = (a + rng.normal(scale=0.01, size=n)).astype(np.float32)
     ta, tb = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
     acc = torch.zeros(2, dtype=torch.float64, device="cuda")
-    ws = torch.empty(2 * 8 * 148, dtype=torch.float64, device="cuda")
+    ws = sq_err_workspace(lib)
     _sq_err(lib, ta, tb, acc, ws)
     _sq_err(lib, ta, tb, acc, ws)  # accumulates
     got = acc.cpu().numpy()

@@ -42,10 +42,12 @@ def main():
     for name, ms in per.items():
         M, N, K, prec, ein, outb = LAYERS[name]
         flops = 2.0 * B * M * N * K
-        cin = K // 9 if ("backbone" in name) else K
-        in_px = M * 4 if name.endswith((".1.0", ".2.0")) else M  # stride-2 convs read 4x their outputs
+        cin = K // 9 if name.startswith("conv backbone.") else K
+        # exact names (a suffix match would also catch the neck.deblocks.* layers)
+        stride2 = name in ("conv backbone.blocks.1.0", "conv backbone.blocks.2.0")
+        in_px = M * 4 if stride2 else M  # stride-2 convs read 4x their outputs
         in_bytes = in_px * cin * ein
-        if name.endswith("blocks.0.0"):
+        if name == "conv backbone.blocks.0.0":
             in_bytes = 16000 * cin * ein  # the gather reads pillar rows, not a canvas
         bytes_ = B * (in_bytes + M * outb)
         t_c, t_m = flops / (peaks[prec] * 1e12), bytes_ / (hbm * 1e9)
