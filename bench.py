@@ -38,6 +38,19 @@ MAX_PILLARS = 16000
 CALIB_FRAMES = 2
 
 
+def _mma_peaks(peaks):
+    """Dense tcgen05 MMA peaks per layer dtype (TFLOP/s): the measured probe when committed,
+    else the bf16 cuBLAS number of MEASURED_PEAKS.json (fp16) and twice that (int8)."""
+    f = ROOT / "profiles" / "r2_mma_peak.json"
+    if f.exists():
+        d = json.loads(f.read_text())
+        return ({"int8": d["int8_tops_burst"], "fp16": d["f16_tflops_burst"], "fp32": d["tf32_tflops_burst"] / 3.0},
+                "measured tcgen05 MMA burst peaks (profiles/r2_mma_peak.json, tools/mma_peak.cu): FLOP-weighted "
+                "mix of the int8 and f16 peaks over the layers")
+    return ({"fp16": peaks["bf16_tflops"], "int8": 2.0 * peaks["bf16_tflops"]},
+            "MEASURED_PEAKS.json bf16 burst (fp16 layers) and 2x bf16 (int8 layers)")
+
+
 def torch_dist_done():
     import torch.distributed as dist
 
@@ -302,10 +315,10 @@ def main():
     dominant = max(by_class, key=by_class.get)
     step_ms_eager = sum(op_ms.values())
     if dominant == "conv":
-        # tensor roofline of the layer mix: each layer at its own dtype's dense peak
-        # (f16: measured bf16 burst -- every op is timed alone from its own graph; int8:
-        # 2x that, the nominal B200 int8:bf16 ratio -- no int8 peak is measured here)
-        pk = {"fp16": peaks["bf16_tflops"], "int8": 2.0 * peaks["bf16_tflops"]}
+        # tensor roofline of the layer mix: each layer at its own dtype's dense tcgen05 peak,
+        # measured on this pool by tools/mma_peak.cu (profiles/r2_mma_peak.json: back-to-back
+        # M=128 N=256 MMAs on every SM, burst -- every op is timed alone from its own graph)
+        pk, pk_src = _mma_peaks(peaks)
         t_min = sum(info[k]["flops"] / (pk.get(info[k]["precision"], peaks["bf16_tflops"]) * 1e12) for k in info)
         peak = conv_flops / t_min / 1e12
         t_bound = sum(max(info[k]["flops"] / (pk.get(info[k]["precision"], peaks["bf16_tflops"]) * 1e12),
@@ -327,8 +340,8 @@ def main():
                     "kernel": "pmx_conv implicit GEMM, all 20 conv/deconv/head launches of a step",
                     "algorithmic": f"{conv_flops / B / 1e9:.2f} GFLOP/frame x {B} frames per step",
                     "share_of_step": conv_ms / step_ms_eager,
-                    "peak_source": peak_src + ": FLOP-weighted mix of bf16 burst (fp16 layers) and 2x bf16 burst "
-                                   "(int8 layers)",
+                    "peak_source": pk_src,
+                    "peaks_tflops": pk,
                     "per_layer_ms": {k: round(op_ms[k], 4) for k in info},
                     # per-layer max(FLOP / dtype peak, algorithmic bytes / HBM): the bound with the
                     # memory-bound layers (deconvs, heads, stride-2 convs) counted as such

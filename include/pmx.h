@@ -42,9 +42,14 @@ typedef enum {
   PMX_ERR_UNSUPPORTED = 3  /* valid request outside what the kernels cover */
 } pmx_status;
 
-typedef enum { PMX_F32 = 0, PMX_F16 = 1, PMX_I8 = 2, PMX_F64 = 3 } pmx_dtype;
+/* PMX_F32X2: an f32 activation stored as a (hi, lo) pair for the 3xTF32 tensor-core
+ * path of FP32 layers -- hi = the value rounded to TF32 (nearest even, low 13
+ * mantissa bits zero), lo = value - hi (exact in f32), hi + lo == value bit for bit.
+ * A pixel holds 2S f32 elements: hi of channel c at [c], lo at [S + c], so the
+ * c_stride of an F32X2 tensor is 2S and the lo plane is c_stride / 2 away. */
+typedef enum { PMX_F32 = 0, PMX_F16 = 1, PMX_I8 = 2, PMX_F64 = 3, PMX_F32X2 = 4 } pmx_dtype;
 
-#define PMX_ABI_VERSION 2
+#define PMX_ABI_VERSION 3
 
 const char* pmx_last_error(void);
 int32_t pmx_abi_version(void);
@@ -147,8 +152,8 @@ pmx_status pmx_pillar_features(const float* points, const int64_t* frame_offsets
 typedef struct {
   void* ptr;         /* NHWC destination */
   double scale;      /* PMX_I8 only: consumer activation scale (codes = quantize(y, scale)) */
-  int32_t dtype;     /* PMX_F32 / PMX_F16 / PMX_I8 */
-  int32_t c_stride;  /* channels per pixel in the destination */
+  int32_t dtype;     /* PMX_F32 / PMX_F16 / PMX_I8 / PMX_F32X2 */
+  int32_t c_stride;  /* elements per pixel in the destination (PMX_F32X2: 2S, both planes) */
   int32_t c_offset;  /* first destination channel (concat slice) */
   int32_t _reserved;
 } pmx_out;
@@ -210,6 +215,11 @@ pmx_status pmx_pfn_pillars(const pmx_pfn_desc* desc, const pmx_grid* grid, int32
  *   INT8: int8 codes x int8 codes -> exact int32, y = f32(acc) * alpha[c] + bias[c]
  *   FP16: binary16 x binary16 -> f32, y = acc + bias[c]
  *   FP32: f32 x f32 -> f32,          y = acc + bias[c]
+ *   FP32 as PMX_F32X2 (3xTF32 on tcgen05): x = hi + lo, w = w_hi + w_lo, acc =
+ *         sum hi*w_hi + lo*w_hi + hi*w_lo (kind::tf32, f32 accumulate),
+ *         y = acc + bias[c]; in_c_stride / in_c_offset count f32 elements of the
+ *         hi plane's pixel (lo at + in_c_stride / 2); weights are prepacked per tap
+ *         as [w_hi | w_hi | w_lo] (K = taps * 3 * Cin, w_hi = tf32 rounding of w).
  * then ReLU, then one store per pmx_out (int8 codes are exact quantize()).
  * Weight layouts: CONV2D [Cout, kh, kw, Cin]; DECONV2D [(dy, dx, co), Cin]
  * (k*k*Cout rows).  alpha/bias are per output channel (Cout).
@@ -229,6 +239,8 @@ typedef struct {
 } pmx_conv_desc;
 
 size_t pmx_conv_workspace(const pmx_conv_desc* desc);
+/* 1 if pmx_conv runs desc on the tcgen05 tensor-core kernels (0: the SIMT kernel). */
+int32_t pmx_conv_tc_supported(const pmx_conv_desc* desc);
 
 /* bn_post (may be NULL): unfolded batch norm applied after the bias as
  * (y - mean[c]) * factor[c] + beta[c] in f32 (pm/model.py:252-258); device
@@ -297,6 +309,29 @@ pmx_status pmx_decode_topk(const pmx_anchor_desc* desc, int32_t batch, int32_t o
                            int32_t cls_off, int32_t box_off, int32_t dir_off, int32_t* topk_idx,
                            float* topk_logit, float* boxes, int32_t* dir_label, void* ws,
                            size_t ws_bytes, pmx_stream_t stream);
+
+/* ------------------------------------------------------------------------
+ * K11b local-peak decode + per-class greedy NMS -- replaces the reference's own
+ * decode entry point pm/detector.py:266-307 (decode_and_nms, with _sigmoid
+ * :251-252, _local_peaks :255-263, iou_matrix pm/metrics.py:52-66).  f64 scores
+ * sigmoid(logit), 3x3 local peaks (ties keep both, NaN never a peak), score >=
+ * score_thresh, box = ((j + .5 + dx) * cell_w, (i + .5 + dy) * cell_h,
+ * base * exp(clip(dw, +-4)), base * exp(clip(dh, +-4))), stable order by score
+ * descending, greedy suppression at IoU >= iou_thresh, classes independent.
+ * ---------------------------------------------------------------------- */
+typedef struct {
+  int32_t n_classes, out_h, out_w; /* class map [B, n_classes, out_h, out_w], out_h*out_w <= 16384 */
+  int32_t _pad;
+  double cell_w, cell_h;           /* field_size / out_w, field_size / out_h */
+  double base_size;
+  double score_thresh, iou_thresh; /* both in [0, 1] (PMX_ERR_INVALID otherwise, the reference's ValueError) */
+} pmx_nms_desc;
+
+/* cls: f32 NCHW [B, n_classes, H, W] logits; reg: f32 NCHW [B, 4, H, W] (dx, dy, dw, dh).
+ * dets: f64 [B, n_classes, H*W, 5] -- per (frame, class) the kept detections in the
+ * reference's order as (cx, cy, w, h, score); n_dets: int32 [B, n_classes]. */
+pmx_status pmx_decode_nms(const pmx_nms_desc* desc, int32_t batch, const float* cls, const float* reg,
+                          double* dets, int32_t* n_dets, pmx_stream_t stream);
 
 /* Fixed-size per-frame top-k records for the host / the NCCL gather:
  * records [B, k, 10] f32 = (idx, logit, box[7], dir) with idx and dir as f32

@@ -18,7 +18,7 @@ PKG = Path(__file__).resolve().parent
 LIB_PATH = Path(os.environ["PMX_LIB"]) if os.environ.get("PMX_LIB") else PKG / "libpmx.so"  # PMX_LIB: A/B builds
 
 PMX_OK, PMX_ERR_INVALID, PMX_ERR_CUDA, PMX_ERR_UNSUPPORTED = 0, 1, 2, 3
-PMX_F32, PMX_F16, PMX_I8, PMX_F64 = 0, 1, 2, 3
+PMX_F32, PMX_F16, PMX_I8, PMX_F64, PMX_F32X2 = 0, 1, 2, 3, 4
 PMX_CONV2D, PMX_DECONV2D = 0, 1
 PMX_PFN_FROM_POINTS9, PMX_PFN_FROM_FEATURES = 0, 1
 PMX_MAX_OUTS = 3
@@ -56,6 +56,12 @@ class AnchorDesc(C.Structure):
                 ("rotations", C.c_float * 4), ("dir_offset", C.c_float), ("_pad", C.c_float)]
 
 
+class NmsDesc(C.Structure):
+    _fields_ = [("n_classes", C.c_int32), ("out_h", C.c_int32), ("out_w", C.c_int32), ("_pad", C.c_int32),
+                ("cell_w", C.c_double), ("cell_h", C.c_double), ("base_size", C.c_double),
+                ("score_thresh", C.c_double), ("iou_thresh", C.c_double)]
+
+
 P = C.c_void_p
 I32, I64, F64, SZ = C.c_int32, C.c_int64, C.c_double, C.c_size_t
 
@@ -83,6 +89,7 @@ SIGNATURES = {
     "pmx_conv_gather_supported": (I32, [C.POINTER(ConvDesc)]),
     "pmx_conv_gather": (I32, [C.POINTER(ConvDesc), P, P, I32, P, P, P, P, C.POINTER(Out), I32, P, P]),
     "pmx_conv_workspace": (SZ, [C.POINTER(ConvDesc)]),
+    "pmx_conv_tc_supported": (I32, [C.POINTER(ConvDesc)]),
     "pmx_conv": (I32, [C.POINTER(ConvDesc), P, P, P, P, P, C.POINTER(Out), I32, P, P, SZ, P]),
     "pmx_set_conv_backend": (None, [I32]),
     "pmx_debug_trace": (None, [P]),
@@ -91,6 +98,7 @@ SIGNATURES = {
     "pmx_decode_workspace": (SZ, [C.POINTER(AnchorDesc), I32, I32, I32]),
     "pmx_decode_topk": (I32, [C.POINTER(AnchorDesc), I32, I32, I32, P, I32, I32, I32, I32, P, P, P, P, P, SZ,
                               P]),
+    "pmx_decode_nms": (I32, [C.POINTER(NmsDesc), I32, P, P, P, P, P]),
     "pmx_pack_topk_records": (I32, [I32, I32, P, P, P, P, P, P]),
     "pmx_zero": (I32, [P, SZ, P]),
     "pmx_sq_err_workspace": (SZ, []),

@@ -16,6 +16,7 @@ pmx_status conv_tc_try(const pmx_conv_desc& d, const void* x, const void* w, con
                        cudaStream_t st, bool* launched, const GatherIn* gin);
 size_t conv_tc_workspace(const pmx_conv_desc& d);
 bool conv_tc_gather_ok(const pmx_conv_desc& d);
+bool conv_tc_supported(const pmx_conv_desc& d);
 const char* conv_tc_backend(int dtype, int kind);
 
 // backend override of the CALLING thread (tests): thread-local, so concurrent callers on
@@ -50,6 +51,12 @@ __device__ __forceinline__ typename Acc<DT>::T load_x(const void* p, int64_t off
   else return reinterpret_cast<const float*>(p)[off];
 }
 
+// PMX_F32X2 activation: hi + lo reassembles the f32 value exactly
+__device__ __forceinline__ float load_x2(const void* p, int64_t off, int plane) {
+  const float* f = reinterpret_cast<const float*>(p);
+  return __fadd_rn(f[off], f[off + plane]);
+}
+
 template <int DT, bool DECONV>
 __global__ void __launch_bounds__(256) conv_simt_kernel(const ConvArgs a, const Outs outs) {
   using T = typename Acc<DT>::T;
@@ -75,7 +82,8 @@ __global__ void __launch_bounds__(256) conv_simt_kernel(const ConvArgs a, const 
       T v = T(0);
       if (m < a.M && k < a.K) {
         if (DECONV) {
-          v = load_x<DT>(a.x, m * d.in_c_stride + d.in_c_offset + k);
+          if constexpr (DT == PMX_F32X2) v = load_x2(a.x, m * d.in_c_stride + d.in_c_offset + k, d.in_c_stride / 2);
+          else v = load_x<DT>(a.x, m * d.in_c_stride + d.in_c_offset + k);
         } else {
           const int c = k % d.in_c;
           const int tap = k / d.in_c;
@@ -86,8 +94,11 @@ __global__ void __launch_bounds__(256) conv_simt_kernel(const ConvArgs a, const 
           const int64_t bb = t / d.out_h;
           const int iy = oy * d.stride_h - d.pad_h + ky;
           const int ix = ox * d.stride_w - d.pad_w + kx;
-          if (iy >= 0 && iy < d.in_h && ix >= 0 && ix < d.in_w)
-            v = load_x<DT>(a.x, ((bb * d.in_h + iy) * d.in_w + ix) * d.in_c_stride + d.in_c_offset + c);
+          if (iy >= 0 && iy < d.in_h && ix >= 0 && ix < d.in_w) {
+            const int64_t off = ((bb * d.in_h + iy) * d.in_w + ix) * d.in_c_stride + d.in_c_offset + c;
+            if constexpr (DT == PMX_F32X2) v = load_x2(a.x, off, d.in_c_stride / 2);
+            else v = load_x<DT>(a.x, off);
+          }
         }
       }
       As[kk][mm] = v;
@@ -96,7 +107,16 @@ __global__ void __launch_bounds__(256) conv_simt_kernel(const ConvArgs a, const 
       const int nn = e / BK, kk = e % BK;
       const int n = n0 + nn, k = k0 + kk;
       T v = T(0);
-      if (n < a.N && k < a.K) v = load_x<DT>(a.w, (int64_t)n * a.K + k);
+      if (n < a.N && k < a.K) {
+        if constexpr (DT == PMX_F32X2) {
+          // prepacked [w_hi | w_hi | w_lo] per tap: w = w_hi + w_lo exactly
+          const int tap = k / d.in_c, c = k - tap * d.in_c;
+          const float* w = reinterpret_cast<const float*>(a.w) + (int64_t)n * 3 * a.K + (int64_t)tap * 3 * d.in_c;
+          v = __fadd_rn(w[c], w[2 * d.in_c + c]);
+        } else {
+          v = load_x<DT>(a.w, (int64_t)n * a.K + k);
+        }
+      }
       Bs[kk][nn] = v;
     }
     __syncthreads();
@@ -166,9 +186,12 @@ void launch_simt(const ConvArgs& a, const Outs& o, cudaStream_t st) {
 
 pmx_status validate(const pmx_conv_desc& d) {
   PMX_REQUIRE(d.kind == PMX_CONV2D || d.kind == PMX_DECONV2D, "bad conv kind");
-  PMX_REQUIRE(d.in_dtype >= PMX_F32 && d.in_dtype <= PMX_I8, "bad conv dtype");
+  PMX_REQUIRE((d.in_dtype >= PMX_F32 && d.in_dtype <= PMX_I8) || d.in_dtype == PMX_F32X2, "bad conv dtype");
   PMX_REQUIRE(d.batch >= 0 && d.in_h >= 1 && d.in_w >= 1 && d.in_c >= 1 && d.out_c >= 1, "bad conv extents");
-  PMX_REQUIRE(d.in_c_offset >= 0 && d.in_c_offset + d.in_c <= d.in_c_stride, "input channel slice exceeds stride");
+  PMX_REQUIRE(d.in_dtype != PMX_F32X2 || d.in_c_stride % 2 == 0, "f32x2 input needs an even in_c_stride");
+  PMX_REQUIRE(d.in_c_offset >= 0 &&
+                  d.in_c_offset + d.in_c <= (d.in_dtype == PMX_F32X2 ? d.in_c_stride / 2 : d.in_c_stride),
+              "input channel slice exceeds stride");
   PMX_REQUIRE(d.k_h >= 1 && d.k_w >= 1 && d.stride_h >= 1 && d.stride_w >= 1 && d.pad_h >= 0 && d.pad_w >= 0,
               "bad kernel/stride/padding");
   if (d.kind == PMX_CONV2D) {
@@ -195,6 +218,11 @@ void pmx_set_conv_backend(int32_t mode) { g_conv_backend_mode = mode; }
 const char* pmx_conv_backend(int32_t in_dtype, int32_t kind) {
   if (g_conv_backend_mode == 1) return "simt";
   return conv_tc_backend(in_dtype, kind);
+}
+
+int32_t pmx_conv_tc_supported(const pmx_conv_desc* desc) {
+  if (!desc || validate(*desc) != PMX_OK) return 0;
+  return conv_tc_supported(*desc) ? 1 : 0;
 }
 
 size_t pmx_conv_workspace(const pmx_conv_desc* desc) {
@@ -239,6 +267,7 @@ pmx_status pmx_conv(const pmx_conv_desc* desc, const void* x, const void* w, con
   }
   if (d.in_dtype == PMX_I8) launch_simt<PMX_I8>(a, o, stream);
   else if (d.in_dtype == PMX_F16) launch_simt<PMX_F16>(a, o, stream);
+  else if (d.in_dtype == PMX_F32X2) launch_simt<PMX_F32X2>(a, o, stream);
   else launch_simt<PMX_F32>(a, o, stream);
   return check_launch("pmx_conv(simt)");
 }

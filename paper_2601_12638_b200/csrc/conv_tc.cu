@@ -110,6 +110,12 @@ __device__ __forceinline__ void tc_mma(uint32_t d, uint64_t a, uint64_t b, uint3
         "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
         "l"(a), "l"(b), "r"(idesc), "r"(acc)
         : "memory");
+  } else if constexpr (DT == PMX_F32X2) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc)
+        : "memory");
   } else {
     asm volatile(
         "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
@@ -191,6 +197,10 @@ struct TcParams {
   int64_t m_total;  // GEMM mode: number of rows (input pixels)
   int n_gemm;       // GEMM N (deconv: k*k*Cout)
   int kc;           // channels per K-block
+  // PMX_F32X2 (3xTF32): the K-blocks of a tap run over three segments of seg_n blocks --
+  // hi x w_hi, lo x w_hi, hi x w_lo; A channel of block cb = a_off (+ a_lo in segment 1)
+  // + (cb mod seg_n) * kc, the map spanning both planes of the pixel.  seg_n = 0: plain.
+  int seg_n, a_off, a_lo;
   int cblocks;      // K-blocks per tap
   int taps;         // 9 or 1
   int bn;           // N tile
@@ -402,6 +412,8 @@ __device__ __forceinline__ void epi_chunk(const TcParams& p, const Outs& outs, c
         float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(od.ptr) + off);
 #pragma unroll
         for (int qq = 0; qq < 4; ++qq) dst[qq] = make_float4(y[4 * qq], y[4 * qq + 1], y[4 * qq + 2], y[4 * qq + 3]);
+      } else if (full16 && od.dtype == PMX_F32X2 && (off & 3) == 0 && (od.c_stride & 7) == 0) {
+        store16_f32x2(od, off, y);
       } else {
         for (int j = 0; j < 16; ++j)
           if (nbase + j < p.n_gemm) store_one(od, pix, cobase + j, y[j]);
@@ -683,18 +695,23 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
           mbar_expect_tx(full(s), p.a_bytes + p.b_bytes);
           const int tap = kb / p.cblocks, cb = kb % p.cblocks;
           const int c0 = cb * p.kc;
+          int ac = c0;  // A channel coordinate
+          if (p.seg_n) {
+            const int seg = cb / p.seg_n;
+            ac = p.a_off + (seg == 1 ? p.a_lo : 0) + (cb - seg * p.seg_n) * p.kc;
+          }
           const uint32_t adst = a_smem + s * p.a_bytes, bdst = b_smem + s * p.b_bytes;
           if (p.mode == MODE_CONV3) {
             const int dy = tap / 3 - 1, dx = tap % 3 - 1;
             if (p.stride == 1) {
-              tma_load_4d(adst, &maps.a[0], c0, ox0 + dx, oy0 + dy, tb, full(s));
+              tma_load_4d(adst, &maps.a[0], ac, ox0 + dx, oy0 + dy, tb, full(s));
             } else {  // 2*o + d = 2*(o + a) + par
               const int ay = dy < 0 ? -1 : 0, py = dy == 0 ? 0 : 1;
               const int ax = dx < 0 ? -1 : 0, px = dx == 0 ? 0 : 1;
-              tma_load_4d(adst, &maps.a[py * 2 + px], c0, ox0 + ax, oy0 + ay, tb, full(s));
+              tma_load_4d(adst, &maps.a[py * 2 + px], ac, ox0 + ax, oy0 + ay, tb, full(s));
             }
           } else {
-            tma_load_2d(adst, &maps.a[0], c0, m0, full(s));
+            tma_load_2d(adst, &maps.a[0], ac, m0, full(s));
           }
           tma_load_2d(bdst, &maps.b, tap * (p.cblocks * p.kc) + c0, n0, full(s));
           if (++s == (uint32_t)p.stages) s = 0, ph ^= 1;
@@ -1272,8 +1289,10 @@ Plan plan_for(const pmx_conv_desc& d, bool gather = false, bool want_stage = fal
               bool want_stage2 = false) {
   Plan pl{};
   pl.ok = false;
-  if (d.in_dtype != PMX_I8 && d.in_dtype != PMX_F16) return pl;
-  const int esz = d.in_dtype == PMX_I8 ? 1 : 2;
+  if (d.in_dtype != PMX_I8 && d.in_dtype != PMX_F16 && d.in_dtype != PMX_F32X2) return pl;
+  const bool x3 = d.in_dtype == PMX_F32X2;
+  if (x3 && (gather || d.in_c % 32 != 0 || d.in_c_stride % 2 != 0)) return pl;
+  const int esz = d.in_dtype == PMX_I8 ? 1 : (x3 ? 4 : 2);
   TcParams& p = pl.p;
   p.deconv = d.kind == PMX_DECONV2D;
   const bool conv3 = d.kind == PMX_CONV2D && d.k_h == 3 && d.k_w == 3 && d.pad_h == 1 && d.pad_w == 1 &&
@@ -1281,15 +1300,19 @@ Plan plan_for(const pmx_conv_desc& d, bool gather = false, bool want_stage = fal
   const bool conv1 = d.kind == PMX_CONV2D && d.k_h == 1 && d.k_w == 1 && d.stride_h == 1 && d.stride_w == 1 &&
                      d.pad_h == 0 && d.pad_w == 0;
   if (!(conv3 || conv1 || p.deconv)) return pl;
-  // K-block = 128 bytes of channels (SW128) or 64 bytes (SW64)
-  const int cin_bytes = d.in_c * esz;
+  // K-block = 128 bytes of channels (SW128) or 64 bytes (SW64); 3xTF32 runs 3 * Cin
+  // "channels" per tap (the hi / lo / hi segments)
+  const int cin_bytes = (x3 ? 3 : 1) * d.in_c * esz;
   int kc_bytes;
   if (cin_bytes % 128 == 0) kc_bytes = 128;
   else if (cin_bytes == 64) kc_bytes = 64;
   else return pl;
   if ((d.in_c_stride * esz) % 16 != 0 || (d.in_c_offset * esz) % 16 != 0) return pl;
   p.kc = kc_bytes / esz;
-  p.cblocks = d.in_c / p.kc;
+  p.cblocks = (x3 ? 3 : 1) * d.in_c / p.kc;
+  p.seg_n = x3 ? d.in_c / p.kc : 0;
+  p.a_off = x3 ? d.in_c_offset : 0;
+  p.a_lo = x3 ? d.in_c_stride / 2 : 0;
   p.layout = kc_bytes == 128 ? 2u : 4u;
   p.sbo = 8u * kc_bytes;
   p.batch = d.batch;
@@ -1370,7 +1393,7 @@ Plan plan_for(const pmx_conv_desc& d, bool gather = false, bool want_stage = fal
   if (stages < 2) stages = 2;
   p.stages = stages;
   p.bres_bytes = 0;
-  if (conv3 && g_conv_backend_mode != 2 && cin_bytes == kc_bytes && p.n_tiles == 1 && d.out_w >= 8) {
+  if (conv3 && !x3 && g_conv_backend_mode != 2 && cin_bytes == kc_bytes && p.n_tiles == 1 && d.out_w >= 8) {
     // stride 1: one (16 + 2) x (8 + 2) halo; stride 2: four parity planes of
     // (16 + py) x (8 + px) pixels (561 in total) -- see the producer
     // stride 1, 64 / 128 channel bytes: swizzled pixel-major halo 16 x 18 (PMX_HALO_SWZ=0: off)
@@ -1439,6 +1462,8 @@ Plan plan_for(const pmx_conv_desc& d, bool gather = false, bool want_stage = fal
   const uint32_t m_enc = 128u >> 4, n_enc = (uint32_t)bn >> 3;
   if (d.in_dtype == PMX_I8)
     p.idesc = (2u << 4) | (1u << 7) | (1u << 10) | (n_enc << 17) | (m_enc << 24);
+  else if (x3)  // f32 <- tf32 x tf32
+    p.idesc = (1u << 4) | (2u << 7) | (2u << 10) | (n_enc << 17) | (m_enc << 24);
   else
     p.idesc = (1u << 4) | (0u << 7) | (0u << 10) | (n_enc << 17) | (m_enc << 24);
   pl.smem = 1024 + (size_t)p.stages * (p.a_bytes + p.b_bytes) + p.bres_bytes + (2 * p.stages + 2 * p.nacc + 1) * 8 + 32 +
@@ -1449,10 +1474,15 @@ Plan plan_for(const pmx_conv_desc& d, bool gather = false, bool want_stage = fal
 
 pmx_status build_maps(const pmx_conv_desc& d, const Plan& pl, const void* x, const void* w, TcMaps* maps) {
   const TcParams& p = pl.p;
-  const int esz = d.in_dtype == PMX_I8 ? 1 : 2;
-  const CUtensorMapDataType dt = d.in_dtype == PMX_I8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+  const bool x3 = d.in_dtype == PMX_F32X2;
+  const int esz = d.in_dtype == PMX_I8 ? 1 : (x3 ? 4 : 2);
+  const CUtensorMapDataType dt = d.in_dtype == PMX_I8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8
+                                 : (x3 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16);
   const CUtensorMapSwizzle sw = p.layout == 2u ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
-  const char* xb = static_cast<const char*>(x) + (size_t)d.in_c_offset * esz;
+  // 3xTF32: the A map spans the whole pixel (both planes); the producer's channel
+  // coordinate carries the offsets
+  const char* xb = static_cast<const char*>(x) + (x3 ? 0 : (size_t)d.in_c_offset * esz);
+  const cuuint64_t a_ch = x3 ? (cuuint64_t)d.in_c_stride : (cuuint64_t)d.in_c;
   const cuuint64_t cs = (cuuint64_t)d.in_c_stride * esz;
   pmx_status st;
   if (x == nullptr) {
@@ -1490,7 +1520,7 @@ pmx_status build_maps(const pmx_conv_desc& d, const Plan& pl, const void* x, con
     if (st != PMX_OK) return st;
   } else if (p.mode == MODE_CONV3) {
     if (p.stride == 1) {
-      cuuint64_t dims[4] = {(cuuint64_t)d.in_c, (cuuint64_t)d.in_w, (cuuint64_t)d.in_h, (cuuint64_t)d.batch};
+      cuuint64_t dims[4] = {a_ch, (cuuint64_t)d.in_w, (cuuint64_t)d.in_h, (cuuint64_t)d.batch};
       cuuint64_t str[3] = {cs, cs * d.in_w, cs * d.in_w * d.in_h};
       cuuint32_t box[4] = {(cuuint32_t)p.kc, (cuuint32_t)p.tw, (cuuint32_t)p.th, 1};
       st = encode(&maps->a[0], dt, 4, xb, dims, str, box, sw);
@@ -1498,8 +1528,7 @@ pmx_status build_maps(const pmx_conv_desc& d, const Plan& pl, const void* x, con
     } else {
       for (int py = 0; py < 2; ++py)
         for (int px = 0; px < 2; ++px) {
-          cuuint64_t dims[4] = {(cuuint64_t)d.in_c, (cuuint64_t)(d.in_w / 2), (cuuint64_t)(d.in_h / 2),
-                                (cuuint64_t)d.batch};
+          cuuint64_t dims[4] = {a_ch, (cuuint64_t)(d.in_w / 2), (cuuint64_t)(d.in_h / 2), (cuuint64_t)d.batch};
           cuuint64_t str[3] = {2 * cs, 2 * cs * d.in_w, cs * d.in_w * d.in_h};
           cuuint32_t box[4] = {(cuuint32_t)p.kc, (cuuint32_t)p.tw, (cuuint32_t)p.th, 1};
           const char* basep = xb + (size_t)(py * d.in_w + px) * cs;
@@ -1508,13 +1537,13 @@ pmx_status build_maps(const pmx_conv_desc& d, const Plan& pl, const void* x, con
         }
     }
   } else {
-    cuuint64_t dims[2] = {(cuuint64_t)d.in_c, (cuuint64_t)p.m_total};
+    cuuint64_t dims[2] = {a_ch, (cuuint64_t)p.m_total};
     cuuint64_t str[1] = {cs};
     cuuint32_t box[2] = {(cuuint32_t)p.kc, 128};
     st = encode(&maps->a[0], dt, 2, xb, dims, str, box, sw);
     if (st != PMX_OK) return st;
   }
-  const int K = p.taps * d.in_c;
+  const int K = p.taps * p.cblocks * p.kc;  // 3xTF32: taps * 3 * Cin
   cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)p.n_gemm};
   cuuint64_t str[1] = {(cuuint64_t)K * esz};
   cuuint32_t box[2] = {(cuuint32_t)p.kc, (cuuint32_t)p.bn};
@@ -1525,7 +1554,12 @@ pmx_status build_maps(const pmx_conv_desc& d, const Plan& pl, const void* x, con
 
 const char* conv_tc_backend(int dtype, int) {
   if (g_conv_backend_mode == 1) return "simt";  // 2 = tcgen05 without the halo variant (tests)
-  return (dtype == PMX_I8 || dtype == PMX_F16) ? "tcgen05" : "simt";
+  return (dtype == PMX_I8 || dtype == PMX_F16 || dtype == PMX_F32X2) ? "tcgen05" : "simt";
+}
+
+bool conv_tc_supported(const pmx_conv_desc& d) {
+  if (g_conv_backend_mode == 1) return false;
+  return plan_for(d).ok;
 }
 
 size_t conv_tc_workspace(const pmx_conv_desc&) { return 0; }
@@ -1612,6 +1646,8 @@ pmx_status conv_tc_try(const pmx_conv_desc& d, const void* x, const void* w, con
   else { PMX_TC_LAUNCH_NG(DTV, 128); }
   if (d.in_dtype == PMX_I8) {
     PMX_TC_SHAPES(PMX_I8)
+  } else if (d.in_dtype == PMX_F32X2) {
+    PMX_TC_LAUNCH_NG(PMX_F32X2, 128);  // 3xTF32: TMA per K-block (no halo variants)
   } else {
     PMX_TC_SHAPES(PMX_F16)
   }

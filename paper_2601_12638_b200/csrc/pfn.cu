@@ -272,6 +272,32 @@ __global__ void __launch_bounds__(kThreads, 2) pfn_points_kernel(const PfnArgs a
   }
   const float INF = __int_as_float(0x7f800000);
   const float4* fp = a.points + a.offs[b];
+#ifdef PMX_DEBUG_BOUNDS
+  const int64_t n_frame = a.offs[b + 1] - a.offs[b];
+#define PMX_CHK(cond, what, v)                                                                                \
+  do {                                                                                                        \
+    if (!(cond)) {                                                                                            \
+      printf("pfn check failed: %s value %lld b %d block %d thread %d line %d\n", what, (long long)(v), b,     \
+             blockIdx.x, threadIdx.x, __LINE__);                                                              \
+      __trap();                                                                                               \
+    }                                                                                                         \
+  } while (0)
+  PMX_CHK(P >= 0 && P <= a.pcap, "n_pillars", P);
+#define PMX_PT(i_)                                                                                            \
+  ([&](int i__) {                                                                                             \
+    if (i__ < 0 || i__ >= n_frame) {                                                                          \
+      printf("pfn: point index %d out of [0, %lld) b %d block %d thread %d line %d\n", i__, (long long)n_frame, b, \
+             blockIdx.x, threadIdx.x, __LINE__);                                                              \
+      __trap();                                                                                               \
+    }                                                                                                         \
+    return i__;                                                                                               \
+  }(i_))
+#else
+#define PMX_PT(i_) (i_)
+#define PMX_CHK(cond, what, v) \
+  do {                         \
+  } while (0)
+#endif
   const float xoff = (float)((double)a.g.cell_w * 0.5 + (double)a.g.x_min);
   const float yoff = (float)((double)a.g.cell_h * 0.5 + (double)a.g.y_min);
   // ---------------- phase A: lane = pillar
@@ -280,13 +306,14 @@ __global__ void __launch_bounds__(kThreads, 2) pfn_points_kernel(const PfnArgs a
   const int64_t q = (int64_t)b * a.pcap + (live ? p : 0);
   const int k = live ? a.counts[q] : 0;
   const int32_t* idx = a.pt_idx + q * M;
+  PMX_CHK(k >= 0 && k <= M, "count", k);
   float in_lo = INF, in_hi = -INF;
   float4 pts[kSlots];
 #pragma unroll
   for (int s = 0; s < kSlots; ++s) pts[s] = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
   for (int s = 0; s < kSlots; ++s)
-    if (s < k) pts[s] = __ldg(fp + __ldg(idx + s));
+    if (s < k) pts[s] = __ldg(fp + PMX_PT(__ldg(idx + s)));
   float sx = 0.f, sy = 0.f, sz = 0.f;
 #pragma unroll
   for (int s = 0; s < kSlots; ++s)
@@ -296,7 +323,7 @@ __global__ void __launch_bounds__(kThreads, 2) pfn_points_kernel(const PfnArgs a
       sz = __fadd_rn(sz, pts[s].z);
     }
   for (int s = kSlots; s < k; ++s) {  // dense cluster tail, still in slot order
-    const float4 pt = __ldg(fp + __ldg(idx + s));
+    const float4 pt = __ldg(fp + PMX_PT(__ldg(idx + s)));
     sx = __fadd_rn(sx, pt.x);
     sy = __fadd_rn(sy, pt.y);
     sz = __fadd_rn(sz, pt.z);
@@ -310,6 +337,7 @@ __global__ void __launch_bounds__(kThreads, 2) pfn_points_kernel(const PfnArgs a
     xc = __fadd_rn(__fmul_rn((float)cc.y, a.g.cell_w), xoff);
     yc = __fadd_rn(__fmul_rn((float)cc.x, a.g.cell_h), yoff);
     if (!a.dense) mypix = ((int64_t)b * a.g.grid_h + cc.x) * a.g.grid_w + cc.y;
+    PMX_CHK(cc.x >= 0 && cc.x < a.g.grid_h && cc.y >= 0 && cc.y < a.g.grid_w, "coords", cc.x * 100000 + cc.y);
   }
   if (live && k < M) { in_lo = 0.f; in_hi = 0.f; }  // zero padding rows are part of layer 1's input
   auto feats = [&](const float4& pt, float (&f)[9]) {
@@ -341,7 +369,7 @@ __global__ void __launch_bounds__(kThreads, 2) pfn_points_kernel(const PfnArgs a
     if (a.in_keys) {
       for (int s = kSlots; s < k; ++s) {
         float f[9];
-        feats(__ldg(fp + __ldg(idx + s)), f);
+        feats(__ldg(fp + PMX_PT(__ldg(idx + s))), f);
 #pragma unroll
         for (int j = 0; j < 9; ++j) { in_lo = nmin(in_lo, f[j]); in_hi = nmax(in_hi, f[j]); }
       }
@@ -421,7 +449,7 @@ __global__ void __launch_bounds__(kThreads, 2) pfn_points_kernel(const PfnArgs a
       const int32_t* idj = a.pt_idx + qj * M;
       for (int s2 = kSlots; s2 < kpair; ++s2) {
         if (s2 >= kj) continue;
-        const float4 pt = __ldg(fp + __ldg(idj + s2));
+        const float4 pt = __ldg(fp + PMX_PT(__ldg(idj + s2)));
         float f[9];
         f[0] = pt.x; f[1] = pt.y; f[2] = pt.z; f[3] = pt.w;
         f[4] = __fsub_rn(pt.x, mt[0]); f[5] = __fsub_rn(pt.y, mt[1]); f[6] = __fsub_rn(pt.z, mt[2]);
@@ -431,6 +459,9 @@ __global__ void __launch_bounds__(kThreads, 2) pfn_points_kernel(const PfnArgs a
         point(f);
       }
     }
+    // every lane takes part in the shuffle (the halves' pillars may differ in liveness:
+    // a shuffle after the divergent `continue` below is undefined and returned garbage)
+    const int64_t pix = __shfl_sync(0xffffffffu, mypix, j);
     if (kj == 0 || c >= C) continue;
     float y[4];
 #pragma unroll
@@ -442,8 +473,8 @@ __global__ void __launch_bounds__(kThreads, 2) pfn_points_kernel(const PfnArgs a
         if (a.d.relu) y[u] = fmaxf(y[u], 0.f);
       }
     }
-    const int64_t pix = __shfl_sync(0xffffffffu, mypix, j);
     const int nl = C - c < 4 ? C - c : 4;
+    PMX_CHK(pix >= 0 && pix < (a.dense ? (int64_t)gridDim.y * a.pcap : (int64_t)gridDim.y * hw), "pix", pix);
     if (f16_only && nl == 4) {
       // the common single binary16 consumer (next layer FP16): one 8-byte store
       *reinterpret_cast<uint2*>(reinterpret_cast<__half*>(outs.o[0].ptr) + pix * outs.o[0].c_stride +

@@ -33,7 +33,7 @@ pmx_status check_launch(const char* what);
       return ::pmx::fail(PMX_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
   } while (0)
 
-inline int elem_size(int dtype) { return dtype == PMX_F32 ? 4 : (dtype == PMX_F16 ? 2 : 1); }
+inline int elem_size(int dtype) { return (dtype == PMX_F32 || dtype == PMX_F32X2) ? 4 : (dtype == PMX_F16 ? 2 : 1); }
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 // SM count of the current device (queried once per device, cached): persistent grids
 // are sized from it, never from a compile-time constant (other SKUs, MIG slices)
@@ -214,10 +214,27 @@ __host__ inline Outs make_outs(const pmx_out* outs, int n) {
   return r;
 }
 
+// TF32 split of an f32 value (PMX_F32X2): hi = round-to-nearest-even to 10 mantissa
+// bits, lo = y - hi exactly (|lo| <= 2^-11 |y|); Inf / NaN pass through in hi
+__device__ __forceinline__ float tf32_hi(float y) {
+  const uint32_t b = __float_as_uint(y);
+  if ((b & 0x7f800000u) == 0x7f800000u) return y;
+  return __uint_as_float((b + 0x0fffu + ((b >> 13) & 1u)) & 0xffffe000u);
+}
+__device__ __forceinline__ float2 tf32_split(float y) {
+  const float hi = tf32_hi(y);
+  const bool fin = (__float_as_uint(y) & 0x7f800000u) != 0x7f800000u;
+  return make_float2(hi, fin ? __fsub_rn(y, hi) : 0.0f);
+}
+
 __device__ __forceinline__ void store_one(const OutDev& o, int64_t pix, int c, float y) {
   int64_t off = pix * o.c_stride + o.c_offset + c;
   if (o.dtype == PMX_F32) {
     reinterpret_cast<float*>(o.ptr)[off] = y;
+  } else if (o.dtype == PMX_F32X2) {
+    const float2 h = tf32_split(y);
+    reinterpret_cast<float*>(o.ptr)[off] = h.x;
+    reinterpret_cast<float*>(o.ptr)[off + (o.c_stride >> 1)] = h.y;
   } else if (o.dtype == PMX_F16) {
     reinterpret_cast<__half*>(o.ptr)[off] = f16_sat(y);
   } else {
@@ -287,6 +304,19 @@ __device__ __forceinline__ uint32_t f16x2_sat(float lo_v, float hi_v) {
   return r;
 }
 
+// 16 channels of one pixel as (hi, lo) planes: 4 + 4 float4 stores
+__device__ __forceinline__ void store16_f32x2(const OutDev& od, int64_t off, const float (&y)[16]) {
+  float4* hi = reinterpret_cast<float4*>(reinterpret_cast<float*>(od.ptr) + off);
+  float4* lo = reinterpret_cast<float4*>(reinterpret_cast<float*>(od.ptr) + off + (od.c_stride >> 1));
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const float2 a = tf32_split(y[4 * q]), b = tf32_split(y[4 * q + 1]), c = tf32_split(y[4 * q + 2]),
+                 d = tf32_split(y[4 * q + 3]);
+    hi[q] = make_float4(a.x, b.x, c.x, d.x);
+    lo[q] = make_float4(a.y, b.y, c.y, d.y);
+  }
+}
+
 // 16 consecutive channels of one pixel -> one consumer format (vectorised when the
 // run is complete and aligned, element-wise otherwise)
 __device__ __forceinline__ void store16(const OutDev& od, int64_t pix, int c0, const float (&y)[16], int n_live) {
@@ -302,6 +332,8 @@ __device__ __forceinline__ void store16(const OutDev& od, int64_t pix, int c0, c
     float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(od.ptr) + off);
 #pragma unroll
     for (int q = 0; q < 4; ++q) dst[q] = make_float4(y[4 * q], y[4 * q + 1], y[4 * q + 2], y[4 * q + 3]);
+  } else if (n_live == 16 && od.dtype == PMX_F32X2 && (off & 3) == 0 && (od.c_stride & 7) == 0) {
+    store16_f32x2(od, off, y);
   } else {
     for (int j = 0; j < n_live; ++j) store_one(od, pix, c0 + j, y[j]);
   }

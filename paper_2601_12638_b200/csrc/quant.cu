@@ -38,8 +38,12 @@ pmx_status validate_outs(const pmx_out* outs, int n, int c_needed) {
   if (n < 1 || n > PMX_MAX_OUTS) return fail(PMX_ERR_INVALID, "n_outs must be 1..3");
   for (int i = 0; i < n; ++i) {
     if (!outs[i].ptr) return fail(PMX_ERR_INVALID, "output pointer is NULL");
-    if (outs[i].dtype < PMX_F32 || outs[i].dtype > PMX_I8) return fail(PMX_ERR_INVALID, "bad output dtype");
-    if (outs[i].c_offset < 0 || outs[i].c_offset + c_needed > outs[i].c_stride)
+    const int dt = outs[i].dtype;
+    if (!(dt == PMX_F32 || dt == PMX_F16 || dt == PMX_I8 || dt == PMX_F32X2))
+      return fail(PMX_ERR_INVALID, "bad output dtype");
+    const int plane = dt == PMX_F32X2 ? outs[i].c_stride / 2 : outs[i].c_stride;
+    if (dt == PMX_F32X2 && (outs[i].c_stride & 1)) return fail(PMX_ERR_INVALID, "f32x2 output needs an even c_stride");
+    if (outs[i].c_offset < 0 || outs[i].c_offset + c_needed > plane)
       return fail(PMX_ERR_INVALID, "output channel slice exceeds c_stride");
     if (outs[i].dtype == PMX_I8 && !(outs[i].scale > 0.0))
       return fail(PMX_ERR_INVALID, "int8 output needs a positive scale");

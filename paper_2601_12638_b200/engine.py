@@ -106,7 +106,27 @@ def _fmt_of(layer, stats) -> tuple:
 
 
 _F32 = ("fp32", None)
-_DT = {"fp32": N.PMX_F32, "fp16": N.PMX_F16, "int8": N.PMX_I8}
+# "fp32x2": an FP32 layer's input stored as TF32 (hi, lo) planes for the 3xTF32
+# tensor-core kernel (include/pmx.h PMX_F32X2); hi + lo is the f32 value exactly
+_DT = {"fp32": N.PMX_F32, "fp16": N.PMX_F16, "int8": N.PMX_I8, "fp32x2": N.PMX_F32X2}
+_ESZ = {"fp32": 4, "fp16": 2, "int8": 1, "fp32x2": 8}  # bytes per channel (both planes for fp32x2)
+
+
+def _cstride(c: int, fmt) -> int:
+    """Elements per pixel of a tensor with c channels in format fmt."""
+    return 2 * c if fmt[0] == "fp32x2" else c
+
+
+def tf32_split(w: np.ndarray):
+    """(hi, lo) with hi = w rounded to TF32 (nearest even), lo = w - hi exactly -- the
+    host twin of tf32_split in csrc/pmx_common.cuh (weights are split once, here)."""
+    w = np.ascontiguousarray(w, np.float32)
+    b = w.view(np.uint32).astype(np.uint64)
+    finite = (b & 0x7F800000) != 0x7F800000
+    hb = np.where(finite, (b + 0x0FFF + ((b >> 13) & 1)) & 0xFFFFE000, b).astype(np.uint32)
+    hi = hb.view(np.float32)
+    lo = np.where(finite, w - hi, np.float32(0)).astype(np.float32)
+    return hi, lo
 
 
 class CompiledGraph:
@@ -149,6 +169,7 @@ class CompiledGraph:
                 _fmt_of(l, stats)
         self._resolve_sources(in_shape, pcap, n_features, max_points_per_frame)
         self._shapes()
+        self._choose_x3()
         self._needs()
         self.gather = self._gather_plan()
         self._allocate()
@@ -250,6 +271,38 @@ class CompiledGraph:
                 raise ValueError(f"unknown kind {l.kind!r}")
             vals[l.name] = out
 
+    def _choose_x3(self):
+        """FP32 layers the 3xTF32 tensor-core kernel runs (their inputs are stored as
+        fp32x2); the others keep f32 inputs and the SIMT kernel."""
+        self.x3 = set()
+        for l in self.graph.layers:
+            if not l.is_weight_layer or l is self.pfn or l.name not in self.layer_src or _prec(l) != "fp32":
+                continue
+            src = self.values[self.layer_src[l.name][0]]
+            B, H, W, C = src.shape
+            _, Ho, Wo, Co = self.values[l.name].shape
+            if l.kind == "linear":
+                if src.logical is not None and src.logical != "pfn":
+                    continue
+                kind, kh, kw, sh, sw, ph, pw = N.PMX_CONV2D, 1, 1, 1, 1, 0, 0
+            elif l.kind == "conv2d":
+                kind = N.PMX_CONV2D
+                kh, kw = l.weight.shape[2:]
+                (sh, sw), (ph, pw) = l.conv.stride, l.conv.padding
+            else:
+                kind = N.PMX_DECONV2D
+                kh, kw = l.weight.shape[2:]
+                sh, sw, ph, pw = kh, kw, 0, 0
+            d = N.ConvDesc(kind=kind, in_dtype=N.PMX_F32X2, batch=B, in_h=H, in_w=W, in_c=C, in_c_stride=2 * C,
+                           in_c_offset=0, out_c=Co, k_h=kh, k_w=kw, stride_h=sh, stride_w=sw, pad_h=ph, pad_w=pw,
+                           out_h=Ho, out_w=Wo, relu=int(l.relu))
+            if self.lib.pmx_conv_tc_supported(ctypes.byref(d)):
+                self.x3.add(l.name)
+
+    def _fmt(self, layer) -> tuple:
+        f = _fmt_of(layer, self.stats)
+        return ("fp32x2", None) if f[0] == "fp32" and layer.name in self.x3 else f
+
     def _consumers(self):
         cons: dict[str, list] = {}
         for l in self.graph.layers:
@@ -271,7 +324,7 @@ class CompiledGraph:
                 v.need[_F32] = None
             for c in cons.get(name, []):
                 if c.is_weight_layer:
-                    v.need[_fmt_of(c, self.stats)] = None
+                    v.need[self._fmt(c)] = None
                     if self.keep_inputs_f32:
                         v.need[_F32] = None
                 else:
@@ -327,7 +380,7 @@ class CompiledGraph:
         if len(cons) != 1 or cons[0].kind != "conv2d" or len(canvas.need) != 1:
             return None
         fmt = next(iter(canvas.need))
-        if fmt[0] not in ("int8", "fp16") or _fmt_of(cons[0], self.stats) != fmt:
+        if fmt[0] not in ("int8", "fp16") or self._fmt(cons[0]) != fmt:
             return None
         C = canvas.shape[3]
         d = self._first_conv_desc(cons[0], canvas, C, 0, fmt)
@@ -345,7 +398,8 @@ class CompiledGraph:
 
     def _empty(self, shape, fmt):
         torch = self.torch
-        dt = {"fp32": torch.float32, "fp16": torch.float16, "int8": torch.int8}[fmt[0]]
+        dt = {"fp32": torch.float32, "fp16": torch.float16, "int8": torch.int8, "fp32x2": torch.float32}[fmt[0]]
+        shape = tuple(shape[:-1]) + (_cstride(shape[-1], fmt),)
         return torch.empty(shape, dtype=dt, device="cuda")
 
     def _allocate(self):
@@ -387,7 +441,7 @@ class CompiledGraph:
                 continue
             for f in v.need:
                 if f not in v.bufs:
-                    v.bufs[f] = (self._empty(v.shape, f), v.shape[3], 0)
+                    v.bufs[f] = (self._empty(v.shape, f), _cstride(v.shape[3], f), 0)
         for name, v in self.values.items():
             if v.alias is not None:
                 cv, off = v.alias
@@ -466,6 +520,14 @@ class CompiledGraph:
                 rec["alpha"] = torch.from_numpy((act * ws).astype(np.float32)).cuda()
             elif p == "fp16":
                 rec["w"] = to_fp16_bits(w2)
+            elif l.name in self.x3:
+                # 3xTF32 prepack: per tap [w_hi | w_hi | w_lo] (include/pmx.h PMX_F32X2)
+                cin = l.weight.shape[1]
+                wt = w2.reshape(w2.shape[0], -1, cin)
+                hi, lo = tf32_split(wt)
+                rec["w"] = torch.from_numpy(np.ascontiguousarray(
+                    np.concatenate([hi, hi, lo], axis=2).reshape(w2.shape[0], -1))).cuda()
+                rec["precision"] = "fp32x2"
             else:
                 rec["w"] = torch.from_numpy(w2).cuda()
             rec["bias"] = torch.from_numpy(np.ascontiguousarray(l.bias, np.float32)).cuda()
@@ -536,7 +598,7 @@ class CompiledGraph:
         by_name = {l.name: l for l in self.graph.layers}
         hs = [by_name[n] for n in (a.cls_head, a.box_head, a.dir_head)]
         src = {tuple(self.layer_src[h.name]) for h in hs}
-        fmts = {_fmt_of(h, self.stats) for h in hs}
+        fmts = {self._fmt(h) for h in hs}
         ok = (len(src) == 1 and len(fmts) == 1 and all(
             h.kind == "conv2d" and h.weight.shape[2:] == (1, 1) and tuple(h.conv.stride) == (1, 1)
             and tuple(h.conv.padding) == (0, 0) and h.bn is None and not h.relu for h in hs))
@@ -565,7 +627,7 @@ class CompiledGraph:
         arr, n = N.outs_array([N.Out(ptr=self.heads_cat.data_ptr(), scale=0.0, dtype=N.PMX_F32, c_stride=ctot,
                                      c_offset=0)])
         self._keep.append(arr)
-        esz = {"fp32": 4, "fp16": 2, "int8": 1}[recs[0]["precision"]]
+        esz = _ESZ[recs[0]["precision"]]
         self.op_info["conv heads(fused)"] = {"flops": 2.0 * B * H * W * ctot * C, "precision": recs[0]["precision"],
                                               "bytes": B * H * W * C * esz + ctot * C * esz + B * H * W * ctot * 4}
         self.ops.append(("conv heads(fused)", lambda s: N.check(lib.pmx_conv(
@@ -621,7 +683,7 @@ class CompiledGraph:
 
     def _src_buf(self, l):
         src = self.values[self.layer_src[l.name][0]]
-        f = _fmt_of(l, self.stats)
+        f = self._fmt(l)
         t, cs, off = src.bufs[f]
         return src, t, cs, off
 
@@ -652,11 +714,12 @@ class CompiledGraph:
         m = B * (H * W if kind == N.PMX_DECONV2D else Ho * Wo)
         n_gemm = Co * (kh * kw if kind == N.PMX_DECONV2D else 1)
         k_gemm = C * (1 if kind == N.PMX_DECONV2D else kh * kw)
-        esz = {"fp32": 4, "fp16": 2, "int8": 1}
+        esz = _ESZ
         out_bytes = sum(B * Ho * Wo * Co * esz[f[0]] for f in out.need)
         self.op_info[f"conv {l.name}"] = {
             "flops": 2.0 * m * n_gemm * k_gemm, "precision": rec["precision"],
-            "bytes": B * H * W * C * esz[rec["precision"]] + n_gemm * k_gemm * esz[rec["precision"]] + out_bytes}
+            "bytes": B * H * W * C * esz[rec["precision"]]
+            + n_gemm * k_gemm * (12 if rec["precision"] == "fp32x2" else esz[rec["precision"]]) + out_bytes}
         if self.gather and self.gather["layer"] == l.name:
             g = self._keep[0]
             cmap = lib.pmx_pillarize_cell_map(ctypes.byref(g), self.B, self.nmax, self.pws.data_ptr())

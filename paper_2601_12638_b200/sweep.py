@@ -26,7 +26,9 @@ from .pointpillars import PointPillarsConfig, PointPillarsEngine
 from .quant import DType
 
 __all__ = ["SensitivityRecord", "head_error", "plan_errors", "sensitivity_sweep", "select_topk",
-           "greedy_candidates", "sharded_plan_sums", "records"]
+           "greedy_candidates", "exhaustive_subsets", "exhaustive_search", "sharded_plan_sums", "records"]
+
+EXHAUSTIVE_GUARD = 10_000  # SPEC.md:395 "guard: <= 10^4" subsets
 
 
 @dataclass(frozen=True)
@@ -109,6 +111,38 @@ def select_topk(errors: dict[int, float], k: int) -> list[int]:
 def greedy_candidates(ranking: list[int], k: int) -> list[PrecisionPlan]:
     """Candidate i = FP16 on the first i ranked layers, INT8 elsewhere."""
     return [parse_plan_label("FP16: " + ",".join(str(i) for i in ranking[:j])) for j in range(1, k + 1)]
+
+
+def exhaustive_subsets(layers, k: int, guard: int = EXHAUSTIVE_GUARD) -> list[tuple[int, ...]]:
+    """All C(L, k) FP16 subsets in lexicographic index order; refuses
+    explicitly, with the count, above the guard."""
+    import itertools
+    import math
+
+    layers = sorted(layers)
+    if not 1 <= k <= len(layers):
+        raise ValueError(f"k={k} out of range [1, {len(layers)}]")
+    n = math.comb(len(layers), k)
+    if n > guard:
+        raise ValueError(f"exhaustive search over C({len(layers)}, {k}) = {n} subsets exceeds the guard {guard}")
+    return list(itertools.combinations(layers, k))
+
+
+def exhaustive_search(graph, stats, frames, k: int, cfg: PointPillarsConfig = PointPillarsConfig(),
+                      batch: int = 32, layers=None, rank: int = 0, world: int = 1, device=None):
+    """The baseline greedy avoids: every k-subset of
+    ``layers`` (default: all indexed layers) in FP16 on an INT8 base, scored by the head
+    error against FP32 on ``frames``; the best subset has the lowest error, ties to the
+    lexicographically first subset.  Plans are sharded round-robin over ranks like the sweep."""
+    layers = [l.index for l in graph.weight_layers] if layers is None else list(layers)
+    subsets = exhaustive_subsets(layers, k)
+    plans = [parse_plan_label("FP16: " + ",".join(str(i) for i in sub)) for sub in subsets]
+    ref = reference_heads(graph, frames, cfg, batch)
+    tot = sharded_plan_sums(len(plans), rank, world, device,
+                            lambda js: plan_errors(graph, stats, frames, [plans[j] for j in js], ref, cfg, batch))
+    errs = {sub: head_error(tot[j]) for j, sub in enumerate(subsets)}
+    best = min(subsets, key=lambda sub: (errs[sub], sub))
+    return {"best": best, "best_error": errs[best], "errors": errs}
 
 
 def sharded_plan_sums(n_plans: int, rank: int, world: int, device, run_plans) -> np.ndarray:

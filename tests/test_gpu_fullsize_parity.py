@@ -149,8 +149,9 @@ def _dummy(pm, name, index, cin, fmt):
     """A 1x1 consumer whose only role is to make the producer write `fmt`."""
     w = np.full((16, cin, 1, 1), 0.01, np.float32)
     prec = pm.DType.INT8 if fmt[0] == "int8" else pm.DType(fmt[0])
+    # a head: its f32 output is an output of the graph, so every dummy stays live
     return pm.LayerSpec(name=name, kind="conv2d", index=index, weight=w, bias=np.zeros(16, np.float32),
-                        conv=pm.ConvParams(), precision=prec, inputs=("L",))
+                        conv=pm.ConvParams(), precision=prec, inputs=("L",), is_head=True)
 
 
 def _run_single(pm, layer, x, stats_l, consumer_fmts, pfn_sample=None):

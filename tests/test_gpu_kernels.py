@@ -313,3 +313,66 @@ def test_pfn_pillar_rows_vs_oracle(pm, prec, clustered):
     assert int(npil.item()) == P
     np.testing.assert_allclose(got[:P], y, rtol=1e-5, atol=1e-5)
     assert (got[P:] == -7.0).all()  # rows past n_pillars untouched
+
+
+@pytest.mark.parametrize("prec", ["int8", "fp32"])
+def test_pfn_every_live_pillar_count(pm, prec):
+    """Regression: the PFN's pillar-pair loop used a full-warp shuffle after a divergent
+    branch, so a warp whose last live pillar sat in the first half of a pair wrote its row
+    at a garbage address.  Every n_pillars from 1 to 70 (and the full count), dense clusters
+    included, must give the reference rows and leave the rest untouched."""
+    import ctypes
+
+    import torch
+
+    from paper_2601_12638_b200 import _native as N
+
+    cfg = pm.PointPillarsConfig.small(max_pillars=800)
+    pts = _kitti_case(pm, 4000, 23, cfg, True)
+    spec = cfg.grid_spec()
+    idx = O.pillar_index(O.bin_points(pts[:, :2], spec.grid, spec.origin, spec.cell), spec.grid, 32, 800)
+    feats, mask = O.pillar_features9(pts, idx, spec.origin, spec.cell)
+    P = len(idx.coords)
+    rng = np.random.default_rng(5)
+    C = 64
+    w = rng.normal(scale=0.3, size=(C, 9)).astype(np.float32)
+    bias = rng.normal(scale=0.1, size=C).astype(np.float32)
+    in_scale = float(np.abs(feats).max() / 127.0)
+    if prec == "int8":
+        ws_ = np.abs(w).max(axis=1) / 127.0
+        wq = np.rint(w.astype(np.float64) / ws_[:, None]).clip(-128, 127)
+        acc = np.einsum("pmj,cj->pmc", O.quantize(feats, in_scale).astype(np.float64), wq)
+        alpha = (in_scale * ws_).astype(np.float32)
+        y = (acc * alpha.astype(np.float64) + bias).astype(np.float32)
+        wdev, adev = torch.from_numpy(wq.astype(np.int8)).cuda(), torch.from_numpy(alpha).cuda()
+    else:
+        y = (np.einsum("pmj,cj->pmc", feats.astype(np.float64), w.astype(np.float64)) + bias).astype(np.float32)
+        wdev, adev = torch.from_numpy(w).cuda(), None
+    y = np.where(mask[:, :, None], np.maximum(y, 0), -np.inf).max(axis=1)
+    lib = N.load()
+    g = pm.engine.GridSpec(grid=spec.grid, origin=spec.origin, cell=spec.cell, max_points=32, max_pillars=800).to_c()
+    dpts = torch.from_numpy(pts).cuda()
+    offs = torch.tensor([0, len(pts)], dtype=torch.int64, device="cuda")
+    coords = torch.empty((1, 800, 2), dtype=torch.int32, device="cuda")
+    counts = torch.empty((1, 800), dtype=torch.int32, device="cuda")
+    pt_idx = torch.empty((1, 800, 32), dtype=torch.int32, device="cuda")
+    npil = torch.empty((1,), dtype=torch.int32, device="cuda")
+    wsb = lib.pmx_pillarize_workspace(ctypes.byref(g), 1, len(pts))
+    wsp = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+    N.check(lib.pmx_pillarize(dpts.data_ptr(), offs.data_ptr(), 1, len(pts), ctypes.byref(g), 800, coords.data_ptr(),
+                              counts.data_ptr(), pt_idx.data_ptr(), npil.data_ptr(), wsp.data_ptr(), wsb,
+                              N.stream_ptr()), "pillarize")
+    d = N.PfnDesc(source=N.PMX_PFN_FROM_POINTS9, in_dtype=N.DTYPE_CODE[prec], n_features=9, channels=C,
+                  max_points=32, relu=1, in_scale=in_scale if prec == "int8" else 0.0)
+    bdev = torch.from_numpy(bias).cuda()
+    for n_live in list(range(1, 71)) + [P - 1, P]:
+        npil.fill_(n_live)
+        rows = torch.full((800, C), -7.0, dtype=torch.float32, device="cuda")
+        arr, n = N.outs_array([N.Out(ptr=rows.data_ptr(), scale=0.0, dtype=N.PMX_F32, c_stride=C, c_offset=0)])
+        N.check(lib.pmx_pfn_pillars(ctypes.byref(d), ctypes.byref(g), 1, 800, dpts.data_ptr(), offs.data_ptr(), None,
+                                    None, coords.data_ptr(), counts.data_ptr(), pt_idx.data_ptr(), npil.data_ptr(),
+                                    wdev.data_ptr(), N.ptr(adev), bdev.data_ptr(), None, arr, n, None, None,
+                                    N.stream_ptr()), "pfn_pillars")
+        got = rows.cpu().numpy()
+        np.testing.assert_allclose(got[:n_live], y[:n_live], rtol=1e-5, atol=1e-5, err_msg=str(n_live))
+        assert (got[n_live:] == -7.0).all(), n_live

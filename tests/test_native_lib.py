@@ -18,7 +18,7 @@ def test_library_exports_every_declared_symbol():
     lib = N.load()
     for name in N.header_symbols():
         assert hasattr(lib, name), name
-    assert lib.pmx_abi_version() == 2
+    assert lib.pmx_abi_version() == 3
     assert lib.pmx_conv_backend(2, 0).decode() in ("tcgen05", "simt")
 
 
