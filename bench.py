@@ -44,7 +44,7 @@ def _mma_peaks(peaks):
     f = ROOT / "profiles" / "r2_mma_peak.json"
     if f.exists():
         d = json.loads(f.read_text())
-        return ({"int8": d["int8_tops_burst"], "fp16": d["f16_tflops_burst"], "fp32": d["tf32_tflops_burst"] / 3.0},
+        return ({"int8": d["int8_tops_burst"], "fp16": d["f16_tflops_burst"], "fp32x2": d["tf32_tflops_burst"] / 3.0},
                 "measured tcgen05 MMA burst peaks (profiles/r2_mma_peak.json, tools/mma_peak.cu): FLOP-weighted "
                 "mix of the int8 and f16 peaks over the layers")
     return ({"fp16": peaks["bf16_tflops"], "int8": 2.0 * peaks["bf16_tflops"]},
@@ -343,6 +343,9 @@ def main():
                     "peak_source": pk_src,
                     "peaks_tflops": pk,
                     "per_layer_ms": {k: round(op_ms[k], 4) for k in info},
+                    "per_layer": {k: {"ms": round(op_ms[k], 5), "flops": info[k]["flops"],
+                                      "bytes": info[k].get("bytes", 0), "precision": info[k]["precision"]}
+                                  for k in info},
                     # per-layer max(FLOP / dtype peak, algorithmic bytes / HBM): the bound with the
                     # memory-bound layers (deconvs, heads, stride-2 convs) counted as such
                     "layer_bound_ms": round(t_bound * 1e3, 4), "frac_of_layer_bound": t_bound * 1e3 / conv_ms,
@@ -353,12 +356,39 @@ def main():
 
     lat = None
     if not args.no_latency:
+        # config 3 (mixed, 120k points) and config 1 (FP32, 20k points / 12000 pillars) at batch 1,
+        # plus FP32 on the config-3 frame itself (same geometry both sides) and config 2
+        # (all-INT8, per-channel weights, 4 calibration frames with 1% outliers)
         mixed_p50, mixed_p99 = b1_latency(pm, graph, stats, cfg, plan, 120000, 77)
+        fp32_c3_p50, _ = b1_latency(pm, graph, None, cfg, pm.PrecisionPlan(), 120000, 77)
         cfg1 = pm.PointPillarsConfig(max_pillars=12000)
         fp32_p50, fp32_p99 = b1_latency(pm, graph, None, cfg1, pm.PrecisionPlan(), 20000, 78)
+        calib4 = [pm.make_frame(120000, 900 + i, cfg, outlier_frac=0.01) for i in range(4)]
+        stats_c2 = pm.calibrate_frames(graph, calib4, cfg, per_channel_weights=True)
+        int8_p50, int8_p99 = b1_latency(pm, graph, stats_c2, cfg, pm.parse_plan_label("INT8"), 120000, 77)
+        # config 3 batch-8 throughput (the same captured step as the headline, 8 frames)
+        f8 = pm.make_frames(8, 3000, cfg, (120000, 120000))
+        e8 = pm.PointPillarsEngine(graph, plan, stats, cfg, batch=8, max_points_per_frame=120000)
+        e8.load_points(f8)
+        e8.capture()
+        for _ in range(5):
+            e8.run()
+        a8, b8 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        a8.record()
+        for _ in range(50):
+            e8.run()
+        b8.record()
+        torch.cuda.synchronize()
+        ms8 = a8.elapsed_time(b8) / 50
+        del e8
         lat = {"mixed_b1_p50_ms": mixed_p50, "mixed_b1_p99_ms": mixed_p99, "fp32_b1_p50_ms": fp32_p50,
                "fp32_b1_p99_ms": fp32_p99, "fp32_over_mixed": fp32_p50 / mixed_p50,
-               "mixed_shape": "C3: 120k pts, 16000 pillars", "fp32_shape": "C1: 20k pts, 12000 pillars"}
+               "mixed_shape": "C3: 120k pts, 16000 pillars", "fp32_shape": "C1: 20k pts, 12000 pillars",
+               "fp32_c3_b1_p50_ms": fp32_c3_p50, "fp32_over_mixed_same_frame": fp32_c3_p50 / mixed_p50,
+               "int8_c2_b1_p50_ms": int8_p50, "int8_c2_b1_p99_ms": int8_p99,
+               "mixed_c3_b8_ms_per_step": ms8, "mixed_c3_b8_frames_per_s": 8 / (ms8 / 1e3),
+               "fp32_backend": "3xTF32 tcgen05 (kind::tf32, hi/lo split, f32 accumulate)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -367,9 +397,13 @@ def main():
         t0 = time.perf_counter()
         cpu_reference_frame(pm, O, graph, stats, cfg, frames[0], plan)
         dt = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        cpu_reference_frame(pm, O, graph, None, cfg, frames[0], pm.PrecisionPlan())
+        dt32 = time.perf_counter() - t0
         cpu = {"value": 1.0 / dt, "unit": "frames/s", "cores": NCORES, "kind": "port",
                "sample": f"1 frame ({len(frames[0])} pts) of the config-4 batch: oracle pillarize + mixed-plan "
-                         f"forward (numpy/OpenBLAS, {NCORES} threads) + top-k"}
+                         f"forward (numpy/OpenBLAS, {NCORES} threads) + top-k",
+               "fp32_value": 1.0 / dt32, "fp32_sample": "the same frame, FP32 plan"}
 
     if rank == 0:
         line = {

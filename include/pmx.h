@@ -272,6 +272,36 @@ void pmx_set_conv_backend(int32_t mode);
  * = kernel entry, setup done, resident weights landed, teardown; row 9 = MMA loop top. */
 void pmx_debug_trace(unsigned long long* buf);
 
+/* ------------------------------------------------------------------------
+ * K9+K10 fused: a neck deconvolution (kernel == stride, Cout == 128, INT8 or FP16
+ * input) whose output feeds only the concat of the three 1x1 INT8 heads
+ * (pm/model.py:329-331 heads on the trunk; pm/model.py:271-307 INT8 head inputs).
+ * The deconv's output tile is quantized with the heads' activation scale (the int8
+ * codes the concat would hold) and multiplied right away, on the tensor core, by its
+ * 128-channel slice of the heads' weight codes; the int32 partial sums of the heads
+ * (order-free, exact) accumulate over the three deconvs in `partial`, and the last one
+ * applies the heads' epilogue -- so the 384-channel concat is never written or read.
+ * Results equal pmx_conv(deconv) -> concat -> pmx_conv(heads) bit for bit.
+ * ---------------------------------------------------------------------- */
+typedef struct {
+  const int8_t* w_codes;    /* [32, 128] int8 head weight codes for this deconv's concat
+                               slice (row n = head output channel; rows >= n_heads zero) */
+  int32_t n_heads;          /* total head output channels, <= 20 (partial rows hold 20) */
+  int32_t stage;            /* 0: write partial; 1: partial += ; 2: partial + this -> heads */
+  double in_scale;          /* the heads' activation scale (codes = quantize(y, in_scale)) */
+  int32_t* partial;         /* int32 [B * out_h * out_w, 20] */
+  float* heads;             /* stage 2: f32 NHWC [B * out_h * out_w, heads_c_stride] */
+  int32_t heads_c_stride;
+  int32_t _pad;
+  const float* head_alpha;  /* stage 2: f32(s_in * s_w[n]), [n_heads] */
+  const float* head_bias;   /* stage 2: [n_heads] */
+} pmx_head_fuse;
+
+/* 1 if pmx_deconv_heads runs desc. */
+int32_t pmx_deconv_heads_supported(const pmx_conv_desc* desc);
+pmx_status pmx_deconv_heads(const pmx_conv_desc* desc, const void* x, const void* w, const float* alpha,
+                            const float* bias, const pmx_head_fuse* heads, pmx_stream_t stream);
+
 /* Stage an f32 [pixels, c] tensor into every consumer format (the precision
  * transform of pm/model.py:273-285 applied to a graph input), optionally
  * widening an observer with its values. */

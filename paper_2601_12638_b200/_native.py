@@ -62,6 +62,12 @@ class NmsDesc(C.Structure):
                 ("score_thresh", C.c_double), ("iou_thresh", C.c_double)]
 
 
+class HeadFuse(C.Structure):
+    _fields_ = [("w_codes", C.c_void_p), ("n_heads", C.c_int32), ("stage", C.c_int32), ("in_scale", C.c_double),
+                ("partial", C.c_void_p), ("heads", C.c_void_p), ("heads_c_stride", C.c_int32), ("_pad", C.c_int32),
+                ("head_alpha", C.c_void_p), ("head_bias", C.c_void_p)]
+
+
 P = C.c_void_p
 I32, I64, F64, SZ = C.c_int32, C.c_int64, C.c_double, C.c_size_t
 
@@ -90,6 +96,8 @@ SIGNATURES = {
     "pmx_conv_gather": (I32, [C.POINTER(ConvDesc), P, P, I32, P, P, P, P, C.POINTER(Out), I32, P, P]),
     "pmx_conv_workspace": (SZ, [C.POINTER(ConvDesc)]),
     "pmx_conv_tc_supported": (I32, [C.POINTER(ConvDesc)]),
+    "pmx_deconv_heads_supported": (I32, [C.POINTER(ConvDesc)]),
+    "pmx_deconv_heads": (I32, [C.POINTER(ConvDesc), P, P, P, P, C.POINTER(HeadFuse), P]),
     "pmx_conv": (I32, [C.POINTER(ConvDesc), P, P, P, P, P, C.POINTER(Out), I32, P, P, SZ, P]),
     "pmx_set_conv_backend": (None, [I32]),
     "pmx_debug_trace": (None, [P]),

@@ -17,6 +17,9 @@ pmx_status conv_tc_try(const pmx_conv_desc& d, const void* x, const void* w, con
 size_t conv_tc_workspace(const pmx_conv_desc& d);
 bool conv_tc_gather_ok(const pmx_conv_desc& d);
 bool conv_tc_supported(const pmx_conv_desc& d);
+bool conv_tc_heads_ok(const pmx_conv_desc& d);
+pmx_status conv_tc_deconv_heads(const pmx_conv_desc& d, const void* x, const void* w, const float* alpha,
+                                const float* bias, const pmx_head_fuse& hf, cudaStream_t st);
 const char* conv_tc_backend(int dtype, int kind);
 
 // backend override of the CALLING thread (tests): thread-local, so concurrent callers on
@@ -218,6 +221,29 @@ void pmx_set_conv_backend(int32_t mode) { g_conv_backend_mode = mode; }
 const char* pmx_conv_backend(int32_t in_dtype, int32_t kind) {
   if (g_conv_backend_mode == 1) return "simt";
   return conv_tc_backend(in_dtype, kind);
+}
+
+int32_t pmx_deconv_heads_supported(const pmx_conv_desc* desc) {
+  if (!desc || validate(*desc) != PMX_OK) return 0;
+  return conv_tc_heads_ok(*desc) ? 1 : 0;
+}
+
+pmx_status pmx_deconv_heads(const pmx_conv_desc* desc, const void* x, const void* w, const float* alpha,
+                            const float* bias, const pmx_head_fuse* heads, pmx_stream_t stream) {
+  PMX_REQUIRE(desc != nullptr && heads != nullptr, "desc/heads is NULL");
+  const pmx_conv_desc d = *desc;
+  pmx_status st = validate(d);
+  if (st != PMX_OK) return st;
+  const pmx_head_fuse& hf = *heads;
+  PMX_REQUIRE(x && w && bias && hf.w_codes && hf.partial, "NULL deconv/heads operand");
+  PMX_REQUIRE(d.in_dtype != PMX_I8 || alpha, "int8 conv needs alpha");
+  PMX_REQUIRE(hf.n_heads >= 1 && hf.n_heads <= 20, "n_heads must be 1..20");
+  PMX_REQUIRE(hf.stage >= 0 && hf.stage <= 2, "stage must be 0, 1 or 2");
+  PMX_REQUIRE(hf.in_scale > 0.0, "heads' activation scale must be positive");
+  PMX_REQUIRE(hf.stage != 2 || (hf.heads && hf.head_alpha && hf.head_bias && hf.heads_c_stride >= hf.n_heads),
+              "the last stage needs heads, head_alpha, head_bias");
+  if (d.batch == 0) return PMX_OK;
+  return conv_tc_deconv_heads(d, x, w, alpha, bias, hf, stream);
 }
 
 int32_t pmx_conv_tc_supported(const pmx_conv_desc* desc) {

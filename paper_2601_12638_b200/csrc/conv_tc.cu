@@ -148,6 +148,23 @@ __device__ __forceinline__ void tmem_ld_wait(uint32_t (&v)[16]) {
                : "memory");
 }
 
+// 16 accumulator columns of this thread's row; 3xTF32 adds its correction accumulator
+// (lo_col columns further) in f32, round to nearest
+template <int DT>
+__device__ __forceinline__ void acc_ld16(uint32_t taddr, int lo_col, uint32_t (&v)[16]) {
+  tmem_ld16_issue(taddr, v);
+  if constexpr (DT == PMX_F32X2) {
+    uint32_t w[16];
+    tmem_ld16_issue(taddr + (uint32_t)lo_col, w);
+    tmem_ld_wait(v);
+    tmem_ld_wait(w);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = __float_as_uint(__fadd_rn(__uint_as_float(v[j]), __uint_as_float(w[j])));
+  } else {
+    tmem_ld_wait(v);
+  }
+}
+
 // one lane of a converged warp (the lowest active one)
 __device__ __forceinline__ bool elect_one() {
   uint32_t pred;
@@ -201,6 +218,25 @@ struct TcParams {
   // hi x w_hi, lo x w_hi, hi x w_lo; A channel of block cb = a_off (+ a_lo in segment 1)
   // + (cb mod seg_n) * kc, the map spanning both planes of the pixel.  seg_n = 0: plain.
   int seg_n, a_off, a_lo;
+  // TMEM columns per accumulator buffer: bn, or 2 * bn for 3xTF32, whose hi x w_hi
+  // products accumulate at column 0 and the small lo x w_hi + hi x w_lo corrections at
+  // column lo_col = bn (summed in f32 by the epilogue): the tensor core's accumulation
+  // truncates, so the corrections must not be added into the large partial sums
+  int acc_stride, lo_col;
+  // HEADS (OUTK 2, deconvs of the neck): the deconv's output tile is never written; its
+  // int8 codes (the heads' input format) are staged in shared memory as the A operand of
+  // a second kind::i8 MMA against this deconv's 128-channel slice of the three 1x1 heads
+  // (N = 32 >= n_heads), and the int32 head partial sums go to hpart (stage 0 writes,
+  // 1 accumulates, 2 accumulates and applies the heads' epilogue into hout)
+  int hstage_mode, n_heads, hcs;
+  const int8_t* hwc;     // [32][128] int8 head weight codes of this slice (rows >= n_heads zero)
+  int32_t* hpart;        // [pixels][n_heads]
+  float* hout;           // stage 2: f32 heads [pixels][hcs]
+  const float* halpha;   // stage 2
+  const float* hbias;    // stage 2
+  double hscale;
+  float hinv;
+  uint32_t hidesc, hcol0;
   int cblocks;      // K-blocks per tap
   int taps;         // 9 or 1
   int bn;           // N tile
@@ -596,9 +632,14 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int total = p.m_tiles * p.n_tiles;
   const int nk = p.taps * p.cblocks;
+  __shared__ uint64_t hbar_s[2];  // HEADS: head MMA done, per epilogue tile slot
 
   if (threadIdx.x == 0) {
     PMX_TRACE(8, 0);
+    if (OUTK == 2) {
+      mbar_init(smem_u32(&hbar_s[0]), 1);
+      mbar_init(smem_u32(&hbar_s[1]), 1);
+    }
     for (int s = 0; s < p.stages; ++s) {
       mbar_init(full(s), GATHER ? 2 * 32 * kGatherWarps : 1);  // TMA: expect_tx; gather: 2 arrivals per thread
       mbar_init(empty(s), 1);
@@ -741,7 +782,7 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
         if (lane == 0) PMX_TRACE(9, i);
         mbar_spin(tempty(acc), aph ^ 1);
         tc_fence_after();
-        const uint32_t d = tmem + acc * bn;
+        const uint32_t d = tmem + acc * (uint32_t)p.acc_stride;
         if (lane == 0) PMX_TRACE(2, i);
         mbar_spin(full(s), ph);
         tc_fence_after();
@@ -816,7 +857,7 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
         if (lane == 0) PMX_TRACE(9, i);
         mbar_spin(tempty(acc), aph ^ 1);
         tc_fence_after();
-        const uint32_t d = tmem + acc * bn;
+        const uint32_t d = tmem + acc * (uint32_t)p.acc_stride;
         if (lane == 0) PMX_TRACE(2, i);
         for (int kb = 0; kb < nk; ++kb) {
           mbar_spin(full(s), ph);
@@ -824,11 +865,21 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
           if (elect_one()) {
             if (kb == 0) PMX_TRACE(3, i);
             const uint32_t alo = lo0 + ((a_smem + s * p.a_bytes) >> 4), blo = lo0 + ((b_smem + s * p.b_bytes) >> 4);
+            uint32_t dk = d;
+            bool first = kb == 0;
+            if constexpr (DT == PMX_F32X2) {
+              // segments 1, 2 (the lo corrections) go to the second accumulator
+              const int cb = kb % p.cblocks;
+              if (cb >= p.seg_n) {
+                dk = d + (uint32_t)p.lo_col;
+                first = kb == p.seg_n;
+              }
+            }
 #pragma unroll
             for (int k = 0; k < ksteps; ++k) {
               const uint64_t ad = ((uint64_t)hi << 32) | (alo + 2u * k);
               const uint64_t bd = ((uint64_t)hi << 32) | (blo + 2u * k);
-              tc_mma<DT>(d, ad, bd, idesc, (kb | k) != 0);
+              tc_mma<DT>(dk, ad, bd, idesc, !(first && k == 0));
             }
             tc_commit(empty(s));
           }
@@ -862,6 +913,20 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
       for (int j = et; j < p.out_c; j += 32 * kEpiWarps) {
         s_alpha[j] = p.alpha ? p.alpha[j] : 0.0f;
         s_bias[j] = p.bias[j];
+      }
+      if constexpr (OUTK == 2) {
+        // head weights -> the B operand: 32 rows x 128 B, SW128 (16-byte chunk j of row r
+        // at chunk j ^ (r & 7))
+        const uint32_t hb = (s_estage + 1023u) & ~1023u;
+        const uint32_t s_hw = hb + 2u * 16384u;
+        if (et < 32 * 8) {
+          const int r = et >> 3, j = et & 7;
+          const uint4 wv = *reinterpret_cast<const uint4*>(p.hwc + r * 128 + 16 * j);
+          asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(s_hw + r * 128 + ((j ^ (r & 7)) << 4)),
+                       "r"(wv.x), "r"(wv.y), "r"(wv.z), "r"(wv.w)
+                       : "memory");
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       }
       asm volatile("bar.sync 1, %0;" ::"r"(32 * kEpiWarps) : "memory");
     }
@@ -902,9 +967,101 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
       tc_fence_after();
       if (warp == 0 && lane == 0) PMX_TRACE(6, i);
       if (lane == 0 && i == 6) PMX_TRACE(8, 8 + 2 * warp);  // per-warp view of one steady-state tile
-      const uint32_t trow = tmem + acc * (uint32_t)p.bn + ((uint32_t)(q * 32) << 16);
+      const uint32_t trow = tmem + acc * (uint32_t)p.acc_stride + ((uint32_t)(q * 32) << 16);
       // deconv: output pixel of tap (0, 0); tap (dy, dx) adds dy * out_w + dx
       const uint32_t pbase = (ib * p.out_h + iy * p.stride) * p.out_w + ix * p.stride;
+      if constexpr (OUTK == 2) {
+        // ---- deconv + heads: one tile = one tap (bn = Cout = 128) of 128 input pixels
+        const uint32_t hb = (s_estage + 1023u) & ~1023u;
+        const uint32_t st = hb + (uint32_t)eg * 16384u, s_hw = hb + 2u * 16384u;
+        const uint32_t hbar = smem_u32(&hbar_s[eg]);
+        const uint32_t hpar = (i / (uint32_t)egn) & 1u;
+        const int tap = (int)nt;
+        const uint32_t opix = pbase + (uint32_t)(tap >> p.st_shift) * (uint32_t)p.out_w +
+                              (uint32_t)(tap & (p.stride - 1));
+#pragma unroll 1
+        for (int k = 0; k < 4; ++k) {
+          uint32_t v[16];
+          acc_ld16<DT>(trow + 16 * (c_begin + k), p.lo_col, v);
+          const int cobase = 16 * (c_begin + k);
+          float y[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            float t;
+            if constexpr (DT == PMX_I8) t = __fmaf_rn((float)(int)v[j], s_alpha[cobase + j], s_bias[cobase + j]);
+            else t = __fadd_rn(__uint_as_float(v[j]), s_bias[cobase + j]);
+            y[j] = p.relu ? fmaxf(t, 0.f) : t;
+          }
+          uint4 code = valid ? quant16(y, p.hscale, p.hinv) : make_uint4(0, 0, 0, 0);
+          const uint32_t jj = (uint32_t)(c_begin + k);  // 16-byte chunk of the 128-byte row
+          asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(st + (uint32_t)row * 128u +
+                                                                         ((jj ^ ((uint32_t)row & 7u)) << 4)),
+                       "r"(code.x), "r"(code.y), "r"(code.z), "r"(code.w)
+                       : "memory");
+        }
+        // main accumulator drained: release it to the MMA warp
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(tempty(acc));
+        // codes -> async proxy, the slot's 8 warps meet, one thread issues the head MMA
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("bar.sync %0, 256;" ::"r"(2 + eg) : "memory");
+        const uint32_t hcol = tmem + p.hcol0 + 32u * (uint32_t)eg;
+        if (cg == 0 && q == 0) {
+          tc_fence_after();
+          if (elect_one()) {
+            const uint32_t ahi = (uint32_t)(sdesc(0, 1024u, 2u) >> 32);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const uint64_t ad = ((uint64_t)ahi << 32) | (uint32_t)sdesc(st + 32u * k, 1024u, 2u);
+              const uint64_t bd = ((uint64_t)ahi << 32) | (uint32_t)sdesc(s_hw + 32u * k, 1024u, 2u);
+              tc_mma<PMX_I8>(hcol, ad, bd, p.hidesc, k != 0);
+            }
+            tc_commit(hbar);
+          }
+          __syncwarp();
+        }
+        mbar_wait(hbar, hpar);
+        tc_fence_after();
+        if (cg == 0) {
+          uint32_t h0[16], h1[16];
+          tmem_ld16_issue(hcol + ((uint32_t)(q * 32) << 16), h0);
+          tmem_ld16_issue(hcol + 16u + ((uint32_t)(q * 32) << 16), h1);
+          tmem_ld_wait(h0);
+          tmem_ld_wait(h1);
+          tc_fence_before();
+          if (valid) {
+            int hs[20];
+#pragma unroll
+            for (int n = 0; n < 16; ++n) hs[n] = (int)h0[n];
+#pragma unroll
+            for (int n = 16; n < 20; ++n) hs[n] = (int)h1[n - 16];
+            int4* pp = reinterpret_cast<int4*>(p.hpart + (size_t)opix * 20u);
+            if (p.hstage_mode != 0) {
+#pragma unroll
+              for (int u = 0; u < 5; ++u) {
+                const int4 o = pp[u];
+                hs[4 * u] += o.x;
+                hs[4 * u + 1] += o.y;
+                hs[4 * u + 2] += o.z;
+                hs[4 * u + 3] += o.w;
+              }
+            }
+            if (p.hstage_mode != 2) {
+#pragma unroll
+              for (int u = 0; u < 5; ++u) pp[u] = make_int4(hs[4 * u], hs[4 * u + 1], hs[4 * u + 2], hs[4 * u + 3]);
+            } else {
+              // the heads' epilogue: f32(acc) * alpha + bias in one rounding (the fused-heads
+              // kernel's formula, so the result is bit-identical)
+              float* ho = p.hout + (size_t)opix * (uint32_t)p.hcs;
+#pragma unroll
+              for (int n = 0; n < 20; ++n)
+                if (n < p.n_heads) ho[n] = __fmaf_rn((float)hs[n], __ldg(p.halpha + n), __ldg(p.hbias + n));
+            }
+          }
+        }
+        continue;
+      }
       if constexpr (OUTK == 0) {
         if (p.estage2) {
           // int8 consumer and f16 consumer (no dynamic indexing of the parameter struct)
@@ -971,8 +1128,7 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
 #pragma unroll 1
             for (int k = 0; k < 4; ++k) {
               uint32_t v[16];
-              tmem_ld16_issue(trow + 16 * (c_begin + k), v);
-              tmem_ld_wait(v);
+              acc_ld16<DT>(trow + 16 * (c_begin + k), p.lo_col, v);
               if (valid && live) {
                 float y[16];
                 chunk(k, v, y);
@@ -1005,8 +1161,7 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
 #pragma unroll 1
             for (int k = 0; k < 4; ++k) {
               uint32_t v[16];
-              tmem_ld16_issue(trow + 16 * (c_begin + k), v);
-              tmem_ld_wait(v);
+              acc_ld16<DT>(trow + 16 * (c_begin + k), p.lo_col, v);
               if (!valid || !live) continue;
               float y[16];
               chunk(k, v, y);
@@ -1054,8 +1209,7 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
 #pragma unroll 1
           for (int k = 0; k < 4; ++k) {
             uint32_t v[16];
-            tmem_ld16_issue(trow + 16 * (c_begin + k), v);
-            tmem_ld_wait(v);
+            acc_ld16<DT>(trow + 16 * (c_begin + k), p.lo_col, v);
             if (!valid || !live) continue;
             const int cobase = cob0 + 16 * k;
             float y[16];
@@ -1124,8 +1278,7 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
         // 5 warps share one SM sub-partition: 96 registers per thread leave no room
         // to double-buffer the TMEM loads; the other tile slots hide the latency
         uint32_t v[16];
-        tmem_ld16_issue(trow + 16 * c, v);
-        tmem_ld_wait(v);
+        acc_ld16<DT>(trow + 16 * c, p.lo_col, v);
         const int nbase = n0 + 16 * c;
         if (!valid || nbase >= p.n_gemm) continue;
         // deconv: 16 consecutive GEMM columns share one tap (Cout % 16 == 0)
@@ -1285,10 +1438,14 @@ int estage_min_row() {  // PMX_ESTAGE=2: stage every eligible layer (experiments
   return v;
 }
 
+constexpr uint32_t kHeadsSmem = 1024u + 2u * 16384u + 4096u;  // alignment + 2 code stages + head weights
+
 Plan plan_for(const pmx_conv_desc& d, bool gather = false, bool want_stage = false, int out_row_bytes = 0,
-              bool want_stage2 = false) {
+              bool want_stage2 = false, bool heads = false) {
   Plan pl{};
   pl.ok = false;
+  if (heads && !(d.kind == PMX_DECONV2D && d.out_c == 128 && (d.in_dtype == PMX_I8 || d.in_dtype == PMX_F16)))
+    return pl;
   if (d.in_dtype != PMX_I8 && d.in_dtype != PMX_F16 && d.in_dtype != PMX_F32X2) return pl;
   const bool x3 = d.in_dtype == PMX_F32X2;
   if (x3 && (gather || d.in_c % 32 != 0 || d.in_c_stride % 2 != 0)) return pl;
@@ -1354,6 +1511,7 @@ Plan plan_for(const pmx_conv_desc& d, bool gather = false, bool want_stage = fal
   // N tile: the whole GEMM N up to 256 (the A tile is then read once); TMEM holds two
   int bn = (int)(ceil_div(p.n_gemm, 16) * 16);
   if (bn > 256) bn = 256;
+  if (x3 && bn > 128) bn = 128;  // two accumulators (hi, corrections) per buffer
   {
     const char* e = getenv("PMX_DECONV_BN");  // experiment: cap the deconv N tile
     if (e && p.deconv && bn > atoi(e)) bn = atoi(e);
@@ -1361,6 +1519,7 @@ Plan plan_for(const pmx_conv_desc& d, bool gather = false, bool want_stage = fal
   // small M (batch-1 blocks.2: 27 M tiles): split N while the tile count still fits
   // one wave -- each CTA then streams a quarter of the weights and issues N=64 MMAs
   while (bn > 64 && bn % 32 == 0 && (int64_t)p.m_tiles * ceil_div(p.n_gemm, bn / 2) <= num_sms()) bn /= 2;
+  if (heads) bn = 128;  // one tile = one deconv tap = one head MMA of K = 128
   p.bn = bn;
   p.n_tiles = (int)ceil_div(p.n_gemm, bn);
   const int64_t tiles = (int64_t)p.m_tiles * p.n_tiles;
@@ -1368,11 +1527,15 @@ Plan plan_for(const pmx_conv_desc& d, bool gather = false, bool want_stage = fal
   pl.grid_y = 1;
   // warp-transposed int8 stores: every epilogue warp owns exactly 4 chunks (64
   // channels) of a tile, groups never straddle a deconv tap
+  p.acc_stride = x3 ? 2 * bn : bn;
+  p.lo_col = x3 ? bn : 0;
   p.nacc = 2;
-  while (p.nacc < 8 && 2 * p.nacc * bn <= 512) p.nacc *= 2;
+  while (!heads && p.nacc < 8 && 2 * p.nacc * p.acc_stride <= 512) p.nacc *= 2;
   p.nacc_shift = __builtin_ctz((unsigned)p.nacc);
   p.egroups = bn <= 64 ? 4 : (bn <= 128 ? 2 : 1);
   if (p.egroups > p.nacc) p.egroups = p.nacc;
+  p.hcol0 = (uint32_t)(p.nacc * p.acc_stride);  // HEADS: 32 columns per tile slot after the accumulators
+  if (heads) want_stage = want_stage2 = false;
   // (measured: a win for 128- and 384-byte output rows -- deconvs into the concat,
   // blocks.1.0 -- a loss for the 64-byte rows of block 0, which are MMA-bound)
   p.estage = want_stage && estage_enabled() && out_row_bytes >= estage_min_row() && (bn / 16) == 4 * (4 / p.egroups) &&
@@ -1388,7 +1551,8 @@ Plan plan_for(const pmx_conv_desc& d, bool gather = false, bool want_stage = fal
   p.a_bytes = 128u * kc_bytes;
   p.b_bytes = (uint32_t)bn * kc_bytes;
   const uint32_t stage = p.a_bytes + p.b_bytes;
-  int stages = (int)((200u * 1024u - 8u * (uint32_t)d.out_c - estage_bytes) / stage);  // one persistent CTA per SM
+  int stages = (int)((200u * 1024u - 8u * (uint32_t)d.out_c - estage_bytes - (heads ? kHeadsSmem : 0u)) /
+                     stage);  // one persistent CTA per SM
   if (stages > 12) stages = 12;
   if (stages < 2) stages = 2;
   p.stages = stages;
@@ -1457,7 +1621,7 @@ Plan plan_for(const pmx_conv_desc& d, bool gather = false, bool want_stage = fal
   p.fd_oc = make_fastdiv((uint32_t)d.out_c);
   // as many TMEM accumulators as fit (a power of two, 2..8): the MMA warp runs ahead
   // of the epilogue; the epilogue drains up to 4 tiles at once (tile slots)
-  const int cols = p.nacc * bn;
+  const int cols = p.nacc * p.acc_stride + (heads ? 64 : 0);
   p.tmem_cols = cols <= 32 ? 32 : (cols <= 64 ? 64 : (cols <= 128 ? 128 : (cols <= 256 ? 256 : 512)));
   const uint32_t m_enc = 128u >> 4, n_enc = (uint32_t)bn >> 3;
   if (d.in_dtype == PMX_I8)
@@ -1467,7 +1631,9 @@ Plan plan_for(const pmx_conv_desc& d, bool gather = false, bool want_stage = fal
   else
     p.idesc = (1u << 4) | (0u << 7) | (0u << 10) | (n_enc << 17) | (m_enc << 24);
   pl.smem = 1024 + (size_t)p.stages * (p.a_bytes + p.b_bytes) + p.bres_bytes + (2 * p.stages + 2 * p.nacc + 1) * 8 + 32 +
-            8 * (size_t)((d.out_c + 3) & ~3) + (gather ? kGatherSmem : 0) + (estage_bytes ? 16 + estage_bytes : 0);
+            8 * (size_t)((d.out_c + 3) & ~3) + (gather ? kGatherSmem : 0) + (estage_bytes ? 16 + estage_bytes : 0) +
+            (heads ? 16 + kHeadsSmem : 0);
+  p.hidesc = (2u << 4) | (1u << 7) | (1u << 10) | ((32u >> 3) << 17) | ((128u >> 4) << 24);  // s32 <- s8 x s8, N 32
   pl.ok = true;
   return pl;
 }
@@ -1657,6 +1823,69 @@ pmx_status conv_tc_try(const pmx_conv_desc& d, const void* x, const void* w, con
   if (s != PMX_OK) return s;
   *launched = true;
   return check_launch(gather ? "pmx_conv_gather(tcgen05)" : "pmx_conv(tcgen05)");
+}
+
+bool conv_tc_heads_ok(const pmx_conv_desc& d) {
+  if (g_conv_backend_mode == 1) return false;
+  return plan_for(d, false, false, 0, false, true).ok;
+}
+
+// deconv with the three 1x1 heads fused into its epilogue (OUTK 2): see TcParams::hstage_mode
+pmx_status conv_tc_deconv_heads(const pmx_conv_desc& d, const void* x, const void* w, const float* alpha,
+                                const float* bias, const pmx_head_fuse& hf, cudaStream_t st) {
+  Plan pl = plan_for(d, false, false, 0, false, true);
+  if (!pl.ok || g_conv_backend_mode == 1)
+    return fail(PMX_ERR_UNSUPPORTED, "pmx_deconv_heads: deconv shape outside the fused tcgen05 kernel");
+  if ((reinterpret_cast<uintptr_t>(x) & 15) || (reinterpret_cast<uintptr_t>(w) & 15) ||
+      (reinterpret_cast<uintptr_t>(hf.w_codes) & 15) || (reinterpret_cast<uintptr_t>(hf.partial) & 15))
+    return fail(PMX_ERR_INVALID, "pmx_deconv_heads: operands must be 16-byte aligned");
+  pmx_status s = get_encode();
+  if (s != PMX_OK) return s;
+  TcMaps maps;
+  memset(&maps, 0, sizeof(maps));
+  s = build_maps(d, pl, x, w, &maps);
+  if (s != PMX_OK) return s;
+  TcParams p = pl.p;
+  p.alpha = alpha;
+  p.bias = bias;
+  p.bn_post = nullptr;
+  p.keys = nullptr;
+  p.trace = g_trace;
+  p.hstage_mode = hf.stage;
+  p.n_heads = hf.n_heads;
+  p.hcs = hf.heads_c_stride;
+  p.hwc = hf.w_codes;
+  p.hpart = hf.partial;
+  p.hout = hf.heads;
+  p.halpha = hf.head_alpha;
+  p.hbias = hf.head_bias;
+  p.hscale = hf.in_scale;
+  p.hinv = (float)(1.0 / hf.in_scale);
+  Outs outs{};
+  outs.n = 0;
+  auto launch = [&](auto kern) -> pmx_status {
+    PMX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(pl.grid_x, pl.grid_y);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = pl.smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    PMX_CUDA(cudaLaunchKernelEx(&cfg, kern, maps, p, outs));
+    return PMX_OK;
+  };
+  const int kcb = (int)(pl.p.sbo / 8);
+  if (d.in_dtype == PMX_I8)
+    s = kcb == 64 ? launch(conv_tc_kernel<PMX_I8, 2, 64, 0, 0, false>) : launch(conv_tc_kernel<PMX_I8, 2, 128, 0, 0, false>);
+  else
+    s = kcb == 64 ? launch(conv_tc_kernel<PMX_F16, 2, 64, 0, 0, false>)
+                  : launch(conv_tc_kernel<PMX_F16, 2, 128, 0, 0, false>);
+  if (s != PMX_OK) return s;
+  return check_launch("pmx_deconv_heads(tcgen05)");
 }
 
 }  // namespace pmx

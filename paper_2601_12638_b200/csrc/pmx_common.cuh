@@ -219,7 +219,9 @@ __host__ inline Outs make_outs(const pmx_out* outs, int n) {
 __device__ __forceinline__ float tf32_hi(float y) {
   const uint32_t b = __float_as_uint(y);
   if ((b & 0x7f800000u) == 0x7f800000u) return y;
-  return __uint_as_float((b + 0x0fffu + ((b >> 13) & 1u)) & 0xffffe000u);
+  uint32_t r = (b + 0x0fffu + ((b >> 13) & 1u)) & 0xffffe000u;
+  if ((r & 0x7f800000u) == 0x7f800000u) r = b & 0xffffe000u;  // no rounding up into Inf near FLT_MAX
+  return __uint_as_float(r);
 }
 __device__ __forceinline__ float2 tf32_split(float y) {
   const float hi = tf32_hi(y);

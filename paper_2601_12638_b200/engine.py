@@ -123,10 +123,32 @@ def tf32_split(w: np.ndarray):
     w = np.ascontiguousarray(w, np.float32)
     b = w.view(np.uint32).astype(np.uint64)
     finite = (b & 0x7F800000) != 0x7F800000
-    hb = np.where(finite, (b + 0x0FFF + ((b >> 13) & 1)) & 0xFFFFE000, b).astype(np.uint32)
+    r = (b + 0x0FFF + ((b >> 13) & 1)) & 0xFFFFE000
+    r = np.where((r & 0x7F800000) == 0x7F800000, b & 0xFFFFE000, r)  # no rounding up into Inf
+    hb = np.where(finite, r, b).astype(np.uint32)
     hi = hb.view(np.float32)
-    lo = np.where(finite, w - hi, np.float32(0)).astype(np.float32)
+    with np.errstate(invalid="ignore"):
+        lo = np.where(finite, w - hi, np.float32(0)).astype(np.float32)
     return hi, lo
+
+
+class _capturing:
+    """Collect dead engines before a CUDA-graph capture and keep the cyclic GC off during it:
+    a CUDAGraph freed by the GC mid-capture (engines hold reference cycles) calls an API
+    that is illegal while a stream captures and invalidates the capture."""
+
+    def __enter__(self):
+        import gc
+
+        gc.collect()
+        self.was = gc.isenabled()
+        gc.disable()
+
+    def __exit__(self, *exc):
+        import gc
+
+        if self.was:
+            gc.enable()
 
 
 class CompiledGraph:
@@ -172,6 +194,7 @@ class CompiledGraph:
         self._choose_x3()
         self._needs()
         self.gather = self._gather_plan()
+        self.hfuse = self._heads_fusion_plan()
         self._allocate()
         self._prep_weights()
         self._build_ops()
@@ -275,6 +298,10 @@ class CompiledGraph:
         """FP32 layers the 3xTF32 tensor-core kernel runs (their inputs are stored as
         fp32x2); the others keep f32 inputs and the SIMT kernel."""
         self.x3 = set()
+        if self.observe:
+            # calibration / observed forwards keep the plain f32 FMA path: the PTQ ranges
+            # must follow the reference's f32 arithmetic as closely as possible
+            return
         for l in self.graph.layers:
             if not l.is_weight_layer or l is self.pfn or l.name not in self.layer_src or _prec(l) != "fp32":
                 continue
@@ -388,6 +415,51 @@ class CompiledGraph:
             return None
         return {"layer": cons[0].name, "fmt": fmt}
 
+    def _heads_fusion_plan(self):
+        """Deconvs -> concat -> three INT8 1x1 heads: fold the heads into the deconvs'
+        epilogues (pmx_deconv_heads) so the concat is never materialised.  Returns the
+        deconv layers in execution order, or None when the graph / plan does not fit."""
+        import os
+
+        # opt-in (PMX_FUSE_HEADS=1): bit-identical, but measured slower than the unfused
+        # deconvs + heads GEMM on the config-4 step (DESIGN.md §8)
+        if self.anchors is None or self.observe or os.environ.get("PMX_FUSE_HEADS", "0") != "1":
+            return None
+        a = self.anchors
+        by_name = {l.name: l for l in self.graph.layers}
+        hs = [by_name[n] for n in (a.cls_head, a.box_head, a.dir_head)]
+        srcs = {tuple(self.layer_src[h.name]) for h in hs}
+        fmts = {self._fmt(h) for h in hs}
+        if len(srcs) != 1 or len(fmts) != 1 or next(iter(fmts))[0] != "int8":
+            return None
+        if any(h.kind != "conv2d" or h.weight.shape[2:] != (1, 1) or h.bn is not None or h.relu for h in hs):
+            return None
+        (src,) = next(iter(srcs))
+        cat = by_name.get(src)
+        if cat is None or cat.kind != "concat" or 10 * len(a.rotations) > 20:
+            return None
+        cons = self.cons.get(src, [])
+        if sorted(c.name for c in cons) != sorted(h.name for h in hs):
+            return None
+        deconvs = [by_name[n] for n in self.layer_src[src]]
+        for d in deconvs:
+            if d.kind != "deconv2d" or d.bn is not None or self.cons.get(d.name, []) != [cat]:
+                return None
+            f = self._fmt(d)
+            if f[0] not in ("int8", "fp16"):
+                return None
+            v_in = self.values[self.layer_src[d.name][0]]
+            B, H, W, C = v_in.shape
+            _, Ho, Wo, Co = self.values[d.name].shape
+            k = d.weight.shape[2]
+            desc = N.ConvDesc(kind=N.PMX_DECONV2D, in_dtype=_DT[f[0]], batch=B, in_h=H, in_w=W, in_c=C, in_c_stride=C,
+                              in_c_offset=0, out_c=Co, k_h=k, k_w=k, stride_h=k, stride_w=k, pad_h=0, pad_w=0,
+                              out_h=Ho, out_w=Wo, relu=int(d.relu))
+            if not self.lib.pmx_deconv_heads_supported(ctypes.byref(desc)):
+                return None
+        order = sorted(deconvs, key=lambda d: self.graph.layers.index(d))
+        return {"deconvs": order, "concat": src, "heads": hs, "fmt": next(iter(fmts))}
+
     def _is_concat(self, name):
         for l in self.graph.layers:
             if l.name == name:
@@ -417,9 +489,20 @@ class CompiledGraph:
                 if v.shape != (B, H, W, c) or list(v.need) != [_F32]:
                     raise ValueError(f"head {name!r} has shape {v.shape}, expected {(B, H, W, c)}")
                 v.bufs[_F32] = (self.heads_cat, self.head_ctot, off)
+        if self.hfuse:
+            # the concat is virtual: the deconvs' epilogues feed the heads directly and
+            # accumulate int32 head partial sums here (20 per output pixel)
+            cv = self.values[self.hfuse["concat"]]
+            B, H, W, _ = cv.shape
+            self.head_partial = torch.empty((B, H, W, 20), dtype=torch.int32, device="cuda")
+            cv.need = {}
+            for d in self.hfuse["deconvs"]:
+                self.values[d.name].need = {}
         # concat buffers first; their inputs alias channel slices
         for l in self.graph.layers:
             if l.kind != "concat" or l.name not in self.values:
+                continue
+            if self.hfuse and l.name == self.hfuse["concat"]:
                 continue
             v = self.values[l.name]
             off = 0
@@ -579,8 +662,11 @@ class CompiledGraph:
             if l.name not in self.layer_src:
                 continue
             if fused and l in fused:
-                if l is fused[-1]:
+                if l is fused[-1] and not self.hfuse:
                     self._op_heads_fused(fused)
+                continue
+            if self.hfuse and l in self.hfuse["deconvs"]:
+                self._op_deconv_heads(l)
                 continue
             if l.is_weight_layer:
                 self._op_conv(l)
@@ -633,6 +719,46 @@ class CompiledGraph:
         self.ops.append(("conv heads(fused)", lambda s: N.check(lib.pmx_conv(
             ctypes.byref(d), t.data_ptr(), w.data_ptr(), N.ptr(alpha), bias.data_ptr(), None, arr, n, None, None, 0,
             s), "fused heads")))
+
+    def _op_deconv_heads(self, l):
+        """pmx_deconv_heads: deconv l + its concat slice of the three heads (K9+K10 fused)."""
+        torch = self.torch
+        lib = self.lib
+        hf = self.hfuse
+        stage = hf["deconvs"].index(l)
+        stage = 0 if stage == 0 else (2 if stage == len(hf["deconvs"]) - 1 else 1)
+        hs = self._fused_order if hasattr(self, "_fused_order") else hf["heads"]
+        recs = [self.weights[h.name] for h in hs]
+        if "w_all" not in hf:
+            hf["w_all"] = torch.cat([r["w"] for r in recs], dim=0).contiguous()  # [20, 384] int8 codes
+            hf["alpha"] = torch.cat([r["alpha"] for r in recs]).contiguous()
+            hf["bias"] = torch.cat([r["bias"] for r in recs]).contiguous()
+            self._keep += [hf["w_all"], hf["alpha"], hf["bias"]]
+        cat_in = self.layer_src[hf["concat"]]  # the concat's channel order
+        off = sum(self.values[n].shape[3] for n in cat_in[: cat_in.index(l.name)])
+        nh = hf["w_all"].shape[0]
+        wsl = torch.zeros((32, 128), dtype=torch.int8, device="cuda")
+        wsl[:nh] = hf["w_all"][:, off:off + 128]
+        rec = self.weights[l.name]
+        src, t, cs, coff = self._src_buf(l)
+        B, H, W, C = src.shape
+        _, Ho, Wo, Co = self.values[l.name].shape
+        k = l.weight.shape[2]
+        d = N.ConvDesc(kind=N.PMX_DECONV2D, in_dtype=_DT[rec["precision"]], batch=B, in_h=H, in_w=W, in_c=C,
+                       in_c_stride=cs, in_c_offset=coff, out_c=Co, k_h=k, k_w=k, stride_h=k, stride_w=k, pad_h=0,
+                       pad_w=0, out_h=Ho, out_w=Wo, relu=int(l.relu))
+        h = N.HeadFuse(w_codes=wsl.data_ptr(), n_heads=nh, stage=stage, in_scale=float(hf["fmt"][1]),
+                       partial=self.head_partial.data_ptr(), heads=self.heads_cat.data_ptr(),
+                       heads_c_stride=self.head_ctot, head_alpha=hf["alpha"].data_ptr(), head_bias=hf["bias"].data_ptr())
+        self._keep += [d, h, wsl]
+        esz = _ESZ[rec["precision"]]
+        px = B * Ho * Wo
+        self.op_info[f"conv {l.name}+heads"] = {
+            "flops": 2.0 * B * H * W * Co * k * k * C + 2.0 * px * nh * 128, "precision": rec["precision"],
+            "bytes": B * H * W * C * esz + Co * k * k * C * esz + px * 80 * (1 if stage == 0 else 2)}
+        self.ops.append((f"conv {l.name}+heads", lambda s: N.check(lib.pmx_deconv_heads(
+            ctypes.byref(d), t.data_ptr(), rec["w"].data_ptr(), N.ptr(rec["alpha"]), rec["bias"].data_ptr(),
+            ctypes.byref(h), s), f"layer {l.name} (+heads)")))
 
     def _op_input(self):
         v = self.input_value
@@ -746,11 +872,13 @@ class CompiledGraph:
         B, H, W, C = src.shape
         for f in out.need:
             t_in, cs, off = src.bufs[f]
-            if cs != C or off != 0:
+            if cs != _cstride(C, f) or off != 0:
                 raise NotImplementedError("upsample2x of a channel slice")
             t_out = out.bufs[f][0]
-            self.ops.append((f"upsample {l.name}", lambda s, a=t_in, b=t_out, dt=_DT[f[0]]: N.check(
-                lib.pmx_upsample2x(a.data_ptr(), dt, B, H, W, C, b.data_ptr(), s), "upsample2x")))
+            # fp32x2: both planes of a pixel are copied as one 2C-channel f32 row
+            dt, cc = (N.PMX_F32, 2 * C) if f[0] == "fp32x2" else (_DT[f[0]], C)
+            self.ops.append((f"upsample {l.name}", lambda s, a=t_in, b=t_out, dt=dt, cc=cc: N.check(
+                lib.pmx_upsample2x(a.data_ptr(), dt, B, H, W, cc, b.data_ptr(), s), "upsample2x")))
 
     def _op_decode(self):
         a = self.anchors
@@ -812,7 +940,7 @@ class CompiledGraph:
         torch.cuda.synchronize()
         for name, fn in self.ops:
             g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g, stream=st):
+            with _capturing(), torch.cuda.graph(g, stream=st):
                 sp = N.stream_ptr()
                 for _ in range(reps):
                     fn(sp)
@@ -849,8 +977,9 @@ class CompiledGraph:
         torch.cuda.current_stream().wait_stream(st)
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g, stream=st):
-            self.launch(st)
+        with _capturing():
+            with torch.cuda.graph(g, stream=st):
+                self.launch(st)
         self.graph_exec = g
         return g
 

@@ -1,60 +1,42 @@
-"""Per-layer roofline table from a bench.py JSON line and the engine's op_info.
+"""Per-layer roofline table from a bench.py JSON line.
 
-    python tools/layer_roofline.py profiles/r1_bench_latest.json > profiles/r1_layer_roofline.md
-FLOPs and algorithmic bytes (inputs once + outputs once per frame, weights ignored) are
-recomputed from the PointPillars shapes; peaks from MEASURED_PEAKS.json (int8 = 2x bf16)."""
+    python tools/layer_roofline.py gpurun_out/<tag>_bench.log > profiles/<round>_layer_roofline.md
+
+Uses the engine's own per-launch bookkeeping that bench.py records under
+roofline.per_layer (FLOPs; algorithmic bytes = each layer's input + weights + outputs
+once per step, as engine.CompiledGraph.op_info counts them) -- no name matching -- and
+the dense peaks bench.py used (roofline.peaks_tflops: measured tcgen05 MMA burst peaks)
+with the HBM bandwidth of MEASURED_PEAKS.json."""
 import json
 import sys
+from pathlib import Path
 
-B = 32
-H0, W0 = 248, 216  # block-0 / concat resolution
-LAYERS = {  # name: (M pixels per frame, N, K, precision, in bytes/elem, out bytes per pixel)
-    "conv backbone.blocks.0.0": (H0 * W0, 64, 9 * 64, "fp16", 2, 64),
-    "conv backbone.blocks.0.3": (H0 * W0, 64, 9 * 64, "int8", 1, 64),
-    "conv backbone.blocks.0.6": (H0 * W0, 64, 9 * 64, "int8", 1, 64),
-    "conv backbone.blocks.0.9": (H0 * W0, 64, 9 * 64, "int8", 1, 64 + 128),
-    "conv backbone.blocks.1.0": (124 * 108, 128, 9 * 64, "int8", 1, 128),
-    "conv backbone.blocks.1.3": (124 * 108, 128, 9 * 128, "int8", 1, 128),
-    "conv backbone.blocks.1.6": (124 * 108, 128, 9 * 128, "int8", 1, 128),
-    "conv backbone.blocks.1.9": (124 * 108, 128, 9 * 128, "int8", 1, 128),
-    "conv backbone.blocks.1.12": (124 * 108, 128, 9 * 128, "int8", 1, 128),
-    "conv backbone.blocks.1.15": (124 * 108, 128, 9 * 128, "int8", 1, 128 + 256),
-    "conv backbone.blocks.2.0": (62 * 54, 256, 9 * 128, "int8", 1, 256),
-    "conv backbone.blocks.2.3": (62 * 54, 256, 9 * 256, "int8", 1, 256),
-    "conv backbone.blocks.2.6": (62 * 54, 256, 9 * 256, "int8", 1, 256),
-    "conv backbone.blocks.2.9": (62 * 54, 256, 9 * 256, "int8", 1, 256),
-    "conv backbone.blocks.2.12": (62 * 54, 256, 9 * 256, "int8", 1, 256),
-    "conv backbone.blocks.2.15": (62 * 54, 256, 9 * 256, "int8", 1, 512),
-    "conv neck.deblocks.0.0": (H0 * W0, 128, 64, "fp16", 2, 128),
-    "conv neck.deblocks.1.0": (124 * 108, 4 * 128, 128, "fp16", 2, 4 * 128),
-    "conv neck.deblocks.2.0": (62 * 54, 16 * 128, 256, "fp16", 2, 16 * 128),
-    "conv heads(fused)": (H0 * W0, 20, 384, "int8", 1, 80),
-}
+ROOT = Path(__file__).resolve().parent.parent
 
 
 def main():
-    d = json.loads(open(sys.argv[1]).read().splitlines()[0])
-    per = d["roofline"]["per_layer_ms"]
-    peaks = {"fp16": 1599.3, "int8": 2 * 1599.3}
-    hbm = 6535.4
-    print("| layer | ms / 32 frames | TFLOP/s | % dtype peak | GB/s (alg.) | % HBM | bound | time / bound |")
-    print("|---|---|---|---|---|---|---|---|")
-    for name, ms in per.items():
-        M, N, K, prec, ein, outb = LAYERS[name]
-        flops = 2.0 * B * M * N * K
-        cin = K // 9 if name.startswith("conv backbone.") else K
-        # exact names (a suffix match would also catch the neck.deblocks.* layers)
-        stride2 = name in ("conv backbone.blocks.1.0", "conv backbone.blocks.2.0")
-        in_px = M * 4 if stride2 else M  # stride-2 convs read 4x their outputs
-        in_bytes = in_px * cin * ein
-        if name == "conv backbone.blocks.0.0":
-            in_bytes = 16000 * cin * ein  # the gather reads pillar rows, not a canvas
-        bytes_ = B * (in_bytes + M * outb)
-        t_c, t_m = flops / (peaks[prec] * 1e12), bytes_ / (hbm * 1e9)
+    line = next(ln for ln in open(sys.argv[1]) if ln.startswith("{"))
+    d = json.loads(line)
+    r = d["roofline"]
+    peaks = r["peaks_tflops"]
+    hbm = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"] if (ROOT / "MEASURED_PEAKS.json").exists() \
+        else 6535.4
+    print(f"Per-layer roofline, {d['config']['workload']} ({d['config'].get('plan')}), one step; peaks (TFLOP/s): "
+          f"{peaks}, HBM {hbm} GB/s\n")
+    print("| layer | precision | ms / step | TFLOP/s | % dtype peak | GB/s (alg.) | % HBM | bound | time / bound |")
+    print("|---|---|---|---|---|---|---|---|---|")
+    tot_t = tot_b = 0.0
+    for name, e in r["per_layer"].items():
+        s = e["ms"] / 1e3
+        pk = peaks.get(e["precision"], peaks.get("fp16"))
+        t_c, t_m = e["flops"] / (pk * 1e12), e["bytes"] / (hbm * 1e9)
         bound = "tensor" if t_c >= t_m else "hbm"
-        s = ms / 1e3
-        print(f"| {name} | {ms:.4f} | {flops / s / 1e12:.0f} | {100 * flops / s / 1e12 / peaks[prec]:.0f} | "
-              f"{bytes_ / s / 1e9:.0f} | {100 * bytes_ / s / 1e9 / hbm:.0f} | {bound} | {s / max(t_c, t_m):.2f} |")
+        tot_t += s
+        tot_b += max(t_c, t_m)
+        print(f"| {name} | {e['precision']} | {e['ms']:.4f} | {e['flops'] / s / 1e12:.0f} | "
+              f"{100 * e['flops'] / s / 1e12 / pk:.0f} | {e['bytes'] / s / 1e9:.0f} | "
+              f"{100 * e['bytes'] / s / 1e9 / hbm:.0f} | {bound} | {s / max(t_c, t_m):.2f} |")
+    print(f"| **sum** | | {tot_t * 1e3:.4f} | | | | | | {tot_t / tot_b:.2f} |")
 
 
 if __name__ == "__main__":
