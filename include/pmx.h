@@ -289,10 +289,11 @@ typedef struct {
   int32_t n_heads;          /* total head output channels, <= 20 (partial rows hold 20) */
   int32_t stage;            /* 0: write partial; 1: partial += ; 2: partial + this -> heads */
   double in_scale;          /* the heads' activation scale (codes = quantize(y, in_scale)) */
-  int32_t* partial;         /* int32 [B * out_h * out_w, 20] */
+  int32_t* partial;         /* int32 [ps, ps, B, out_h / ps, out_w / ps, 20]: output pixel
+                               (b, y, x) at [y % ps, x % ps, b, y / ps, x / ps] */
   float* heads;             /* stage 2: f32 NHWC [B * out_h * out_w, heads_c_stride] */
   int32_t heads_c_stride;
-  int32_t _pad;
+  int32_t part_stride;      /* ps: a power of two dividing out_h and out_w (the largest stride) */
   const float* head_alpha;  /* stage 2: f32(s_in * s_w[n]), [n_heads] */
   const float* head_bias;   /* stage 2: [n_heads] */
 } pmx_head_fuse;

@@ -64,7 +64,7 @@ class NmsDesc(C.Structure):
 
 class HeadFuse(C.Structure):
     _fields_ = [("w_codes", C.c_void_p), ("n_heads", C.c_int32), ("stage", C.c_int32), ("in_scale", C.c_double),
-                ("partial", C.c_void_p), ("heads", C.c_void_p), ("heads_c_stride", C.c_int32), ("_pad", C.c_int32),
+                ("partial", C.c_void_p), ("heads", C.c_void_p), ("heads_c_stride", C.c_int32), ("part_stride", C.c_int32),
                 ("head_alpha", C.c_void_p), ("head_bias", C.c_void_p)]
 
 

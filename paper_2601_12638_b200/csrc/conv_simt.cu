@@ -240,6 +240,9 @@ pmx_status pmx_deconv_heads(const pmx_conv_desc* desc, const void* x, const void
   PMX_REQUIRE(hf.n_heads >= 1 && hf.n_heads <= 20, "n_heads must be 1..20");
   PMX_REQUIRE(hf.stage >= 0 && hf.stage <= 2, "stage must be 0, 1 or 2");
   PMX_REQUIRE(hf.in_scale > 0.0, "heads' activation scale must be positive");
+  PMX_REQUIRE(hf.part_stride >= 1 && (hf.part_stride & (hf.part_stride - 1)) == 0 &&
+                  d.out_h % hf.part_stride == 0 && d.out_w % hf.part_stride == 0,
+              "part_stride must be a power of two dividing the output extents");
   PMX_REQUIRE(hf.stage != 2 || (hf.heads && hf.head_alpha && hf.head_bias && hf.heads_c_stride >= hf.n_heads),
               "the last stage needs heads, head_alpha, head_bias");
   if (d.batch == 0) return PMX_OK;

@@ -229,6 +229,10 @@ struct TcParams {
   // (N = 32 >= n_heads), and the int32 head partial sums go to hpart (stage 0 writes,
   // 1 accumulates, 2 accumulates and applies the heads' epilogue into hout)
   int hstage_mode, n_heads, hcs;
+  // partial layout: [ps][ps][B][out_h / ps][out_w / ps][20] -- the sub-pixel phase of the
+  // output pixel outermost (ps = the largest deconv stride), so every deconv's tile (one
+  // tap of consecutive input pixels) reads and writes contiguous runs of partials
+  int pshift, part_b;
   const int8_t* hwc;     // [32][128] int8 head weight codes of this slice (rows >= n_heads zero)
   int32_t* hpart;        // [pixels][n_heads]
   float* hout;           // stage 2: f32 heads [pixels][hcs]
@@ -632,14 +636,12 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int total = p.m_tiles * p.n_tiles;
   const int nk = p.taps * p.cblocks;
-  __shared__ uint64_t hbar_s[2];  // HEADS: head MMA done, per epilogue tile slot
+  __shared__ uint64_t hbar_s[4];  // HEADS: head MMA done, per (epilogue tile slot, buffer)
 
   if (threadIdx.x == 0) {
     PMX_TRACE(8, 0);
-    if (OUTK == 2) {
-      mbar_init(smem_u32(&hbar_s[0]), 1);
-      mbar_init(smem_u32(&hbar_s[1]), 1);
-    }
+    if (OUTK == 2)
+      for (int b = 0; b < 4; ++b) mbar_init(smem_u32(&hbar_s[b]), 1);
     for (int s = 0; s < p.stages; ++s) {
       mbar_init(full(s), GATHER ? 2 * 32 * kGatherWarps : 1);  // TMA: expect_tx; gather: 2 arrivals per thread
       mbar_init(empty(s), 1);
@@ -918,7 +920,7 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
         // head weights -> the B operand: 32 rows x 128 B, SW128 (16-byte chunk j of row r
         // at chunk j ^ (r & 7))
         const uint32_t hb = (s_estage + 1023u) & ~1023u;
-        const uint32_t s_hw = hb + 2u * 16384u;
+        const uint32_t s_hw = hb + 4u * 16384u;
         if (et < 32 * 8) {
           const int r = et >> 3, j = et & 7;
           const uint4 wv = *reinterpret_cast<const uint4*>(p.hwc + r * 128 + 16 * j);
@@ -936,9 +938,76 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
     const double o_scale = outs.o[0].scale;
     const float o_inv = outs.o[0].inv;
     const bool fast = OUTK == 1 && !p.bn_post && !p.keys && (p.n_gemm % 16) == 0;
+    // HEADS: wait for the head MMA of the slot's tile `ti`, then its partial sums (and the
+    // heads' epilogue in the last stage); every warp of the slot waits (its code stage is
+    // rewritten two tiles later), the column-half-0 warps do the memory work
+    auto heads_finish = [&](uint32_t ti) {
+      if constexpr (OUTK == 2) {
+        const uint32_t ilx = ti / (uint32_t)egn, bx = ilx & 1u;
+        mbar_wait(smem_u32(&hbar_s[eg * 2 + bx]), (ilx >> 1) & 1u);
+        tc_fence_after();
+        if (cg != 0) return;
+        const uint32_t t = blockIdx.x + ti * gridDim.x;
+        const uint32_t mt = fdiv(t, p.fd_nt), nt = t - mt * (uint32_t)p.n_tiles;
+        const uint32_t pin = mt * 128u + row;
+        const bool ok = pin < (uint32_t)p.m_total;
+        const uint32_t tt = fdiv(pin, p.fd_iw);
+        const uint32_t ixx = pin - tt * (uint32_t)p.in_w;
+        const uint32_t ibb = fdiv(tt, p.fd_ih);
+        const uint32_t iyy = tt - ibb * (uint32_t)p.in_h;
+        const uint32_t oy = iyy * (uint32_t)p.stride + (nt >> p.st_shift);
+        const uint32_t ox = ixx * (uint32_t)p.stride + (nt & (uint32_t)(p.stride - 1));
+        const uint32_t pm = (1u << p.pshift) - 1u;
+        const uint32_t ppix =
+            ((((oy & pm) << p.pshift | (ox & pm)) * (uint32_t)p.part_b + ibb) * ((uint32_t)p.out_h >> p.pshift) +
+             (oy >> p.pshift)) * ((uint32_t)p.out_w >> p.pshift) + (ox >> p.pshift);
+        int4 o4[5];
+        int4* pp = reinterpret_cast<int4*>(p.hpart + (size_t)ppix * 20u);
+        if (ok && p.hstage_mode != 0) {
+#pragma unroll
+          for (int u = 0; u < 5; ++u) o4[u] = pp[u];
+        }
+        const uint32_t hcol = tmem + p.hcol0 + 32u * ((uint32_t)eg * 2u + bx) + ((uint32_t)(q * 32) << 16);
+        uint32_t h0[16], h1[16];
+        tmem_ld16_issue(hcol, h0);
+        tmem_ld16_issue(hcol + 16u, h1);
+        tmem_ld_wait(h0);
+        tmem_ld_wait(h1);
+        tc_fence_before();
+        if (!ok) return;
+        int hs[20];
+#pragma unroll
+        for (int n = 0; n < 16; ++n) hs[n] = (int)h0[n];
+#pragma unroll
+        for (int n = 16; n < 20; ++n) hs[n] = (int)h1[n - 16];
+        if (p.hstage_mode != 0) {
+#pragma unroll
+          for (int u = 0; u < 5; ++u) {
+            hs[4 * u] += o4[u].x;
+            hs[4 * u + 1] += o4[u].y;
+            hs[4 * u + 2] += o4[u].z;
+            hs[4 * u + 3] += o4[u].w;
+          }
+        }
+        if (p.hstage_mode != 2) {
+#pragma unroll
+          for (int u = 0; u < 5; ++u) pp[u] = make_int4(hs[4 * u], hs[4 * u + 1], hs[4 * u + 2], hs[4 * u + 3]);
+        } else {
+          // the heads' epilogue: f32(acc) * alpha + bias in one rounding (the fused-heads
+          // kernel's formula, so the result is bit-identical)
+          const uint32_t opix = (ibb * (uint32_t)p.out_h + oy) * (uint32_t)p.out_w + ox;
+          float* ho = p.hout + (size_t)opix * (uint32_t)p.hcs;
+#pragma unroll
+          for (int n = 0; n < 20; ++n)
+            if (n < p.n_heads) ho[n] = __fmaf_rn((float)hs[n], __ldg(p.halpha + n), __ldg(p.hbias + n));
+        }
+      }
+    };
+    uint32_t i_last = 0xffffffffu;
     for (uint32_t i = (uint32_t)eg;; i += (uint32_t)egn) {
       const uint32_t t = blockIdx.x + i * gridDim.x;
       if (t >= (uint32_t)total) break;
+      i_last = i;
       const uint32_t acc = i & (uint32_t)(p.nacc - 1), aph = (i >> p.nacc_shift) & 1;
       const uint32_t mt = fdiv(t, p.fd_nt), nt = t - mt * (uint32_t)p.n_tiles;
       const int n0 = (int)nt * p.bn;
@@ -971,14 +1040,13 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
       // deconv: output pixel of tap (0, 0); tap (dy, dx) adds dy * out_w + dx
       const uint32_t pbase = (ib * p.out_h + iy * p.stride) * p.out_w + ix * p.stride;
       if constexpr (OUTK == 2) {
-        // ---- deconv + heads: one tile = one tap (bn = Cout = 128) of 128 input pixels
+        // ---- deconv + heads: one tile = one tap (bn = Cout = 128) of 128 input pixels.
+        // Software-pipelined per tile slot: the codes of tile i go to code stage (i & 1) and
+        // its head MMA to head accumulator (i & 1); the head results of the slot's previous
+        // tile are finished while that MMA runs
+        const uint32_t il = i / (uint32_t)egn, buf = il & 1u;
         const uint32_t hb = (s_estage + 1023u) & ~1023u;
-        const uint32_t st = hb + (uint32_t)eg * 16384u, s_hw = hb + 2u * 16384u;
-        const uint32_t hbar = smem_u32(&hbar_s[eg]);
-        const uint32_t hpar = (i / (uint32_t)egn) & 1u;
-        const int tap = (int)nt;
-        const uint32_t opix = pbase + (uint32_t)(tap >> p.st_shift) * (uint32_t)p.out_w +
-                              (uint32_t)(tap & (p.stride - 1));
+        const uint32_t st = hb + ((uint32_t)eg * 2u + buf) * 16384u, s_hw = hb + 4u * 16384u;
 #pragma unroll 1
         for (int k = 0; k < 4; ++k) {
           uint32_t v[16];
@@ -1006,60 +1074,22 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
         // codes -> async proxy, the slot's 8 warps meet, one thread issues the head MMA
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         asm volatile("bar.sync %0, 256;" ::"r"(2 + eg) : "memory");
-        const uint32_t hcol = tmem + p.hcol0 + 32u * (uint32_t)eg;
         if (cg == 0 && q == 0) {
           tc_fence_after();
           if (elect_one()) {
             const uint32_t ahi = (uint32_t)(sdesc(0, 1024u, 2u) >> 32);
+            const uint32_t hcol = tmem + p.hcol0 + 32u * ((uint32_t)eg * 2u + buf);
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
               const uint64_t ad = ((uint64_t)ahi << 32) | (uint32_t)sdesc(st + 32u * k, 1024u, 2u);
               const uint64_t bd = ((uint64_t)ahi << 32) | (uint32_t)sdesc(s_hw + 32u * k, 1024u, 2u);
               tc_mma<PMX_I8>(hcol, ad, bd, p.hidesc, k != 0);
             }
-            tc_commit(hbar);
+            tc_commit(smem_u32(&hbar_s[eg * 2 + buf]));
           }
           __syncwarp();
         }
-        mbar_wait(hbar, hpar);
-        tc_fence_after();
-        if (cg == 0) {
-          uint32_t h0[16], h1[16];
-          tmem_ld16_issue(hcol + ((uint32_t)(q * 32) << 16), h0);
-          tmem_ld16_issue(hcol + 16u + ((uint32_t)(q * 32) << 16), h1);
-          tmem_ld_wait(h0);
-          tmem_ld_wait(h1);
-          tc_fence_before();
-          if (valid) {
-            int hs[20];
-#pragma unroll
-            for (int n = 0; n < 16; ++n) hs[n] = (int)h0[n];
-#pragma unroll
-            for (int n = 16; n < 20; ++n) hs[n] = (int)h1[n - 16];
-            int4* pp = reinterpret_cast<int4*>(p.hpart + (size_t)opix * 20u);
-            if (p.hstage_mode != 0) {
-#pragma unroll
-              for (int u = 0; u < 5; ++u) {
-                const int4 o = pp[u];
-                hs[4 * u] += o.x;
-                hs[4 * u + 1] += o.y;
-                hs[4 * u + 2] += o.z;
-                hs[4 * u + 3] += o.w;
-              }
-            }
-            if (p.hstage_mode != 2) {
-#pragma unroll
-              for (int u = 0; u < 5; ++u) pp[u] = make_int4(hs[4 * u], hs[4 * u + 1], hs[4 * u + 2], hs[4 * u + 3]);
-            } else {
-              // the heads' epilogue: f32(acc) * alpha + bias in one rounding (the fused-heads
-              // kernel's formula, so the result is bit-identical)
-              float* ho = p.hout + (size_t)opix * (uint32_t)p.hcs;
-#pragma unroll
-              for (int n = 0; n < 20; ++n)
-                if (n < p.n_heads) ho[n] = __fmaf_rn((float)hs[n], __ldg(p.halpha + n), __ldg(p.hbias + n));
-            }
-          }
-        }
+        if (il > 0) heads_finish(i - (uint32_t)egn);
         continue;
       }
       if constexpr (OUTK == 0) {
@@ -1351,6 +1381,9 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
       if (warp == 0 && lane == 0) PMX_TRACE(7, i);
       if (lane == 0 && i == 6) PMX_TRACE(8, 9 + 2 * warp);
     }
+    if constexpr (OUTK == 2) {
+      if (i_last != 0xffffffffu) heads_finish(i_last);
+    }
     if (p.keys) block_minmax_commit<kThreads>(lo, hi, p.keys);
   }
   tc_fence_before();
@@ -1438,7 +1471,7 @@ int estage_min_row() {  // PMX_ESTAGE=2: stage every eligible layer (experiments
   return v;
 }
 
-constexpr uint32_t kHeadsSmem = 1024u + 2u * 16384u + 4096u;  // alignment + 2 code stages + head weights
+constexpr uint32_t kHeadsSmem = 1024u + 4u * 16384u + 4096u;  // alignment + 2 x 2 code stages + head weights
 
 Plan plan_for(const pmx_conv_desc& d, bool gather = false, bool want_stage = false, int out_row_bytes = 0,
               bool want_stage2 = false, bool heads = false) {
@@ -1534,7 +1567,7 @@ Plan plan_for(const pmx_conv_desc& d, bool gather = false, bool want_stage = fal
   p.nacc_shift = __builtin_ctz((unsigned)p.nacc);
   p.egroups = bn <= 64 ? 4 : (bn <= 128 ? 2 : 1);
   if (p.egroups > p.nacc) p.egroups = p.nacc;
-  p.hcol0 = (uint32_t)(p.nacc * p.acc_stride);  // HEADS: 32 columns per tile slot after the accumulators
+  p.hcol0 = (uint32_t)(p.nacc * p.acc_stride);  // HEADS: 2 x 32 columns per tile slot after the accumulators
   if (heads) want_stage = want_stage2 = false;
   // (measured: a win for 128- and 384-byte output rows -- deconvs into the concat,
   // blocks.1.0 -- a loss for the 64-byte rows of block 0, which are MMA-bound)
@@ -1621,7 +1654,7 @@ Plan plan_for(const pmx_conv_desc& d, bool gather = false, bool want_stage = fal
   p.fd_oc = make_fastdiv((uint32_t)d.out_c);
   // as many TMEM accumulators as fit (a power of two, 2..8): the MMA warp runs ahead
   // of the epilogue; the epilogue drains up to 4 tiles at once (tile slots)
-  const int cols = p.nacc * p.acc_stride + (heads ? 64 : 0);
+  const int cols = p.nacc * p.acc_stride + (heads ? 128 : 0);
   p.tmem_cols = cols <= 32 ? 32 : (cols <= 64 ? 64 : (cols <= 128 ? 128 : (cols <= 256 ? 256 : 512)));
   const uint32_t m_enc = 128u >> 4, n_enc = (uint32_t)bn >> 3;
   if (d.in_dtype == PMX_I8)
@@ -1861,6 +1894,8 @@ pmx_status conv_tc_deconv_heads(const pmx_conv_desc& d, const void* x, const voi
   p.hbias = hf.head_bias;
   p.hscale = hf.in_scale;
   p.hinv = (float)(1.0 / hf.in_scale);
+  p.part_b = d.batch;
+  p.pshift = __builtin_ctz((unsigned)hf.part_stride);
   Outs outs{};
   outs.n = 0;
   auto launch = [&](auto kern) -> pmx_status {

@@ -457,8 +457,16 @@ class CompiledGraph:
                               out_h=Ho, out_w=Wo, relu=int(d.relu))
             if not self.lib.pmx_deconv_heads_supported(ctypes.byref(desc)):
                 return None
-        order = sorted(deconvs, key=lambda d: self.graph.layers.index(d))
-        return {"deconvs": order, "concat": src, "heads": hs, "fmt": next(iter(fmts))}
+        # all three run once the last of their inputs exists, largest stride first: the
+        # partial sums live in that deconv's sub-pixel-phase layout, and the stride-1 one
+        # finishes the heads into the NHWC heads block with contiguous rows
+        order = sorted(deconvs, key=lambda d: (-d.weight.shape[2], self.graph.layers.index(d)))
+        ps = order[0].weight.shape[2]
+        _, Ho, Wo, _ = self.values[src].shape
+        if ps & (ps - 1) or Ho % ps or Wo % ps:
+            return None
+        last = max(deconvs, key=lambda d: self.graph.layers.index(d))
+        return {"deconvs": order, "concat": src, "heads": hs, "fmt": next(iter(fmts)), "ps": ps, "emit_at": last}
 
     def _is_concat(self, name):
         for l in self.graph.layers:
@@ -666,7 +674,9 @@ class CompiledGraph:
                     self._op_heads_fused(fused)
                 continue
             if self.hfuse and l in self.hfuse["deconvs"]:
-                self._op_deconv_heads(l)
+                if l is self.hfuse["emit_at"]:
+                    for d in self.hfuse["deconvs"]:
+                        self._op_deconv_heads(d)
                 continue
             if l.is_weight_layer:
                 self._op_conv(l)
@@ -749,7 +759,8 @@ class CompiledGraph:
                        pad_w=0, out_h=Ho, out_w=Wo, relu=int(l.relu))
         h = N.HeadFuse(w_codes=wsl.data_ptr(), n_heads=nh, stage=stage, in_scale=float(hf["fmt"][1]),
                        partial=self.head_partial.data_ptr(), heads=self.heads_cat.data_ptr(),
-                       heads_c_stride=self.head_ctot, head_alpha=hf["alpha"].data_ptr(), head_bias=hf["bias"].data_ptr())
+                       heads_c_stride=self.head_ctot, part_stride=hf["ps"], head_alpha=hf["alpha"].data_ptr(),
+                       head_bias=hf["bias"].data_ptr())
         self._keep += [d, h, wsl]
         esz = _ESZ[rec["precision"]]
         px = B * Ho * Wo

@@ -71,7 +71,15 @@ def test_fused_heads_captured_graph_replays(pm):
     graph = pm.build_pointpillars(cfg, seed=10)
     stats = pm.calibrate_frames(graph, [pm.make_frame(3000, 61, cfg)], cfg)
     batches = [[pm.make_frame(2000 + 300 * j + 50 * i, 70 + 10 * j + i, cfg) for i in range(2)] for j in range(3)]
-    eng = pm.PointPillarsEngine(graph, pm.MIXED_PLAN_LABEL, stats, cfg, batch=2, max_points_per_frame=3000)
+    old = os.environ.get("PMX_FUSE_HEADS")
+    os.environ["PMX_FUSE_HEADS"] = "1"
+    try:
+        eng = pm.PointPillarsEngine(graph, pm.MIXED_PLAN_LABEL, stats, cfg, batch=2, max_points_per_frame=3000)
+    finally:
+        if old is None:
+            del os.environ["PMX_FUSE_HEADS"]
+        else:
+            os.environ["PMX_FUSE_HEADS"] = old
     assert eng.cg.hfuse is not None
     eng.capture()
     for fr in batches:

@@ -1,3 +1,2 @@
 #!/bin/bash
-export PMX_FUSE_HEADS=1
-KEEP_REP=0 bash tools/ncu_ops.sh r2m "conv neck.deblocks.2.0+heads" "conv neck.deblocks.0.0+heads"
+KEEP_REP=0 bash tools/ncu_ops.sh r2q "conv backbone.blocks.1.3" "conv backbone.blocks.2.3" "conv backbone.blocks.0.3"
