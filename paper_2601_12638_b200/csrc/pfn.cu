@@ -244,7 +244,10 @@ constexpr size_t pfn_points_smem() {
 }
 
 template <int DT>
-__global__ void __launch_bounds__(kThreads, 2) pfn_points_kernel(const PfnArgs a, const Outs outs) {
+#ifndef PMX_PFN_MINB
+#define PMX_PFN_MINB 2
+#endif
+__global__ void __launch_bounds__(kThreads, PMX_PFN_MINB) pfn_points_kernel(const PfnArgs a, const Outs outs) {
   pdl_begin();
   using R = Rec<DT>;
   using T = typename R::T;
@@ -410,7 +413,9 @@ __global__ void __launch_bounds__(kThreads, 2) pfn_points_kernel(const PfnArgs a
     if (kpair == 0) continue;  // warp-uniform
     const int64_t qj = __shfl_sync(0xffffffffu, q, j);
     float m[4] = {-INF, -INF, -INF, -INF};
-    auto point = [&](const float (&f)[9]) {
+    // live: this half's pillar holds the point (the loop runs to the pair's max count
+    // without diverging; a dead slot's products are computed and discarded)
+    auto point = [&](const float (&f)[9], bool live) {
       float2 acc01 = make_float2(0.f, 0.f), acc23 = make_float2(0.f, 0.f);
 #pragma unroll
       for (int t = 0; t < 9; ++t) {
@@ -419,9 +424,10 @@ __global__ void __launch_bounds__(kThreads, 2) pfn_points_kernel(const PfnArgs a
       }
       const float acc[4] = {acc01.x, acc01.y, acc23.x, acc23.y};
       if (a.bn_post == nullptr) {
+        // NaN-propagating max (max.NaN): a NaN product reaches the canvas like numpy's max
 #pragma unroll
-        for (int u = 0; u < 4; ++u) m[u] = nmax(m[u], acc[u]);
-      } else {  // unfolded BN may have a negative gamma: finish every point
+        for (int u = 0; u < 4; ++u) m[u] = live ? fmax_nan(m[u], acc[u]) : m[u];
+      } else if (live) {  // unfolded BN may have a negative gamma: finish every point
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           float y;
@@ -435,14 +441,13 @@ __global__ void __launch_bounds__(kThreads, 2) pfn_points_kernel(const PfnArgs a
       }
     };
     const int kk = kpair < kSlots ? kpair : kSlots;
-    for (int s2 = 0; s2 < kk; ++s2) {
-      if (s2 >= kj) continue;
+    for (int s2 = 0; s2 < kk; ++s2) {  // warp-uniform trip count
       float f[9];
       const float4* src = reinterpret_cast<const float4*>(sf[warp][j][s2]);  // two broadcast addresses
       const float4 f0 = src[0], f1 = src[1], f2 = src[2];
       f[0] = f0.x; f[1] = f0.y; f[2] = f0.z; f[3] = f0.w; f[4] = f1.x; f[5] = f1.y; f[6] = f1.z; f[7] = f1.w;
       f[8] = f2.x;
-      point(f);
+      point(f, s2 < kj);
     }
     if (kpair > kSlots) {  // dense cluster: rebuild the remaining points (broadcast loads per half)
       const float* mt = smeta[warp][j];
@@ -456,7 +461,7 @@ __global__ void __launch_bounds__(kThreads, 2) pfn_points_kernel(const PfnArgs a
         f[7] = __fsub_rn(pt.x, mt[3]); f[8] = __fsub_rn(pt.y, mt[4]);
 #pragma unroll
         for (int t = 0; t < 9; ++t) f[t] = transform_in<DT>(f[t], a);
-        point(f);
+        point(f, true);
       }
     }
     // every lane takes part in the shuffle (the halves' pillars may differ in liveness:
