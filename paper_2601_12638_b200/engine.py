@@ -684,6 +684,7 @@ class CompiledGraph:
                 self._op_upsample(l)
         if self.anchors is not None:
             self._op_decode()
+        self._plan_branches()
 
     def _fusable_heads(self):
         """cls/box/dir heads -> one GEMM (N = 10A) writing the heads block, when they are
@@ -913,10 +914,57 @@ class CompiledGraph:
 
     # ---------------- execution
 
+    def _plan_branches(self):
+        """Small batches leave SMs idle: run the neck deconvolutions of blocks 0 and 1 on a
+        side stream (a fork after the block's last conv, a join before the heads) so they
+        overlap the next blocks' convolutions.  PMX_NECK_STREAM=0/1 forces it off/on."""
+        import os
+
+        self.branch_src, self.joins = {}, {}
+        mode = os.environ.get("PMX_NECK_STREAM", "auto")
+        if mode == "0" or (mode == "auto" and self.B > 8) or self.anchors is None or self.hfuse:
+            return
+        names = [n for n, _ in self.ops]
+        head_op = "conv heads(fused)"
+        if head_op not in names:
+            return
+        deconvs = [l for l in self.graph.layers if l.kind == "deconv2d" and f"conv {l.name}" in names]
+        if not deconvs:
+            return
+        last_src = max(names.index(f"conv {self.layer_src[d.name][0]}") for d in deconvs
+                       if f"conv {self.layer_src[d.name][0]}" in names)
+        for d in deconvs:
+            src = f"conv {self.layer_src[d.name][0]}"
+            if src in names and names.index(src) < last_src:  # the last one gains nothing
+                self.branch_src[f"conv {d.name}"] = src
+        if self.branch_src:
+            self.joins[head_op] = list(self.branch_src)
+            torch = self.torch
+            self.side_stream = torch.cuda.Stream()
+            self.branch_ev = {n: torch.cuda.Event() for n in set(self.branch_src.values()) | set(self.branch_src)}
+
     def launch(self, stream=None):
-        s = N.stream_ptr(stream)
-        for _, fn in self.ops:
-            fn(s)
+        if not getattr(self, "branch_src", None):
+            s = N.stream_ptr(stream)
+            for _, fn in self.ops:
+                fn(s)
+            return
+        torch = self.torch
+        main = stream if stream is not None else torch.cuda.current_stream()
+        s = N.stream_ptr(main)
+        side = self.side_stream
+        forks = set(self.branch_src.values())
+        for name, fn in self.ops:
+            for b in self.joins.get(name, ()):
+                main.wait_event(self.branch_ev[b])
+            if name in self.branch_src:
+                side.wait_event(self.branch_ev[self.branch_src[name]])
+                fn(N.stream_ptr(side))
+                self.branch_ev[name].record(side)
+            else:
+                fn(s)
+                if name in forks:
+                    self.branch_ev[name].record(main)
 
     def timed_launch(self, reps: int = 5) -> dict:
         """Eager launch with CUDA events around every op on the current stream -> mean ms per op."""
