@@ -327,14 +327,16 @@ def main():
         # DRAM traffic of the same 20 conv launches (one step, batch 32) from the committed ncu
         # capture (tools/traffic.py) next to their algorithmic bytes
         traffic = None
-        tf = ROOT / "profiles" / "r1_step_traffic.json"
+        tf = ROOT / "profiles" / "r2_step_traffic.json"
+        if not tf.exists():
+            tf = ROOT / "profiles" / "r1_step_traffic.json"
         if tf.exists():
             traffic = json.loads(tf.read_text()).get("conv_dram_bytes")
         alg_bytes = sum(info[k].get("bytes", 0) for k in info)
         roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                     "frac": achieved / peak, "traffic": traffic,
-                    "traffic_note": "bytes per step: DRAM read+write of the 20 conv launches (ncu, "
-                                    "profiles/r1_step_traffic.json) vs algorithmic_bytes (each layer's input + "
+                    "traffic_note": f"bytes per step: DRAM read+write of the conv launches (ncu, "
+                                    f"profiles/{tf.name}) vs algorithmic_bytes (each layer's input + "
                                     "weights + outputs once)",
                     "algorithmic_bytes": alg_bytes,
                     "kernel": "pmx_conv implicit GEMM, all 20 conv/deconv/head launches of a step",

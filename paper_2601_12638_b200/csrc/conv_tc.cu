@@ -1456,6 +1456,14 @@ uint32_t halo_swz_width() {  // PMX_HSWZ_W: swizzled halo row width in pixels (1
   return v;
 }
 
+int lat_tiles() {
+  static const int v = [] {
+    const char* e = getenv("PMX_LAT_TILES");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
 bool estage_enabled() {
   static const bool on = [] {
     const char* e = getenv("PMX_ESTAGE");
@@ -1590,7 +1598,12 @@ Plan plan_for(const pmx_conv_desc& d, bool gather = false, bool want_stage = fal
   if (stages < 2) stages = 2;
   p.stages = stages;
   p.bres_bytes = 0;
-  if (conv3 && !x3 && g_conv_backend_mode != 2 && cin_bytes == kc_bytes && p.n_tiles == 1 && d.out_w >= 8) {
+  // few tiles per CTA (small batches): the resident-weight halo kernel loads every tap's
+  // weights before its first MMA; the per-K-block ring streams them behind the MMAs
+  // instead.  PMX_LAT_TILES = the tiles-per-SM threshold (0: always the halo kernel)
+  const bool latency_mode = !gather && (int64_t)p.m_tiles * p.n_tiles <= (int64_t)lat_tiles() * num_sms();
+  if (conv3 && !x3 && !latency_mode && g_conv_backend_mode != 2 && cin_bytes == kc_bytes && p.n_tiles == 1 &&
+      d.out_w >= 8) {
     // stride 1: one (16 + 2) x (8 + 2) halo; stride 2: four parity planes of
     // (16 + py) x (8 + px) pixels (561 in total) -- see the producer
     // stride 1, 64 / 128 channel bytes: swizzled pixel-major halo 16 x 18 (PMX_HALO_SWZ=0: off)
@@ -1667,6 +1680,16 @@ Plan plan_for(const pmx_conv_desc& d, bool gather = false, bool want_stage = fal
             8 * (size_t)((d.out_c + 3) & ~3) + (gather ? kGatherSmem : 0) + (estage_bytes ? 16 + estage_bytes : 0) +
             (heads ? 16 + kHeadsSmem : 0);
   p.hidesc = (2u << 4) | (1u << 7) | (1u << 10) | ((32u >> 3) << 17) | ((128u >> 4) << 24);  // s32 <- s8 x s8, N 32
+  // experiment (PMX_GRID_DIV=d): at small tile counts use num_sms / d persistent CTAs, so
+  // the next layer's CTAs find free SMs and run their prologue under this layer
+  {
+    static const int div = [] {
+      const char* e = getenv("PMX_GRID_DIV");
+      return e ? atoi(e) : 1;
+    }();
+    const int64_t tl = (int64_t)p.m_tiles * p.n_tiles;
+    if (div > 1 && !gather && tl <= 4LL * num_sms() && pl.grid_x > num_sms() / div) pl.grid_x = num_sms() / div;
+  }
   pl.ok = true;
   return pl;
 }

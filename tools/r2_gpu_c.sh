@@ -1,8 +1,3 @@
 #!/bin/bash
-T=${1:-r2}
-export PMX_NO_BUILD=1
 mkdir -p gpurun_out
-timeout 1500 python -m pytest tests -m gpu -q -x > gpurun_out/${T}_tests.log 2>&1
-echo "rc=$?" >> gpurun_out/${T}_tests.log
-timeout 600 python bench.py --steps 30 --warmup 5 --no-cpu-baseline > gpurun_out/${T}_base.log 2>&1
-PMX_NECK_STREAM=0 timeout 600 python bench.py --steps 30 --warmup 5 --no-cpu-baseline > gpurun_out/${T}_noneck.log 2>&1
+nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/mma_micro tools/mma_micro.cu && timeout 120 /tmp/mma_micro > gpurun_out/r2_mma_micro.txt 2>&1
