@@ -248,37 +248,51 @@ class PointPillarsEngine:
 
 class PipelinedEngine:
     """Host-to-device streaming around a PointPillarsEngine: two input slots (points +
-    frame offsets) with one captured CUDA graph each; while the graph of batch i runs
-    on the compute stream, the pinned-host copy of batch i+1 lands in the other slot on
-    an H2D stream and the top-k records of batch i-1 go back on a D2H stream (the
-    copy engines overlap the SMs).  Every batch's H2D and D2H still happen."""
+    frame offsets) with one captured CUDA graph each; while the graph of batch i runs,
+    the pinned-host copy of batch i+1 lands in the other slot on an H2D stream and the
+    top-k records of batch i-1 go back on a D2H stream (the copy engines overlap the
+    SMs).  Every batch's H2D and D2H still happen.
 
-    def __init__(self, eng: "PointPillarsEngine"):
+    With a second engine (``eng2``, same graph / plan / stats / batch, its own
+    activation buffers) slot 1 runs on that engine and each slot replays on its own
+    compute stream, so consecutive batches overlap on the SMs as well (one kernel's
+    tail and the next kernel's launch of one batch are filled by the other's)."""
+
+    def __init__(self, eng: "PointPillarsEngine", eng2: "PointPillarsEngine | None" = None):
         import torch
 
         self.eng = eng
-        cg = eng.cg
-        # slot 1 starts as a copy of slot 0: capture() warms up on whatever the slot holds;
-        # each slot's graph also writes its own top-k records buffer (read back D2H)
-        rec0 = getattr(cg, "records", None)
-        self.slots = [(cg.points, cg.offsets, rec0),
-                      (cg.points.clone(), cg.offsets.clone(), None if rec0 is None else rec0.clone())]
-        self.graphs = []
-        for pts, offs, rec in self.slots:
-            cg.points, cg.offsets = pts, offs
-            if rec is not None:
-                cg.records = rec
-            self.graphs.append(cg.capture())
-        cg.points, cg.offsets = self.slots[0][:2]
-        if rec0 is not None:
-            cg.records = rec0
-        cg.graph_exec = self.graphs[0]
+        self.engines = [eng, eng2 if eng2 is not None else eng]
+        if eng2 is not None and (eng2.batch != eng.batch or eng2.nmax != eng.nmax):
+            raise ValueError("the two engines of a PipelinedEngine need the same batch and point capacity")
+        self.slots, self.graphs = [], []
+        for k, e in enumerate(self.engines):
+            cg = e.cg
+            # a shared engine's slot 1 starts as a copy of slot 0 (capture() warms up on whatever
+            # the slot holds); each slot's graph writes its own top-k records buffer (read back D2H)
+            rec0 = getattr(cg, "records", None)
+            if k == 1 and eng2 is None:
+                pts, offs = cg.points.clone(), cg.offsets.clone()
+                rec = None if rec0 is None else rec0.clone()
+                keep = (cg.points, cg.offsets, rec0)
+                cg.points, cg.offsets = pts, offs
+                if rec is not None:
+                    cg.records = rec
+                self.graphs.append(cg.capture())
+                cg.points, cg.offsets = keep[0], keep[1]
+                if rec0 is not None:
+                    cg.records = rec0
+                cg.graph_exec = self.graphs[0]
+                self.slots.append((pts, offs, rec))
+            else:
+                self.graphs.append(cg.capture())
+                self.slots.append((cg.points, cg.offsets, rec0))
         self.h2d = torch.cuda.Stream()
         self.d2h = torch.cuda.Stream()
+        self.comp = [None, torch.cuda.Stream() if eng2 is not None else None]
         self.copied = [torch.cuda.Event(), torch.cuda.Event()]
         self.done = [torch.cuda.Event(), torch.cuda.Event()]
         self.fetched = [torch.cuda.Event(), torch.cuda.Event()]
-        self._pending = 0
 
     def _upload(self, i: int, host_points, host_offsets):
         import torch
@@ -298,13 +312,20 @@ class PipelinedEngine:
         (written inside the graph), or pack(topk) when a pack function is given."""
         import torch
 
-        comp = torch.cuda.current_stream()
+        main = torch.cuda.current_stream()
+        comps = [main if c is None else c for c in self.comp]
+        start = torch.cuda.Event()
+        start.record(main)
+        for c in comps:
+            if c is not main:
+                c.wait_event(start)
         n = len(batches)
         if n == 0:
             return
         self._upload(0, *batches[0])
         for i in range(n):
             slot = i % 2
+            comp = comps[slot]
             if i + 1 < n:
                 self._upload(i + 1, *batches[i + 1])
             comp.wait_event(self.copied[slot])
@@ -312,12 +333,16 @@ class PipelinedEngine:
                 # batch i-2's D2H copy (d2h stream) must have finished reading this slot's
                 # records buffer before the graph rewrites it
                 comp.wait_event(self.fetched[slot])
-            self.graphs[slot].replay()
-            rec = pack(self.eng.topk()) if pack is not None else self.slots[slot][2]
-            self.done[slot].record(comp)
+            with torch.cuda.stream(comp):
+                self.graphs[slot].replay()
+                rec = pack(self.engines[slot].topk()) if pack is not None else self.slots[slot][2]
+                self.done[slot].record(comp)
             with torch.cuda.stream(self.d2h):
                 self.d2h.wait_event(self.done[slot])
                 host_out[i].copy_(rec, non_blocking=True)
                 rec.record_stream(self.d2h)
                 self.fetched[slot].record(self.d2h)
-        comp.wait_stream(self.d2h)
+        for c in comps:
+            if c is not main:
+                main.wait_stream(c)
+        main.wait_stream(self.d2h)

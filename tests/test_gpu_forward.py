@@ -339,6 +339,38 @@ def test_pipelined_engine_batch1_many_distinct_frames(pm):
             assert torch.equal(o, w), j
 
 
+def test_pipelined_two_engines_match_sequential(pm):
+    """PipelinedEngine over two engine instances (own buffers, one compute stream each:
+    consecutive batches overlap on the SMs) returns every batch's own records."""
+    import torch
+
+    from paper_2601_12638_b200 import distributed as D
+
+    cfg = pm.PointPillarsConfig.small(max_pillars=1500)
+    graph = pm.build_pointpillars(cfg, seed=6)
+    stats = pm.calibrate_frames(graph, [pm.make_frame(3000, 800 + i, cfg) for i in range(2)], cfg)
+    batches_np = [[pm.make_frame(1800 + 90 * j + 40 * i, 900 + 10 * j + i, cfg) for i in range(2)] for j in range(9)]
+    e1 = pm.PointPillarsEngine(graph, pm.MIXED_PLAN_LABEL, stats, cfg, batch=2, max_points_per_frame=3000)
+    e2 = pm.PointPillarsEngine(graph, pm.MIXED_PLAN_LABEL, stats, cfg, batch=2, max_points_per_frame=3000)
+    want = []
+    for fr in batches_np:
+        e1.load_points(fr)
+        e1.run()
+        want.append(D.pack_topk(e1.topk()).cpu())
+    pipe = pm.PipelinedEngine(e1, e2)
+    batches = []
+    for fr in batches_np:
+        offs = np.zeros(3, np.int64)
+        offs[1:] = np.cumsum([len(f) for f in fr])
+        batches.append((torch.from_numpy(np.concatenate(fr)).pin_memory(), torch.from_numpy(offs).pin_memory()))
+    for _ in range(2):
+        outs = [torch.empty_like(w).pin_memory() for w in want]
+        pipe.run(batches, outs)
+        torch.cuda.synchronize()
+        for j, (o, w) in enumerate(zip(outs, want)):
+            assert torch.equal(o, w), j
+
+
 def test_int8_plan_tcgen05_equals_simt_end_to_end(pm):
     """All-INT8 plan, two full-size KITTI frames: every conv through the tcgen05 kernels
     (swizzled halos, cp.async gather, staged stores, fused heads) vs every conv through

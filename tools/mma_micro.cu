@@ -39,7 +39,7 @@ __global__ void mma_bench(int n_mma, uint32_t idesc, uint32_t layout, uint32_t s
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = tslot;
   if (threadIdx.x == 0) {
-    const uint32_t step = vary == 1 ? 32u : (vary == 2 ? 16u : (vary == 3 ? 512u : 1024u));
+    const uint32_t step = vary == 1 ? 32u : (vary == 2 ? 16u : (vary == 3 ? 512u : (vary == 5 ? 64u : (vary == 6 ? 128u : 1024u))));
     uint64_t ad[9], bd[9];
 #pragma unroll
     for (int j = 0; j < 9; ++j) {
@@ -83,9 +83,11 @@ int main() {
   Cfg cfgs[] = {{2, 1024, 16, 0, "SW128 fixed"}, {2, 1024, 16, 1, "SW128 vary+32B"}, {4, 512, 16, 0, "SW64 fixed"},
                 {0, 128, 2048, 0, "NONE sbo128"}, {0, 160, 2880, 0, "NONE sbo160 lbo2880"},
                 {0, 160, 2880, 2, "NONE sbo160 vary+16B"},
-                {4, 512, 16, 3, "SW64 vary+512B"}, {2, 1024, 16, 4, "SW128 vary+1024B"}, {0, 128, 1024, 3, "NONE sbo128 vary+512B"}};
-  for (int kind = 0; kind < 2; ++kind)
-    for (int N : {64, 128, 256})
+                {4, 512, 16, 3, "SW64 vary+512B"}, {2, 1024, 16, 4, "SW128 vary+1024B"}, {0, 128, 1024, 3, "NONE sbo128 vary+512B"},
+                {4, 512, 16, 5, "SW64 vary+64B (row)"}, {4, 1024, 16, 5, "SW64 sbo1024 vary+64B"},
+                {2, 1024, 16, 6, "SW128 vary+128B (row)"}, {2, 2048, 16, 6, "SW128 sbo2048 vary+128B"}};
+  for (int kind = 0; kind < 1; ++kind)
+    for (int N : {64, 128})
       for (const Cfg& c : cfgs) {
         const int lay = c.lay;
         uint32_t idesc = kind == 0 ? ((2u << 4) | (1u << 7) | (1u << 10)) : (1u << 4);

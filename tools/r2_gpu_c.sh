@@ -1,3 +1,7 @@
 #!/bin/bash
+export PMX_NO_BUILD=1
 mkdir -p gpurun_out
-nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/mma_micro tools/mma_micro.cu && timeout 120 /tmp/mma_micro > gpurun_out/r2_mma_micro.txt 2>&1
+timeout 900 python -m pytest tests/test_gpu_forward.py -m gpu -q -x -k "pipelined" > gpurun_out/r3d_tests.log 2>&1
+echo "rc=$?" >> gpurun_out/r3d_tests.log
+timeout 600 python bench.py --steps 30 --warmup 5 --no-latency --no-cpu-baseline > gpurun_out/r3d_b2.log 2>&1
+timeout 600 python bench.py --steps 30 --warmup 5 --no-latency --no-cpu-baseline --inflight 1 > gpurun_out/r3d_b1.log 2>&1
