@@ -306,6 +306,7 @@ struct TcMaps {
 // HIGHEST id first, so the latency-critical single-thread roles get the top ids:
 // warps 0..15 epilogue (warp & 3 = TMEM lane quarter), 16 TMA producer (GATHER: a
 // halo builder), 17 MMA issuer, 18..19 the other GATHER halo builders.
+constexpr uint32_t kHaloW = 16;  // swizzled stride-1 halo row width (pixels)
 constexpr int kEpiWarps = 16;
 constexpr int kProdWarp = 16;
 constexpr int kMmaWarp = 17;
@@ -702,6 +703,15 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
           const int oy0 = (tq - tb * p.tiles_y) * p.th, ox0 = tx * p.tw;
           PMX_TRACE(0, it);
           mbar_wait(empty(s), ph ^ 1);
+#if defined(PMX_ABLATE) && PMX_ABLATE == 4
+          // diagnostic: after the first ring of halos, no more TMA traffic (stale data)
+          if ((int)it >= p.stages) {
+            mbar_arrive(full(s));
+            PMX_TRACE(1, it);
+            if (++s == (uint32_t)p.stages) s = 0, ph ^= 1;
+            continue;
+          }
+#endif
           mbar_expect_tx(full(s), p.halo_tx);
           const uint32_t slot = a_smem + s * p.a_bytes;
           if (p.stride == 1) {
@@ -776,6 +786,15 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
       constexpr int CB = CINB / KCB;
       const uint32_t bblk = p.bblk_bytes;
       const uint32_t b_hi = (uint32_t)(sdesc(0, p.sbo, p.layout) >> 32), b_lo0 = (uint32_t)sdesc(bres, p.sbo, p.layout);
+      // resident weights: the B descriptor of every (tap, 32-byte K step), hoisted out of
+      // the tile loop
+      uint32_t b_lo_tap[9 * (CINB / 32)];
+#pragma unroll
+      for (int tap = 0; tap < 9; ++tap)
+#pragma unroll
+        for (int k = 0; k < CINB / 32; ++k)
+          b_lo_tap[tap * (CINB / 32) + k] =
+              b_lo0 + (((uint32_t)(tap * CB + (k * 32) / KCB) * bblk + (uint32_t)((k * 32) % KCB)) >> 4);
       mbar_wait(bfull, 0);
       tc_fence_after();
       if (lane == 0) PMX_TRACE(8, 2);
@@ -794,24 +813,21 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
           if (elect_one()) {
             // pixel-major halo rows of CINB bytes (SW128 / SW64, TMA-swizzled by address):
             // tap (dy, dx) starts at halo pixel (dy + 1) * 16 + dx + 1; 8-row groups are
-            // 16 pixels = whole swizzle patterns apart; the start's pattern phase goes in
-            // the descriptor's base offset
-            const uint32_t sbase = a_smem + s * p.a_bytes;
+            // 16 pixels = whole swizzle patterns apart (the swizzle follows the absolute
+            // address, base offset 0).  Every descriptor is the stage's base plus a
+            // compile-time offset: the issue path is one add per MMA (the per-MMA address
+            // arithmetic it replaced made the MMA warp issue-bound, ~80 cycles per MMA)
             constexpr uint32_t lay = CINB == 128 ? 2u : 4u;
-            const uint32_t hi0 = (uint32_t)(p.hw * CINB) >> 4 | (1u << 14) | (lay << 29);
+            constexpr uint32_t a_hi = (kHaloW * CINB) >> 4 | (1u << 14) | (lay << 29);
+            const uint32_t a_lo = (1u << 16) + ((a_smem + s * p.a_bytes) >> 4);  // smem < 256 KB
 #pragma unroll
             for (int tap = 0; tap < 9; ++tap) {
               const int dy = tap / 3 - 1, dx = tap % 3 - 1;
-              const uint32_t st0 = sbase + (uint32_t)(((dy + 1) * (int)p.hw + dx + 1) * CINB);
 #pragma unroll
               for (int k = 0; k < CINB / 32; ++k) {
-                const int kb = k * 32;
-                const uint32_t sa = st0 + kb;
-                const uint32_t bo = p.hswz_bo == 0 ? 0u : (p.hswz_bo == 1 ? ((st0 >> 7) & 7u) : ((st0 >> 7) & 3u));
-                const uint32_t hi = hi0 | (bo << 17);
-                const uint64_t ad = ((uint64_t)hi << 32) | ((1u << 16) | ((sa & 0x3FFFFu) >> 4));
-                const uint32_t boff = (uint32_t)((tap * CB + kb / KCB)) * bblk + (uint32_t)(kb % KCB);
-                const uint64_t bd = ((uint64_t)b_hi << 32) | (b_lo0 + (boff >> 4));
+                const uint32_t aoff = (uint32_t)((((dy + 1) * (int)kHaloW + dx + 1) * CINB + 32 * k) >> 4);
+                const uint64_t ad = ((uint64_t)a_hi << 32) | (a_lo + aoff);
+                const uint64_t bd = ((uint64_t)b_hi << 32) | b_lo_tap[tap * (CINB / 32) + k];
                 tc_mma<DT>(d, ad, bd, idesc, (tap | k) != 0);
               }
             }
@@ -837,9 +853,8 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
             for (int k = 0; k < CINB / 32; ++k) {
               // two 16-byte channel groups per instruction (core matrices at +LBO)
               const uint32_t aoff = (uint32_t)(plane_px * CINB + ((2 * k) * HPX + pix0) * 16);
-              const uint32_t boff = (uint32_t)((tap * CB + (k * 32) / KCB)) * bblk + (uint32_t)((k * 32) % KCB);
               const uint64_t ad = ((uint64_t)a_hi << 32) | (alo + ((a_lbo << 16) + (aoff >> 4)));
-              const uint64_t bd = ((uint64_t)b_hi << 32) | (b_lo0 + (boff >> 4));
+              const uint64_t bd = ((uint64_t)b_hi << 32) | b_lo_tap[tap * (CINB / 32) + k];
               tc_mma<DT>(d, ad, bd, idesc, (tap | k) != 0);
             }
           }
@@ -1329,7 +1344,7 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
         if constexpr (OUTK == 1) {
           if (fast) {
             // one aligned int8 consumer, no unfolded BN / observer, full 16-column run
-#if defined(PMX_ABLATE) && PMX_ABLATE == 1
+#if defined(PMX_ABLATE) && (PMX_ABLATE == 1 || PMX_ABLATE == 4)
             continue;
 #elif defined(PMX_ABLATE) && PMX_ABLATE == 3
             *reinterpret_cast<uint4*>(reinterpret_cast<int8_t*>(outs.o[0].ptr) + outs.o[0].c_offset +
@@ -1448,13 +1463,7 @@ bool halo_swz_enabled() {
   return on;
 }
 
-uint32_t halo_swz_width() {  // PMX_HSWZ_W: swizzled halo row width in pixels (10 or 16)
-  static const uint32_t v = [] {
-    const char* e = getenv("PMX_HSWZ_W");
-    return (e && atoi(e) == 10) ? 10u : 16u;
-  }();
-  return v;
-}
+uint32_t halo_swz_width() { return kHaloW; }  // swizzled halo row width (16 px; 10 measured slower)
 
 int lat_tiles() {
   static const int v = [] {

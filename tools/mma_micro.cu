@@ -17,6 +17,9 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t sbo, uint32_t
   return d;
 }
 
+#ifndef RANDOM_FILL
+#define RANDOM_FILL 1
+#endif
 template <int KIND>
 __global__ void mma_bench(int n_mma, uint32_t idesc, uint32_t layout, uint32_t sbo, uint32_t lbo, int vary,
                           long long* out) {
@@ -24,7 +27,13 @@ __global__ void mma_bench(int n_mma, uint32_t idesc, uint32_t layout, uint32_t s
   __shared__ uint64_t bar;
   __shared__ uint32_t tslot;
   const uint32_t base = (smem_u32(sm) + 1023u) & ~1023u;
-  for (int i = threadIdx.x; i < 96 * 1024 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(sm)[i] = 0;
+  for (int i = threadIdx.x; i < 96 * 1024 / 4; i += blockDim.x) {
+    uint32_t h = (uint32_t)i * 2654435761u ^ 0x9e3779b9u;
+    h ^= h >> 15;
+    h *= 2246822519u;
+    h ^= h >> 13;
+    reinterpret_cast<uint32_t*>(sm)[i] = (RANDOM_FILL) ? (KIND == 1 ? (h & 0x3BFF3BFFu) : h) : 0u;
+  }
   if (threadIdx.x == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)));
     asm volatile("fence.mbarrier_init.release.cluster;");
@@ -43,7 +52,8 @@ __global__ void mma_bench(int n_mma, uint32_t idesc, uint32_t layout, uint32_t s
     uint64_t ad[9], bd[9];
 #pragma unroll
     for (int j = 0; j < 9; ++j) {
-      const uint32_t off = vary ? (uint32_t)j * step : 0u;
+      uint32_t off = vary ? (uint32_t)j * step : 0u;
+      if (vary == 7) off = (uint32_t)(((j / 3) * 16 + (j % 3)) * 64 + (j & 1) * 32);
       ad[j] = sdesc(base + off, sbo, layout, lbo);
       bd[j] = sdesc(base + 32768 + (off & ~1023u), sbo, layout, lbo);
     }
@@ -85,7 +95,9 @@ int main() {
                 {0, 160, 2880, 2, "NONE sbo160 vary+16B"},
                 {4, 512, 16, 3, "SW64 vary+512B"}, {2, 1024, 16, 4, "SW128 vary+1024B"}, {0, 128, 1024, 3, "NONE sbo128 vary+512B"},
                 {4, 512, 16, 5, "SW64 vary+64B (row)"}, {4, 1024, 16, 5, "SW64 sbo1024 vary+64B"},
-                {2, 1024, 16, 6, "SW128 vary+128B (row)"}, {2, 2048, 16, 6, "SW128 sbo2048 vary+128B"}};
+                {2, 1024, 16, 6, "SW128 vary+128B (row)"}, {2, 2048, 16, 6, "SW128 sbo2048 vary+128B"},
+                {4, 512, 16, 1, "SW64 vary+32B (K)"}, {4, 1024, 16, 1, "SW64 sbo1024 vary+32B"},
+                {4, 1024, 16, 7, "SW64 sbo1024 halo taps"}};
   for (int kind = 0; kind < 1; ++kind)
     for (int N : {64, 128})
       for (const Cfg& c : cfgs) {
