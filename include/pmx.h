@@ -239,7 +239,9 @@ typedef struct {
 } pmx_conv_desc;
 
 size_t pmx_conv_workspace(const pmx_conv_desc* desc);
-/* 1 if pmx_conv runs desc on the tcgen05 tensor-core kernels (0: the SIMT kernel). */
+/* Nonzero if pmx_conv runs desc on the tcgen05 tensor-core kernels (0: the SIMT kernel):
+ * bit 0 set; bit 1 = the 2-CTA-cluster (cta_group::2, M = 256) plan; bits 2-3 = the
+ * operand mode (0 3x3 per-tap TMA, 1 GEMM, 2 halo tile with resident weights). */
 int32_t pmx_conv_tc_supported(const pmx_conv_desc* desc);
 
 /* bn_post (may be NULL): unfolded batch norm applied after the bias as

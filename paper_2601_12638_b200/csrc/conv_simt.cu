@@ -16,7 +16,7 @@ pmx_status conv_tc_try(const pmx_conv_desc& d, const void* x, const void* w, con
                        cudaStream_t st, bool* launched, const GatherIn* gin);
 size_t conv_tc_workspace(const pmx_conv_desc& d);
 bool conv_tc_gather_ok(const pmx_conv_desc& d);
-bool conv_tc_supported(const pmx_conv_desc& d);
+int conv_tc_supported(const pmx_conv_desc& d);
 bool conv_tc_heads_ok(const pmx_conv_desc& d);
 pmx_status conv_tc_deconv_heads(const pmx_conv_desc& d, const void* x, const void* w, const float* alpha,
                                 const float* bias, const pmx_head_fuse& hf, cudaStream_t st);
@@ -251,7 +251,7 @@ pmx_status pmx_deconv_heads(const pmx_conv_desc* desc, const void* x, const void
 
 int32_t pmx_conv_tc_supported(const pmx_conv_desc* desc) {
   if (!desc || validate(*desc) != PMX_OK) return 0;
-  return conv_tc_supported(*desc) ? 1 : 0;
+  return conv_tc_supported(*desc);
 }
 
 size_t pmx_conv_workspace(const pmx_conv_desc* desc) {

@@ -99,6 +99,49 @@ __device__ __forceinline__ void tma_load_5d(uint32_t dst, const CUtensorMap* map
       : "memory");
 }
 
+// ---- CTA pairs (cta_group::2): the two CTAs of a 2-CTA cluster compute one M = 256
+// tile; each holds its 128 rows of A and half of B, the leader (rank 0) issues the MMAs.
+// In the shared::cluster window bit 24 of a CTA's shared address is its rank, so an
+// address with bit 24 cleared names the same offset in the leader CTA (as CUTLASS does).
+constexpr uint32_t kPeerMask = 0xFEFFFFFFu;
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// TMA into this CTA's shared memory, completing transaction bytes on the LEADER's barrier
+__device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+      "[%4];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar & kPeerMask)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_4d_pair(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
+                                                 uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
+      "%4, %5}], [%6];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar & kPeerMask)
+      : "memory");
+}
+// MMA completion -> the barrier at this offset in BOTH CTAs of the pair
+__device__ __forceinline__ void tc_commit_pair(uint32_t bar) {
+  asm volatile(
+      "{\n\t.reg .b16 m;\n\tmov.b16 m, 3;\n\t"
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n\t}" ::"r"(
+          bar)
+      : "memory");
+}
+// arrive on the leader CTA's barrier at this offset
+__device__ __forceinline__ void mbar_arrive_leader(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(bar & kPeerMask) : "memory");
+}
+
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
@@ -120,6 +163,23 @@ __device__ __forceinline__ void tc_mma(uint32_t d, uint64_t a, uint64_t b, uint3
     asm volatile(
         "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
         "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc)
+        : "memory");
+  }
+}
+
+template <int DT>
+__device__ __forceinline__ void tc_mma_pair(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  if constexpr (DT == PMX_I8) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc)
+        : "memory");
+  } else {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
         "l"(a), "l"(b), "r"(idesc), "r"(acc)
         : "memory");
   }
@@ -223,6 +283,7 @@ struct TcParams {
   // column lo_col = bn (summed in f32 by the epilogue): the tensor core's accumulation
   // truncates, so the corrections must not be added into the large partial sums
   int acc_stride, lo_col;
+  int pair;  // 2-CTA cluster (cta_group::2, M = 256): the kernel's PAIR instantiation
   // HEADS (OUTK 2, deconvs of the neck): the deconv's output tile is never written; its
   // int8 codes (the heads' input format) are staged in shared memory as the A operand of
   // a second kind::i8 MMA against this deconv's 128-channel slice of the three 1x1 heads
@@ -611,7 +672,7 @@ __device__ __forceinline__ void gather_producer(const TcParams& p, uint32_t a_sm
 // Persistent: grid = min(tiles, SMs); every role walks the same static tile sequence.
 // Accumulators are double-buffered in TMEM so the epilogue of tile i overlaps the
 // TMA + MMA of tile i+1; the smem ring runs across tile boundaries.
-template <int DT, int OUTK, int KCB, int CINB, int HS, bool GATHER>
+template <int DT, int OUTK, int KCB, int CINB, int HS, bool GATHER, bool PAIR = false>
 __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
     conv_tc_kernel(const __grid_constant__ TcMaps maps, const TcParams p, const Outs outs) {
   extern __shared__ uint8_t smem_raw[];
@@ -635,7 +696,17 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
   auto tempty = [&](int a) { return bar_base + 8u * (2 * p.stages + p.nacc + a); };
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int total = p.m_tiles * p.n_tiles;
+  // PAIR: the 2-CTA cluster walks pair tiles (two adjacent M tiles x one N tile); this
+  // CTA's M tile is 2 * (pair tile's M index) + rank
+  const uint32_t rank = PAIR ? cluster_rank() : 0u;
+  const int total = PAIR ? ((p.m_tiles + 1) / 2) * p.n_tiles : p.m_tiles * p.n_tiles;
+  const int tstart = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const int tstride = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+  auto tile_of = [&](uint32_t t, uint32_t& mt, uint32_t& nt) {
+    const uint32_t q = fdiv(t, p.fd_nt);
+    nt = t - q * (uint32_t)p.n_tiles;
+    mt = PAIR ? 2u * q + rank : q;
+  };
   const int nk = p.taps * p.cblocks;
   __shared__ uint64_t hbar_s[4];  // HEADS: head MMA done, per (epilogue tile slot, buffer)
 
@@ -649,19 +720,27 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
     }
     for (int a = 0; a < p.nacc; ++a) {
       mbar_init(tfull(a), 1);
-      mbar_init(tempty(a), 4 * (4 / p.egroups));  // the warps draining one tile
+      mbar_init(tempty(a), (PAIR ? 2 : 1) * 4 * (4 / p.egroups));  // the warps draining one tile (both CTAs)
     }
     mbar_init(bfull, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == kMmaWarp) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(p.tmem_cols)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    if constexpr (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(p.tmem_cols)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(p.tmem_cols)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (PAIR) cluster_sync_all();  // both CTAs' barriers initialised before any remote arrive / TMA
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   if (threadIdx.x == 0) PMX_TRACE(8, 1);
@@ -731,9 +810,12 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
           if (++s == (uint32_t)p.stages) s = 0, ph ^= 1;
         }
       }
-      for (int t = blockIdx.x; t < total && p.mode != MODE_HALO; t += gridDim.x) {
-        const int mt = (int)fdiv((uint32_t)t, p.fd_nt), nt = t - mt * p.n_tiles;
-        const int n0 = nt * p.bn;
+      for (int t = tstart; t < total && p.mode != MODE_HALO; t += tstride) {
+        uint32_t mtu, ntu;
+        tile_of((uint32_t)t, mtu, ntu);
+        const int mt = (int)mtu, nt = (int)ntu;
+        // PAIR: this CTA's half of the N tile
+        const int n0 = nt * p.bn + (PAIR ? (int)rank * (p.bn >> 1) : 0);
         int tb = 0, oy0 = 0, ox0 = 0, m0 = 0;
         if (p.mode == MODE_CONV3) {
           const int tq = (int)fdiv((uint32_t)mt, p.fd_tx), tx = mt - tq * p.tiles_x;
@@ -745,7 +827,8 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
         }
         for (int kb = 0; kb < nk; ++kb, ++it) {
           mbar_wait(empty(s), ph ^ 1);
-          mbar_expect_tx(full(s), p.a_bytes + p.b_bytes);
+          // PAIR: the leader's full barrier counts the bytes of both CTAs' loads
+          if (!PAIR || rank == 0) mbar_expect_tx(full(s), (PAIR ? 2u : 1u) * (p.a_bytes + p.b_bytes));
           const int tap = kb / p.cblocks, cb = kb % p.cblocks;
           const int c0 = cb * p.kc;
           int ac = c0;  // A channel coordinate
@@ -754,6 +837,21 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
             ac = p.a_off + (seg == 1 ? p.a_lo : 0) + (cb - seg * p.seg_n) * p.kc;
           }
           const uint32_t adst = a_smem + s * p.a_bytes, bdst = b_smem + s * p.b_bytes;
+          if constexpr (PAIR) {
+            if (p.mode == MODE_CONV3) {
+              const int dy = tap / 3 - 1, dx = tap % 3 - 1;
+              if (p.stride == 1) {
+                tma_load_4d_pair(adst, &maps.a[0], ac, ox0 + dx, oy0 + dy, tb, full(s));
+              } else {
+                const int ay = dy < 0 ? -1 : 0, py = dy == 0 ? 0 : 1;
+                const int ax = dx < 0 ? -1 : 0, px = dx == 0 ? 0 : 1;
+                tma_load_4d_pair(adst, &maps.a[py * 2 + px], ac, ox0 + ax, oy0 + ay, tb, full(s));
+              }
+            } else {
+              tma_load_2d_pair(adst, &maps.a[0], ac, m0, full(s));
+            }
+            tma_load_2d_pair(bdst, &maps.b, tap * (p.cblocks * p.kc) + c0, n0, full(s));
+          } else {
           if (p.mode == MODE_CONV3) {
             const int dy = tap / 3 - 1, dx = tap % 3 - 1;
             if (p.stride == 1) {
@@ -767,6 +865,7 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
             tma_load_2d(adst, &maps.a[0], ac, m0, full(s));
           }
           tma_load_2d(bdst, &maps.b, tap * (p.cblocks * p.kc) + c0, n0, full(s));
+          }
           if (++s == (uint32_t)p.stages) s = 0, ph ^= 1;
         }
       }
@@ -870,7 +969,8 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
       constexpr int ksteps = KCB / 32;  // 32 bytes of K per instruction
       const uint32_t hi = (uint32_t)(sdesc(0, p.sbo, p.layout) >> 32), lo0 = (uint32_t)sdesc(0, p.sbo, p.layout);
       uint32_t s = 0, ph = 0, acc = 0, aph = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x, ++i) {
+      // PAIR: only the leader issues (M = 256 over both CTAs' A, N over both B halves)
+      for (int t = tstart; t < total && (!PAIR || rank == 0); t += tstride, ++i) {
         if (lane == 0) PMX_TRACE(9, i);
         mbar_spin(tempty(acc), aph ^ 1);
         tc_fence_after();
@@ -896,15 +996,18 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
             for (int k = 0; k < ksteps; ++k) {
               const uint64_t ad = ((uint64_t)hi << 32) | (alo + 2u * k);
               const uint64_t bd = ((uint64_t)hi << 32) | (blo + 2u * k);
-              tc_mma<DT>(dk, ad, bd, idesc, !(first && k == 0));
+              if constexpr (PAIR) tc_mma_pair<DT>(dk, ad, bd, idesc, !(first && k == 0));
+              else tc_mma<DT>(dk, ad, bd, idesc, !(first && k == 0));
             }
-            tc_commit(empty(s));
+            if constexpr (PAIR) tc_commit_pair(empty(s));
+            else tc_commit(empty(s));
           }
           __syncwarp();
           if (++s == (uint32_t)p.stages) s = 0, ph ^= 1;
         }
         if (elect_one()) {
-          tc_commit(tfull(acc));
+          if constexpr (PAIR) tc_commit_pair(tfull(acc));
+          else tc_commit(tfull(acc));
           PMX_TRACE(4, i);
         }
         __syncwarp();
@@ -1019,12 +1122,17 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
       }
     };
     uint32_t i_last = 0xffffffffu;
+    auto release_acc = [&](uint32_t a) {
+      if constexpr (PAIR) mbar_arrive_leader(tempty(a));
+      else mbar_arrive(tempty(a));
+    };
     for (uint32_t i = (uint32_t)eg;; i += (uint32_t)egn) {
-      const uint32_t t = blockIdx.x + i * gridDim.x;
+      const uint32_t t = (uint32_t)tstart + i * (uint32_t)tstride;
       if (t >= (uint32_t)total) break;
       i_last = i;
       const uint32_t acc = i & (uint32_t)(p.nacc - 1), aph = (i >> p.nacc_shift) & 1;
-      const uint32_t mt = fdiv(t, p.fd_nt), nt = t - mt * (uint32_t)p.n_tiles;
+      uint32_t mt, nt;
+      tile_of(t, mt, nt);
       const int n0 = (int)nt * p.bn;
       bool valid;
       uint32_t pix_in;  // < 2^31 (checked on the host)
@@ -1034,11 +1142,11 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
         const uint32_t tb = fdiv(tq, p.fd_ty), ty = tq - tb * (uint32_t)p.tiles_y;
         const uint32_t oy = ty * p.th + ((uint32_t)row >> p.tw_shift);
         const uint32_t ox = tx * p.tw + ((uint32_t)row & (uint32_t)(p.tw - 1));
-        valid = oy < (uint32_t)p.out_h && ox < (uint32_t)p.out_w;
+        valid = oy < (uint32_t)p.out_h && ox < (uint32_t)p.out_w && mt < (uint32_t)p.m_tiles;
         pix_in = (tb * p.out_h + oy) * p.out_w + ox;
       } else {
         pix_in = mt * 128u + row;
-        valid = pix_in < (uint32_t)p.m_total;
+        valid = pix_in < (uint32_t)p.m_total && mt < (uint32_t)p.m_tiles;
         if (p.deconv) {
           const uint32_t tt = fdiv(pix_in, p.fd_iw);
           ix = pix_in - tt * (uint32_t)p.in_w;
@@ -1085,7 +1193,7 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
         // main accumulator drained: release it to the MMA warp
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(tempty(acc));
+        if (lane == 0) release_acc(acc);
         // codes -> async proxy, the slot's 8 warps meet, one thread issues the head MMA
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         asm volatile("bar.sync %0, 256;" ::"r"(2 + eg) : "memory");
@@ -1232,7 +1340,7 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
           }
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(tempty(acc));
+          if (lane == 0) release_acc(acc);
           continue;
         }
       }
@@ -1314,7 +1422,7 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
           // release this accumulator buffer to the MMA warp
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(tempty(acc));
+          if (lane == 0) release_acc(acc);
           continue;
         }
       }
@@ -1392,7 +1500,7 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
       // release this accumulator buffer to the MMA warp
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(tempty(acc));
+      if (lane == 0) release_acc(acc);
       if (warp == 0 && lane == 0) PMX_TRACE(7, i);
       if (lane == 0 && i == 6) PMX_TRACE(8, 9 + 2 * warp);
     }
@@ -1403,10 +1511,16 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
+  // PAIR: neither CTA leaves (or frees its TMEM) while the leader's MMAs may still read
+  // the peer's shared memory or write its accumulators
+  if constexpr (PAIR) cluster_sync_all();
   if (threadIdx.x == 0) PMX_TRACE(8, 3);
   if (warp == kMmaWarp) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(p.tmem_cols) : "memory");
+    if constexpr (PAIR)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(p.tmem_cols) : "memory");
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(p.tmem_cols) : "memory");
   }
 }
 
@@ -1464,6 +1578,14 @@ bool halo_swz_enabled() {
 }
 
 uint32_t halo_swz_width() { return kHaloW; }  // swizzled halo row width (16 px; 10 measured slower)
+
+bool pair_enabled() {  // PMX_PAIR=0: no 2-CTA clusters (A/B runs)
+  static const bool on = [] {
+    const char* e = getenv("PMX_PAIR");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 
 int lat_tiles() {
   static const int v = [] {
@@ -1685,6 +1807,20 @@ Plan plan_for(const pmx_conv_desc& d, bool gather = false, bool want_stage = fal
     p.idesc = (1u << 4) | (2u << 7) | (2u << 10) | (n_enc << 17) | (m_enc << 24);
   else
     p.idesc = (1u << 4) | (0u << 7) | (0u << 10) | (n_enc << 17) | (m_enc << 24);
+  // CTA pairs for the TMA-ring modes with a wide N tile: each SM then reads its own A and
+  // HALF of B from shared memory per MMA (operand bandwidth is what limits these layers)
+  p.pair = 0;
+  if (!gather && !heads && !x3 && p.mode == MODE_CONV3 && bn >= 128 && bn % 32 == 0 && pair_enabled() &&
+      (int64_t)p.m_tiles * p.n_tiles >= 2LL * num_sms() && num_sms() >= 2) {
+    p.pair = 1;
+    p.b_bytes = (uint32_t)(bn / 2) * kc_bytes;
+    int st2 = (int)((200u * 1024u - 8u * (uint32_t)d.out_c - estage_bytes) / (p.a_bytes + p.b_bytes));
+    p.stages = st2 > 12 ? 12 : (st2 < 2 ? 2 : st2);
+    p.idesc = (p.idesc & ~(0x1Fu << 24)) | ((256u >> 4) << 24);  // M = 256 over the pair
+    const int64_t pair_tiles = (int64_t)((p.m_tiles + 1) / 2) * p.n_tiles;
+    const int gmax = num_sms() & ~1;
+    pl.grid_x = (int)(2 * pair_tiles < gmax ? 2 * pair_tiles : gmax);
+  }
   pl.smem = 1024 + (size_t)p.stages * (p.a_bytes + p.b_bytes) + p.bres_bytes + (2 * p.stages + 2 * p.nacc + 1) * 8 + 32 +
             8 * (size_t)((d.out_c + 3) & ~3) + (gather ? kGatherSmem : 0) + (estage_bytes ? 16 + estage_bytes : 0) +
             (heads ? 16 + kHeadsSmem : 0);
@@ -1697,7 +1833,7 @@ Plan plan_for(const pmx_conv_desc& d, bool gather = false, bool want_stage = fal
       return e ? atoi(e) : 1;
     }();
     const int64_t tl = (int64_t)p.m_tiles * p.n_tiles;
-    if (div > 1 && !gather && tl <= 4LL * num_sms() && pl.grid_x > num_sms() / div) pl.grid_x = num_sms() / div;
+    if (div > 1 && !gather && !p.pair && tl <= 4LL * num_sms() && pl.grid_x > num_sms() / div) pl.grid_x = num_sms() / div;
   }
   pl.ok = true;
   return pl;
@@ -1777,7 +1913,7 @@ pmx_status build_maps(const pmx_conv_desc& d, const Plan& pl, const void* x, con
   const int K = p.taps * p.cblocks * p.kc;  // 3xTF32: taps * 3 * Cin
   cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)p.n_gemm};
   cuuint64_t str[1] = {(cuuint64_t)K * esz};
-  cuuint32_t box[2] = {(cuuint32_t)p.kc, (cuuint32_t)p.bn};
+  cuuint32_t box[2] = {(cuuint32_t)p.kc, (cuuint32_t)(p.pair ? p.bn / 2 : p.bn)};  // PAIR: half of N per CTA
   return encode(&maps->b, dt, 2, w, dims, str, box, sw);
 }
 
@@ -1788,9 +1924,10 @@ const char* conv_tc_backend(int dtype, int) {
   return (dtype == PMX_I8 || dtype == PMX_F16 || dtype == PMX_F32X2) ? "tcgen05" : "simt";
 }
 
-bool conv_tc_supported(const pmx_conv_desc& d) {
-  if (g_conv_backend_mode == 1) return false;
-  return plan_for(d).ok;
+int conv_tc_supported(const pmx_conv_desc& d) {
+  if (g_conv_backend_mode == 1) return 0;
+  const Plan pl = plan_for(d);
+  return pl.ok ? 1 | (pl.p.pair << 1) | (pl.p.mode << 2) : 0;
 }
 
 size_t conv_tc_workspace(const pmx_conv_desc&) { return 0; }
@@ -1847,11 +1984,18 @@ pmx_status conv_tc_try(const pmx_conv_desc& d, const void* x, const void* w, con
     cfg.blockDim = dim3(threads);
     cfg.dynamicSmemBytes = pl.smem;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    if (pl.p.pair) {  // 2-CTA clusters
+      attr[1].id = cudaLaunchAttributeClusterDimension;
+      attr[1].val.clusterDim.x = 2;
+      attr[1].val.clusterDim.y = 1;
+      attr[1].val.clusterDim.z = 1;
+      cfg.numAttrs = 2;
+    }
     PMX_CUDA(cudaLaunchKernelEx(&cfg, kern, maps, pl.p, outs));
     return PMX_OK;
   };
@@ -1866,8 +2010,12 @@ pmx_status conv_tc_try(const pmx_conv_desc& d, const void* x, const void* w, con
     s = one_i8 ? launch(conv_tc_kernel<DTV, 1, KB, CB, HSV, false>, kThreads)                                 \
                : launch(conv_tc_kernel<DTV, 0, KB, CB, HSV, false>, kThreads)
 #define PMX_TC_LAUNCH_NG(DTV, KB)                                                                              \
-  s = one_i8 ? launch(conv_tc_kernel<DTV, 1, KB, 0, 0, false>, kThreads)                                      \
-             : launch(conv_tc_kernel<DTV, 0, KB, 0, 0, false>, kThreads)
+  if (pl.p.pair)                                                                                               \
+    s = one_i8 ? launch(conv_tc_kernel<DTV, 1, KB, 0, 0, false, true>, kThreads)                              \
+               : launch(conv_tc_kernel<DTV, 0, KB, 0, 0, false, true>, kThreads);                             \
+  else                                                                                                         \
+    s = one_i8 ? launch(conv_tc_kernel<DTV, 1, KB, 0, 0, false>, kThreads)                                    \
+               : launch(conv_tc_kernel<DTV, 0, KB, 0, 0, false>, kThreads)
 #define PMX_TC_SHAPES(DTV)                                          \
   if (cinb == 64 && hs == 1) { PMX_TC_LAUNCH(DTV, 64, 64, 1); }     \
   else if (cinb == 64) { PMX_TC_LAUNCH(DTV, 64, 64, 2); }           \

@@ -30,7 +30,13 @@ CASES = [  # kind, cin, cout, k, stride, (h, w), batch
     ("conv", 128, 128, 3, 1, (124, 108), 1), # blocks.1.x full size, batch 1
     ("conv", 256, 256, 3, 1, (62, 54), 1),   # blocks.2.x full size, batch 1 (N split to 4 x 64)
     ("deconv", 256, 128, 4, 4, (62, 54), 1), # deblocks.2 full size, batch 1
+] + [  # 2-CTA clusters (cta_group::2, M = 256): enough tiles for the pair plan
+    ("conv", 256, 256, 3, 1, (62, 54), 12),  # blocks.2.x full size, batch 12 (324 tiles)
+    ("conv", 128, 256, 3, 2, (124, 108), 12),# blocks.2.0 full size, batch 12
+    ("conv", 256, 256, 3, 1, (61, 37), 17),  # 323 pixel tiles: the last pair's rank 1 idles
+    ("conv", 128, 128, 3, 1, (124, 108), 4), # blocks.1.x: pair plan in the nohalo mode
 ]
+CLUSTER_CASES = CASES[-4:]
 
 
 def _run(lib, N, torch, desc, x, w, alpha, bias, outs_spec, mode, observe=True):
@@ -193,3 +199,24 @@ def test_tcgen05_int8_f16_pair(case, order):
     ref, _ = _run(lib, N, torch, desc, x, wt, alpha, bias, spec, 1, observe=False)
     for a, b in zip(tc, ref):
         assert torch.equal(a, b), (a.float() - b.float()).abs().max()
+
+
+@pytest.mark.parametrize("case", CLUSTER_CASES, ids=lambda c: f"{c[1]}x{c[2]}s{c[4]}_{c[5][0]}x{c[5][1]}b{c[6]}")
+def test_pair_plan_selected(case):
+    """The CLUSTER_CASES really run the 2-CTA plan (bit 1 of pmx_conv_tc_supported), so the
+    parity tests above cover it; PMX_PAIR=0 is the only way to turn it off."""
+    from paper_2601_12638_b200 import _native as N
+
+    lib = N.load()
+    kind, cin, cout, k, s, (h, w), batch = case
+    oh, ow = (h + 2 - 3) // s + 1, (w + 2 - 3) // s + 1
+    desc = N.ConvDesc(kind=N.PMX_CONV2D, in_dtype=N.PMX_I8, batch=batch, in_h=h, in_w=w, in_c=cin, in_c_stride=cin,
+                      in_c_offset=0, out_c=cout, k_h=3, k_w=3, stride_h=s, stride_w=s, pad_h=1, pad_w=1, out_h=oh,
+                      out_w=ow, relu=1)
+    lib.pmx_set_conv_backend(2 if cout == 128 else 0)
+    try:
+        code = lib.pmx_conv_tc_supported(ctypes.byref(desc))
+    finally:
+        lib.pmx_set_conv_backend(0)
+    assert code & 1 and code & 2, code
+    assert (code >> 2) & 3 == 0  # the per-tap TMA ring (pairs are never planned for halo / GEMM)
