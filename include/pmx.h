@@ -385,6 +385,77 @@ size_t pmx_sq_err_workspace(void);
 pmx_status pmx_sq_err(const float* a, const float* b, int64_t n, double* out2, double* ws,
                       size_t ws_bytes, pmx_stream_t stream);
 
+/* ------------------------------------------------------------------------
+ * QAT (pm/qat.py:79-306) on the GPU: the training forward's pre-activation
+ * convolutions and the backward pass over its tape.  f32 throughout; activations
+ * NHWC, weights as the model stores them ([Cout, Cin, kh, kw]; a linear layer is a
+ * 1x1 conv over rows with batch = rows).  desc: PMX_CONV2D (any kernel / stride /
+ * padding) or PMX_DECONV2D (kernel == stride); in_dtype / in_c_stride /
+ * in_c_offset / relu are ignored.  Every reduction has a fixed order: a training
+ * run is bit-reproducible on one device.
+ * ---------------------------------------------------------------------- */
+/* out = conv(x, w) + bias, before any ReLU (the tape's pre_act, pm/model.py:286-292) */
+pmx_status pmx_train_conv_fwd(const pmx_conv_desc* desc, const float* x, const float* w, const float* bias,
+                              float* out, pmx_stream_t stream);
+/* dx = the data gradient of dout (pm/qat.py:145-152 col2im; linear :130-131) */
+pmx_status pmx_train_conv_dgrad(const pmx_conv_desc* desc, const float* dout, const float* w, float* dx,
+                                pmx_stream_t stream);
+/* dw = dout^T . im2col(x), db = column sums of dout (pm/qat.py:142-144); either may be NULL */
+pmx_status pmx_train_conv_wgrad(const pmx_conv_desc* desc, const float* dout, const float* x, float* dw,
+                                float* db, pmx_stream_t stream);
+/* np.maximum(x, 0) (NaN propagates) and its adjoint dout * (pre_act > 0) (pm/qat.py:160-161) */
+pmx_status pmx_train_relu(const float* x, int64_t n, float* out, pmx_stream_t stream);
+pmx_status pmx_train_relu_bwd(const float* dout, const float* pre_act, int64_t n, float* dx, pmx_stream_t stream);
+/* clipped STE (pm/qat.py:68-85): out = upstream * (q_min*s <= x <= q_max*s).  Per tensor
+ * the bounds are compared as f32 (NumPy 2 promotion of a Python float against an f32
+ * array); per row (per-channel weights, scales f64 [rows]) in f64. */
+pmx_status pmx_train_ste(const float* x, int64_t n, double scale, int32_t q_min, int32_t q_max,
+                         const float* upstream, float* out, pmx_stream_t stream);
+pmx_status pmx_train_ste_rows(const float* x, int64_t rows, int64_t cols, const double* scales, int32_t q_min,
+                              int32_t q_max, const float* upstream, float* out, pmx_stream_t stream);
+/* masked max over points of x [P, M, C] with the np.argmax winner per (pillar, channel)
+ * (pm/model.py:338-345); argmax may be NULL.  Adjoint: dx[p, argmax, c] = dout[p, c]. */
+pmx_status pmx_train_maxpool(const float* x, const uint8_t* mask, int64_t pillars, int32_t m, int32_t c,
+                             float* out, int32_t* argmax, pmx_stream_t stream);
+pmx_status pmx_train_maxpool_bwd(const float* dout, const int32_t* argmax, int64_t pillars, int32_t m, int32_t c,
+                                 float* dx, pmx_stream_t stream);
+/* scatter of pillar rows into a zeroed NHWC canvas (coords int32 [P, 2] = (row, col)) and
+ * its adjoint, the gather (pm/tensor_ops.py:138-160, pm/qat.py:184-186) */
+pmx_status pmx_train_scatter(const float* feats, const int32_t* coords, int64_t pillars, int32_t c,
+                             int32_t grid_w, float* canvas, pmx_stream_t stream);
+pmx_status pmx_train_scatter_bwd(const float* dcanvas, const int32_t* coords, int64_t pillars, int32_t c,
+                                 int32_t grid_w, float* dfeats, pmx_stream_t stream);
+/* adjoint of pmx_upsample2x: each input cell sums its 2x2 block (pm/qat.py:188-190);
+ * h, w are the INPUT extents */
+pmx_status pmx_train_upsample2x_bwd(const float* dout, int32_t batch, int32_t h, int32_t w, int32_t c,
+                                    float* dx, pmx_stream_t stream);
+/* out = a + b (f32) -- gradient accumulation, the heads' trunk sum */
+pmx_status pmx_train_add(const float* a, const float* b, int64_t n, float* out, pmx_stream_t stream);
+/* dst[p, dst_offset + k] = src[p, src_offset + k], k < c: concat and its adjoint */
+pmx_status pmx_train_copy_channels(const float* src, int64_t pixels, int32_t c, int32_t src_stride,
+                                   int32_t src_offset, float* dst, int32_t dst_stride, int32_t dst_offset,
+                                   pmx_stream_t stream);
+/* device scratch (bytes) of the f64 reductions below */
+size_t pmx_train_reduce_workspace(void);
+/* detection_loss (pm/qat.py:92-116) on NHWC maps: cls [hw, n_cls] logits and
+ * cls_target (f64), ignore_mask / pos_mask u8 [hw] (ignore may be NULL), reg [hw, n_reg]
+ * and reg_target (f64).  d_cls / d_reg get the f32 gradients; sums[0] = sum(w * bce),
+ * sums[1] = sum(diff^2), both f64 (the loss is formed on the host). */
+pmx_status pmx_train_detection_loss(const float* cls, const double* cls_target, const uint8_t* ignore_mask,
+                                    const uint8_t* pos_mask, const float* reg, const double* reg_target,
+                                    int64_t hw, int32_t n_cls, int32_t n_reg, double n_pos, double cls_weight,
+                                    double reg_weight, double pos_weight, float* d_cls, float* d_reg,
+                                    double* sums, double* ws, pmx_stream_t stream);
+/* mse_loss (pm/qat.py:119-125): grad = f32(2 (out - target) / n), sum = sum((out - target)^2) */
+pmx_status pmx_train_mse_loss(const float* out, const double* target, int64_t n, float* grad, double* sum,
+                              double* ws, pmx_stream_t stream);
+/* sum of (inv * g)^2 (f32 product and square, f64 sum): the gradient-norm clip */
+pmx_status pmx_train_sumsq(const float* g, int64_t n, float inv, double* sum, double* ws, pmx_stream_t stream);
+/* SGD step (pm/qat.py:289-301): step = inv * g (momentum: step = mu * v + step, v = step),
+ * w -= lr * step, all f32 */
+pmx_status pmx_train_sgd(float* w, const float* grad, int64_t n, float inv, float lr, float momentum,
+                         float* velocity, pmx_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

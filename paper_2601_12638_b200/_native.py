@@ -111,6 +111,26 @@ SIGNATURES = {
     "pmx_zero": (I32, [P, SZ, P]),
     "pmx_sq_err_workspace": (SZ, []),
     "pmx_sq_err": (I32, [P, P, I64, P, P, SZ, P]),
+    # QAT (train.cu)
+    "pmx_train_conv_fwd": (I32, [C.POINTER(ConvDesc), P, P, P, P, P]),
+    "pmx_train_conv_dgrad": (I32, [C.POINTER(ConvDesc), P, P, P, P]),
+    "pmx_train_conv_wgrad": (I32, [C.POINTER(ConvDesc), P, P, P, P, P]),
+    "pmx_train_relu": (I32, [P, I64, P, P]),
+    "pmx_train_relu_bwd": (I32, [P, P, I64, P, P]),
+    "pmx_train_ste": (I32, [P, I64, F64, I32, I32, P, P, P]),
+    "pmx_train_ste_rows": (I32, [P, I64, I64, P, I32, I32, P, P, P]),
+    "pmx_train_maxpool": (I32, [P, P, I64, I32, I32, P, P, P]),
+    "pmx_train_maxpool_bwd": (I32, [P, P, I64, I32, I32, P, P]),
+    "pmx_train_scatter": (I32, [P, P, I64, I32, I32, P, P]),
+    "pmx_train_scatter_bwd": (I32, [P, P, I64, I32, I32, P, P]),
+    "pmx_train_upsample2x_bwd": (I32, [P, I32, I32, I32, I32, P, P]),
+    "pmx_train_add": (I32, [P, P, I64, P, P]),
+    "pmx_train_copy_channels": (I32, [P, I64, I32, I32, I32, P, I32, I32, P]),
+    "pmx_train_reduce_workspace": (SZ, []),
+    "pmx_train_detection_loss": (I32, [P, P, P, P, P, P, I64, I32, I32, F64, F64, F64, F64, P, P, P, P, P]),
+    "pmx_train_mse_loss": (I32, [P, P, I64, P, P, P, P]),
+    "pmx_train_sumsq": (I32, [P, I64, C.c_float, P, P, P]),
+    "pmx_train_sgd": (I32, [P, P, I64, C.c_float, C.c_float, C.c_float, P, P]),
 }
 
 _LIB = None

@@ -26,7 +26,8 @@ from paper_2601_12638_b200.model import (
     weights_digest,
 )
 from paper_2601_12638_b200.pointpillars import PointPillarsConfig, build_pointpillars
-from paper_2601_12638_b200.quant import DType, MinMaxObserver, QuantParams, compute_scale, weight_quant_params
+from paper_2601_12638_b200.quant import (DType, MinMaxObserver, PerChannelQuantParams, QuantParams, compute_scale,
+                                         weight_quant_params)
 from paper_2601_12638_b200.tensor_ops import ConvParams
 from tests.conftest import GOLDEN
 
@@ -191,3 +192,23 @@ def test_sweep_ranking_and_greedy_plans():
     assert head_error([4.0, 16.0]) == 0.5 and head_error([1.0, 0.0]) == float("inf")
     recs = records({"layer_errors": errs, "ranking": select_topk(errs, 5)})
     assert [(r.layer_index, r.rank) for r in recs] == [(1, 4), (2, 1), (3, 5), (4, 2), (5, 3)]
+
+
+def test_qat_config_and_golden_stats():
+    """QAT host pieces (pm/qat.py:34-64): config validation, and the reference-written
+    calibration stats of the QAT fixtures load through this package's reader."""
+    from paper_2601_12638_b200 import qat
+
+    cfg = qat.TrainConfig()
+    assert (cfg.learning_rate, cfg.epochs, cfg.batch_size, cfg.pos_weight) == (2e-4, 1, 4, 4.0)
+    with pytest.raises(ValueError, match="learning_rate must be positive"):
+        qat.TrainConfig(learning_rate=0.0)
+    with pytest.raises(ValueError, match="epochs must be >= 1"):
+        qat.TrainConfig(epochs=0)
+    with pytest.raises(ValueError, match=r"momentum must lie in \[0, 1\)"):
+        qat.TrainConfig(momentum=1.0)
+    st = CAL.load_stats(GOLDEN / "qat_stats_pc.json")
+    assert st.indices() == list(range(1, 14))
+    assert all(isinstance(st[i].weight_qp, PerChannelQuantParams) for i in st.indices())
+    g = load_model(GOLDEN / "qat_chain")
+    assert [l.kind for l in g.layers] == ["conv2d", "conv2d", "upsample2x", "conv2d"]
