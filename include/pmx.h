@@ -273,6 +273,11 @@ void pmx_set_conv_backend(int32_t mode);
  * CTA 0 into buf[10][64]: rows 0-7 producer/MMA/epilogue hand-offs per tile, row 8
  * = kernel entry, setup done, resident weights landed, teardown; row 9 = MMA loop top. */
 void pmx_debug_trace(unsigned long long* buf);
+/* Debug (trace builds, -DPMX_CONV_TRACE): every tcgen05 conv CTA launched after this
+ * call appends {launch tag << 32 | cta, t_entry, t_after_griddepcontrol_wait, t_exit}
+ * (%globaltimer ns) at buf[1 + 4 * atomicAdd(buf[0], 1)]; tags count launches from 0.
+ * NULL turns it off.  A no-op in production builds. */
+void pmx_debug_timeline(unsigned long long* buf);
 
 /* ------------------------------------------------------------------------
  * K9+K10 fused: a neck deconvolution (kernel == stride, Cout == 128, INT8 or FP16

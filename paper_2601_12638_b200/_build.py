@@ -44,9 +44,12 @@ def up_to_date() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False, ptxas_verbose: bool = False) -> Path:
-    if not force and up_to_date():
+    out = Path(os.environ["PMX_BUILD_OUT"]).resolve() if os.environ.get("PMX_BUILD_OUT") else LIB
+    if out == LIB and not force and up_to_date():
         return LIB
-    BUILD.mkdir(parents=True, exist_ok=True)
+    # PMX_BUILD_OUT: a variant library (trace / ablation builds) with its own object dir
+    bdir = BUILD if out == LIB else BUILD.parent / ("pmx_" + out.stem)
+    bdir.mkdir(parents=True, exist_ok=True)
     nvcc = _nvcc()
     extra = ["-Xptxas", "-v"] if ptxas_verbose else []
     if os.environ.get("PMX_TRACE_BUILD") == "1":  # per-role conv timeline (tools/op_profile.py --trace)
@@ -55,7 +58,7 @@ def build(force: bool = False, verbose: bool = False, ptxas_verbose: bool = Fals
         extra += [f"-DPMX_ABLATE={int(os.environ['PMX_ABLATE'])}"]
 
     def compile_one(src: Path) -> Path:
-        obj = BUILD / (src.stem + ".o")
+        obj = bdir / (src.stem + ".o")
         cmd = [nvcc, *ARCH, *NVCC_FLAGS, *extra, "-c", str(src), "-o", str(obj)]
         if verbose:
             print(" ".join(cmd), flush=True)
@@ -68,15 +71,15 @@ def build(force: bool = False, verbose: bool = False, ptxas_verbose: bool = Fals
 
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
         objs = list(ex.map(compile_one, _sources()))
-    tmp = LIB.with_suffix(".so.tmp")
+    tmp = out.with_suffix(".so.tmp")
     cmd = [nvcc, *ARCH, "-shared", "-o", str(tmp), *map(str, objs)]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, out)
+    return out
 
 
 if __name__ == "__main__":
     build(force="--force" in sys.argv, verbose=True, ptxas_verbose="--ptxas" in sys.argv)
-    print(LIB)
+    print(os.environ.get("PMX_BUILD_OUT", LIB))

@@ -101,6 +101,7 @@ SIGNATURES = {
     "pmx_conv": (I32, [C.POINTER(ConvDesc), P, P, P, P, P, C.POINTER(Out), I32, P, P, SZ, P]),
     "pmx_set_conv_backend": (None, [I32]),
     "pmx_debug_trace": (None, [P]),
+    "pmx_debug_timeline": (None, [P]),
     "pmx_upsample2x": (I32, [P, I32, I32, I32, I32, I32, P, P]),
     "pmx_cast_out": (I32, [P, I64, I32, C.POINTER(Out), I32, P, P]),
     "pmx_decode_workspace": (SZ, [C.POINTER(AnchorDesc), I32, I32, I32]),

@@ -34,6 +34,8 @@ namespace pmx {
 
 extern thread_local int g_conv_backend_mode;  // per calling thread (test override)
 thread_local unsigned long long* g_trace = nullptr;  // pmx_debug_trace (per calling thread)
+thread_local unsigned long long* g_timeline = nullptr;  // pmx_debug_timeline (per calling thread)
+thread_local uint32_t g_tl_tag = 0;
 
 namespace {
 
@@ -338,6 +340,8 @@ struct TcParams {
   const float* bn_post;
   uint32_t* keys;
   unsigned long long* trace;  // debug: per-role clock64 stamps of CTA 0 (pmx_debug_trace)
+  unsigned long long* tl;     // debug: per-CTA globaltimer stamps of every launch (pmx_debug_timeline)
+  uint32_t tl_tag;
   // GATHER (first conv on the pillar canvas)
   const void* g_feats;   // [B * pcap, row] pillar features (+ channel offset)
   const int32_t* g_map;  // [B, in_h, in_w] pillar slot per cell, -1 empty
@@ -356,6 +360,31 @@ struct TcParams {
 #define PMX_TRACE(ev, idx) \
   do {                     \
   } while (0)
+#endif
+
+// whole-graph timeline (tools/b1_timeline.py): thread 0 of every CTA stamps entry, the
+// return of griddepcontrol.wait and exit with %globaltimer (trace builds only)
+#ifdef PMX_CONV_TRACE
+#define PMX_TL_DECL unsigned long long tl_t0 = 0, tl_t1 = 0
+#define PMX_TL_STAMP(v) \
+  if (p.tl && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v))
+#define PMX_TL_COMMIT()                                                                            \
+  do {                                                                                             \
+    if (p.tl && threadIdx.x == 0) {                                                                \
+      unsigned long long t2;                                                                       \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t2));                                       \
+      const unsigned long long slot = atomicAdd(p.tl, 1ull);                                       \
+      unsigned long long* r = p.tl + 1 + 4 * slot;                                                 \
+      r[0] = ((unsigned long long)p.tl_tag << 32) | blockIdx.x;                                    \
+      r[1] = tl_t0;                                                                                \
+      r[2] = tl_t1;                                                                                \
+      r[3] = t2;                                                                                   \
+    }                                                                                              \
+  } while (0)
+#else
+#define PMX_TL_DECL
+#define PMX_TL_STAMP(v)
+#define PMX_TL_COMMIT()
 #endif
 
 struct TcMaps {
@@ -675,6 +704,8 @@ __device__ __forceinline__ void gather_producer(const TcParams& p, uint32_t a_sm
 template <int DT, int OUTK, int KCB, int CINB, int HS, bool GATHER, bool PAIR = false>
 __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
     conv_tc_kernel(const __grid_constant__ TcMaps maps, const TcParams p, const Outs outs) {
+  PMX_TL_DECL;
+  PMX_TL_STAMP(tl_t0);
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
@@ -765,6 +796,7 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
     }
   }
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  PMX_TL_STAMP(tl_t1);
 
   if (GATHER && (warp == kProdWarp || warp > kMmaWarp)) {
     if constexpr (GATHER) {
@@ -1515,6 +1547,7 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
   // the peer's shared memory or write its accumulators
   if constexpr (PAIR) cluster_sync_all();
   if (threadIdx.x == 0) PMX_TRACE(8, 3);
+  PMX_TL_COMMIT();
   if (warp == kMmaWarp) {
     tc_fence_after();
     if constexpr (PAIR)
@@ -1578,6 +1611,14 @@ bool halo_swz_enabled() {
 }
 
 uint32_t halo_swz_width() { return kHaloW; }  // swizzled halo row width (16 px; 10 measured slower)
+
+bool one_slot_enabled() {  // PMX_ONE_SLOT=0: keep the tile slots at one tile per CTA (A/B runs)
+  static const bool on = [] {
+    const char* e = getenv("PMX_ONE_SLOT");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 
 bool pair_enabled() {  // PMX_PAIR=0: no 2-CTA clusters (A/B runs)
   static const bool on = [] {
@@ -1706,6 +1747,9 @@ Plan plan_for(const pmx_conv_desc& d, bool gather = false, bool want_stage = fal
   p.nacc_shift = __builtin_ctz((unsigned)p.nacc);
   p.egroups = bn <= 64 ? 4 : (bn <= 128 ? 2 : 1);
   if (p.egroups > p.nacc) p.egroups = p.nacc;
+  // one tile per CTA (batch-1 layers): every epilogue warp works on that tile instead of
+  // one slot's 4 or 8 warps (the other slots would have nothing to drain)
+  if (!heads && tiles <= num_sms() && one_slot_enabled()) p.egroups = 1;
   p.hcol0 = (uint32_t)(p.nacc * p.acc_stride);  // HEADS: 2 x 32 columns per tile slot after the accumulators
   if (heads) want_stage = want_stage2 = false;
   // (measured: a win for 128- and 384-byte output rows -- deconvs into the concat,
@@ -1969,6 +2013,8 @@ pmx_status conv_tc_try(const pmx_conv_desc& d, const void* x, const void* w, con
   pl.p.bn_post = bn_post;
   pl.p.keys = keys;
   pl.p.trace = g_trace;
+  pl.p.tl = g_timeline;
+  pl.p.tl_tag = g_timeline ? g_tl_tag++ : 0u;
   if (gather) {
     const int esz = d.in_dtype == PMX_I8 ? 1 : 2;
     pl.p.g_feats = static_cast<const char*>(gin->feats) + (size_t)d.in_c_offset * esz;
@@ -2064,6 +2110,8 @@ pmx_status conv_tc_deconv_heads(const pmx_conv_desc& d, const void* x, const voi
   p.bn_post = nullptr;
   p.keys = nullptr;
   p.trace = g_trace;
+  p.tl = g_timeline;
+  p.tl_tag = g_timeline ? g_tl_tag++ : 0u;
   p.hstage_mode = hf.stage;
   p.n_heads = hf.n_heads;
   p.hcs = hf.heads_c_stride;
@@ -2106,3 +2154,8 @@ pmx_status conv_tc_deconv_heads(const pmx_conv_desc& d, const void* x, const voi
 }  // namespace pmx
 
 extern "C" void pmx_debug_trace(unsigned long long* buf) { pmx::g_trace = buf; }
+
+extern "C" void pmx_debug_timeline(unsigned long long* buf) {
+  pmx::g_timeline = buf;
+  pmx::g_tl_tag = 0;
+}
