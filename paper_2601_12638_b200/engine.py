@@ -400,7 +400,9 @@ class CompiledGraph:
         format that the tcgen05 gather kernel covers, the PFN writes pillar rows and
         that conv reads them through pillarize's cell map (pmx_conv_gather) -- the
         scatter of pm/tensor_ops.py:138-160 happens in shared memory, never in HBM."""
-        if self.source != "points" or self.pfn is None:
+        import os
+
+        if self.source != "points" or self.pfn is None or os.environ.get("PMX_GATHER") == "0":
             return None
         canvas = self.values[self.graph.layers[2].name]
         cons = self.cons.get(canvas.name, [])

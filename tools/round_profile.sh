@@ -12,7 +12,7 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --c
 echo "list rc=$?" >> $OUT/${TAG}_ncu_list.log
 timeout 600 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
   --profile-from-start off --csv python tools/op_profile.py --op all > $OUT/${TAG}_traffic.csv 2> $OUT/${TAG}_traffic.err
-for op in "conv neck.deblocks.0.0" "conv backbone.blocks.0.0"; do
+for op in "conv neck.deblocks.0.0" "conv backbone.blocks.0.0" "conv backbone.blocks.2.3" "conv backbone.blocks.1.3" "pfn"; do
   f=$(echo "$op" | tr ' ().' '___')
   timeout 600 ncu --set full --clock-control none --import-source on --profile-from-start off \
     -o $OUT/${TAG}_${f} python tools/op_profile.py --op "$op" > $OUT/${TAG}_${f}.log 2>&1
