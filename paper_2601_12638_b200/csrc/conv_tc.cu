@@ -784,7 +784,8 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
     mbar_expect_tx(bfull, p.bres_bytes);
     for (int kb = 0; kb < nk; ++kb) {
       const int tap = kb / p.cblocks, cb = kb % p.cblocks;
-      tma_load_2d(bres + kb * p.bblk_bytes, &maps.b, tap * (p.cblocks * p.kc) + cb * p.kc, 0, bfull);
+      tma_load_2d(bres + kb * p.bblk_bytes, &maps.b, tap * (p.cblocks * p.kc) + cb * p.kc,
+                  (int)(blockIdx.x % (uint32_t)p.n_tiles) * p.bn, bfull);
     }
   }
   if (warp < kEpiWarps) {
@@ -809,7 +810,10 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
       uint32_t it = 0, s = 0, ph = 0;  // ring position, slot, phase
       if (p.mode == MODE_HALO) {
         for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
-          const int tq = (int)fdiv((uint32_t)t, p.fd_tx), tx = t - tq * p.tiles_x;
+          uint32_t mtu, ntu;
+          tile_of((uint32_t)t, mtu, ntu);  // N tile: blockIdx.x % n_tiles for every t
+          const int mt = (int)mtu;
+          const int tq = (int)fdiv((uint32_t)mt, p.fd_tx), tx = mt - tq * p.tiles_x;
           const int tb = (int)fdiv((uint32_t)tq, p.fd_ty);
           const int oy0 = (tq - tb * p.tiles_y) * p.th, ox0 = tx * p.tw;
           PMX_TRACE(0, it);
@@ -919,13 +923,22 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
       const uint32_t b_hi = (uint32_t)(sdesc(0, p.sbo, p.layout) >> 32), b_lo0 = (uint32_t)sdesc(bres, p.sbo, p.layout);
       // resident weights: the B descriptor of every (tap, 32-byte K step), hoisted out of
       // the tile loop
-      uint32_t b_lo_tap[9 * (CINB / 32)];
+      // (256-byte rows: 72 descriptors would spill; those are one IMAD each instead)
+      constexpr bool kHoistB = CINB <= 128;
+      uint32_t b_lo_tap[kHoistB ? 9 * (CINB / 32) : 1];
+      const uint32_t bblk16 = bblk >> 4;
+      if constexpr (kHoistB) {
 #pragma unroll
-      for (int tap = 0; tap < 9; ++tap)
+        for (int tap = 0; tap < 9; ++tap)
 #pragma unroll
-        for (int k = 0; k < CINB / 32; ++k)
-          b_lo_tap[tap * (CINB / 32) + k] =
-              b_lo0 + (((uint32_t)(tap * CB + (k * 32) / KCB) * bblk + (uint32_t)((k * 32) % KCB)) >> 4);
+          for (int k = 0; k < CINB / 32; ++k)
+            b_lo_tap[tap * (CINB / 32) + k] =
+                b_lo0 + (((uint32_t)(tap * CB + (k * 32) / KCB) * bblk + (uint32_t)((k * 32) % KCB)) >> 4);
+      }
+      auto b_lo_of = [&](int tap, int k) -> uint32_t {
+        if constexpr (kHoistB) return b_lo_tap[tap * (CINB / 32) + k];
+        else return b_lo0 + (uint32_t)(tap * CB + (k * 32) / KCB) * bblk16 + (uint32_t)(((k * 32) % KCB) >> 4);
+      };
       mbar_wait(bfull, 0);
       tc_fence_after();
       if (lane == 0) PMX_TRACE(8, 2);
@@ -958,7 +971,7 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
               for (int k = 0; k < CINB / 32; ++k) {
                 const uint32_t aoff = (uint32_t)((((dy + 1) * (int)kHaloW + dx + 1) * CINB + 32 * k) >> 4);
                 const uint64_t ad = ((uint64_t)a_hi << 32) | (a_lo + aoff);
-                const uint64_t bd = ((uint64_t)b_hi << 32) | b_lo_tap[tap * (CINB / 32) + k];
+                const uint64_t bd = ((uint64_t)b_hi << 32) | b_lo_of(tap, k);
                 tc_mma<DT>(d, ad, bd, idesc, (tap | k) != 0);
               }
             }
@@ -968,7 +981,9 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
         } else if (elect_one()) {
           PMX_TRACE(3, i);
           const uint32_t alo = (a_smem + s * p.a_bytes) >> 4;
-#pragma unroll
+          // (256-byte rows: a tap loop, not 72 unrolled descriptors held in registers)
+          constexpr int kTapUnroll = CINB <= 128 ? 9 : 1;
+#pragma unroll kTapUnroll
           for (int tap = 0; tap < 9; ++tap) {
             // A operand of this tap inside the halo: plane base, pixel offset, row width
             const int dy = tap / 3 - 1, dx = tap % 3 - 1;
@@ -985,7 +1000,7 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
               // two 16-byte channel groups per instruction (core matrices at +LBO)
               const uint32_t aoff = (uint32_t)(plane_px * CINB + ((2 * k) * HPX + pix0) * 16);
               const uint64_t ad = ((uint64_t)a_hi << 32) | (alo + ((a_lbo << 16) + (aoff >> 4)));
-              const uint64_t bd = ((uint64_t)b_hi << 32) | b_lo_tap[tap * (CINB / 32) + k];
+              const uint64_t bd = ((uint64_t)b_hi << 32) | b_lo_of(tap, k);
               tc_mma<DT>(d, ad, bd, idesc, (tap | k) != 0);
             }
           }
@@ -1612,6 +1627,14 @@ bool halo_swz_enabled() {
 
 uint32_t halo_swz_width() { return kHaloW; }  // swizzled halo row width (16 px; 10 measured slower)
 
+bool small_halo_enabled() {  // PMX_SMALL_HALO=0: no halo for N-split / 256-byte layers (A/B runs)
+  static const bool on = [] {
+    const char* e = getenv("PMX_SMALL_HALO");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 bool one_slot_enabled() {  // PMX_ONE_SLOT=0: keep the tile slots at one tile per CTA (A/B runs)
   static const bool on = [] {
     const char* e = getenv("PMX_ONE_SLOT");
@@ -1777,8 +1800,13 @@ Plan plan_for(const pmx_conv_desc& d, bool gather = false, bool want_stage = fal
   // weights before its first MMA; the per-K-block ring streams them behind the MMAs
   // instead.  PMX_LAT_TILES = the tiles-per-SM threshold (0: always the halo kernel)
   const bool latency_mode = !gather && (int64_t)p.m_tiles * p.n_tiles <= (int64_t)lat_tiles() * num_sms();
-  if (conv3 && !x3 && !latency_mode && g_conv_backend_mode != 2 && cin_bytes == kc_bytes && p.n_tiles == 1 &&
-      d.out_w >= 8) {
+  // at most one tile per CTA (small batches): the halo also serves 256-byte channel rows
+  // and N-split layers -- every CTA keeps one N tile's weights resident for all its tiles
+  // (grid a multiple of n_tiles) and one halo stage is enough
+  const bool one_tile = tiles <= num_sms() && !gather && small_halo_enabled();
+  if (conv3 && !x3 && !latency_mode && g_conv_backend_mode != 2 &&
+      (cin_bytes == kc_bytes || (one_tile && p.stride == 1 && cin_bytes == 256 && kc_bytes == 128)) &&
+      (p.n_tiles == 1 || one_tile) && d.out_w >= 8) {
     // stride 1: one (16 + 2) x (8 + 2) halo; stride 2: four parity planes of
     // (16 + py) x (8 + px) pixels (561 in total) -- see the producer
     // stride 1, 64 / 128 channel bytes: swizzled pixel-major halo 16 x 18 (PMX_HALO_SWZ=0: off)
@@ -1798,7 +1826,7 @@ Plan plan_for(const pmx_conv_desc& d, bool gather = false, bool want_stage = fal
     // dynamic smem minus alignment, barriers and the alpha / bias copies
     const uint32_t budget0 = 227u * 1024u - 2048u - 8u * (uint32_t)((d.out_c + 3) & ~3) - (gather ? (uint32_t)kGatherSmem : 0u);
     uint32_t budget = budget0 - estage_bytes;
-    const uint32_t two_stages = 2 * halo_al;
+    const uint32_t two_stages = (one_tile ? 1u : 2u) * halo_al;  // (one tile per CTA: one stage)
     if (p.estage2 == 1 && bres_total + two_stages > budget &&
         bres_total + two_stages <= budget0 - (uint32_t)kEpiWarps * 1024u) {
       p.estage2 = 2;  // resident weights + two halo stages fit next to the 1 KB-per-warp staging
@@ -1817,8 +1845,9 @@ Plan plan_for(const pmx_conv_desc& d, bool gather = false, bool want_stage = fal
       p.tiles_x = (int)ceil_div(d.out_w, 8);
       p.tiles_y = (int)ceil_div(d.out_h, 16);
       p.m_tiles = d.batch * p.tiles_x * p.tiles_y;
-      const int64_t t2 = (int64_t)p.m_tiles;
-      pl.grid_x = (int)(t2 < num_sms() ? t2 : num_sms());
+      const int64_t t2 = (int64_t)p.m_tiles * p.n_tiles;
+      const int gmax = (num_sms() / p.n_tiles) * p.n_tiles;  // CTA b keeps N tile b % n_tiles
+      pl.grid_x = (int)(t2 < gmax ? t2 : gmax);
       p.a_bytes = halo_al;
       p.b_bytes = 0;
       int hs = (int)((budget - bres_total) / halo_al);
@@ -2067,6 +2096,9 @@ pmx_status conv_tc_try(const pmx_conv_desc& d, const void* x, const void* w, con
   else if (cinb == 64) { PMX_TC_LAUNCH(DTV, 64, 64, 2); }           \
   else if (cinb == 128 && hs == 1) { PMX_TC_LAUNCH(DTV, 128, 128, 1); } \
   else if (cinb == 128) { PMX_TC_LAUNCH(DTV, 128, 128, 2); }        \
+  else if (cinb == 256 && hs == 1) {                                \
+    s = one_i8 ? launch(conv_tc_kernel<DTV, 1, 128, 256, 1, false>, kThreads) \
+               : launch(conv_tc_kernel<DTV, 0, 128, 256, 1, false>, kThreads); }  \
   else if (kcb == 64) { PMX_TC_LAUNCH_NG(DTV, 64); }                \
   else { PMX_TC_LAUNCH_NG(DTV, 128); }
   if (d.in_dtype == PMX_I8) {
