@@ -423,9 +423,13 @@ class CompiledGraph:
         deconv layers in execution order, or None when the graph / plan does not fit."""
         import os
 
-        # opt-in (PMX_FUSE_HEADS=1): bit-identical, but measured slower than the unfused
-        # deconvs + heads GEMM on the config-4 step (DESIGN.md §8)
-        if self.anchors is None or self.observe or os.environ.get("PMX_FUSE_HEADS", "0") != "1":
+        # bit-identical either way; measured faster at batch 1 (the 20 MB concat round trip
+        # and the heads' launch dominate there: mixed p50 0.272 -> 0.258 ms) and slower from
+        # batch 8 on (config 4: 16.6k -> 15.6k frames/s), so on for B <= 2 by default;
+        # PMX_FUSE_HEADS=1 / 0 forces it (DESIGN.md §8)
+        mode = os.environ.get("PMX_FUSE_HEADS", "")
+        want = mode == "1" or (mode == "" and self.B <= 2)
+        if self.anchors is None or self.observe or not want:
             return None
         a = self.anchors
         by_name = {l.name: l for l in self.graph.layers}
