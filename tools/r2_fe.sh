@@ -1,0 +1,16 @@
+#!/bin/bash
+export PMX_NO_BUILD=1
+mkdir -p gpurun_out
+O=gpurun_out/r2_fe.log
+: > $O
+timeout 1800 python -m pytest tests -m gpu -q -x 2>&1 | tail -4 >> $O
+for v in 1 0; do
+  PMX_DECODE_FUSED=$v timeout 400 python bench.py --steps 20 --warmup 5 --no-cpu-baseline > gpurun_out/r2_fe_$v.json 2>gpurun_out/r2_fe_$v.err
+  echo "== PMX_DECODE_FUSED=$v rc=$?" >> $O
+  python - gpurun_out/r2_fe_$v.json >> $O <<'PY'
+import json,sys
+d=[json.loads(l) for l in open(sys.argv[1]) if l.startswith("{")][0]
+print(round(d["value"]), d["op_ms"], {k: round(v,4) for k,v in d["latency"].items() if isinstance(v,(int,float))})
+PY
+done
+PMX_NECK_STREAM=0 timeout 600 python tools/b1_prefix.py > gpurun_out/r2_prefix2.log 2>&1
