@@ -409,20 +409,24 @@ constexpr int kThreadsGather = kThreads + 32 * (kGatherWarps - 1);
 // rint(q) is already the code (pm/quant.py:98-103 semantics, no clip needed); NaN /
 // Inf / saturation / near-ties return false and the caller takes the exact path.
 // RELU: relu(y) then quantize == max(code, 0): negative bytes are zeroed with a
-// sign-replicating byte permute.  ~4.5 instructions per value.
+// sign-replicating byte permute.  ~4 instructions per value.
 template <bool RELU>
 __device__ __forceinline__ bool quant16_noclamp(const float (&y)[16], float inv, uint4& out) {
   const float2 M2 = make_float2(12582912.0f, 12582912.0f), I2 = make_float2(inv, inv);
   uint32_t tb[16];
-  float dm = 0.0f, qm = 0.0f;
+  float dm = 0.0f, rm = 0.0f;
 #pragma unroll
   for (int j = 0; j < 16; j += 2) {
-    const float2 q = __fmul2_rn(make_float2(y[j], y[j + 1]), I2);
-    const float2 t = __fadd2_rn(q, M2);                                  // rint(q) in the low bits
-    const float2 r = __fadd2_rn(t, make_float2(-12582912.0f, -12582912.0f));  // rint(q), exact
-    const float2 d = __fadd2_rn(q, make_float2(-r.x, -r.y));             // q - rint(q), exact
+    // t = RN(y * inv + M): the exact product rounded once to an integer (ties to even)
+    // in the low mantissa bits; r = that integer; d = RN(y * inv - r), the product's
+    // distance to it.  |d| < kTieBand => r == rint(y / s) (|y * inv - y / s| < 8e-6 for
+    // |y / s| < 128), |r| <= 127 => no clamp.  5 instructions per pair.
+    const float2 yy = make_float2(y[j], y[j + 1]);
+    const float2 t = __ffma2_rn(yy, I2, M2);
+    const float2 r = __fadd2_rn(t, make_float2(-12582912.0f, -12582912.0f));
+    const float2 d = __ffma2_rn(yy, I2, make_float2(-r.x, -r.y));
     dm = fmax3_nan(dm, fabsf(d.x), fabsf(d.y));
-    qm = fmax3_nan(qm, fabsf(q.x), fabsf(q.y));
+    rm = fmax3_nan(rm, fabsf(r.x), fabsf(r.y));
     tb[j] = __float_as_uint(t.x);
     tb[j + 1] = __float_as_uint(t.y);
   }
@@ -440,7 +444,7 @@ __device__ __forceinline__ bool quant16_noclamp(const float (&y)[16], float inv,
     }
   }
   out = make_uint4(w[0], w[1], w[2], w[3]);
-  return dm < kTieBand && qm < 127.0f;
+  return dm < kTieBand && rm < 127.5f;
 }
 
 // One chunk (16 accumulator columns of one pixel row): y = acc * alpha + bias (int8)
