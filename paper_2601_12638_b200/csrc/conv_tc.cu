@@ -131,6 +131,14 @@ __device__ __forceinline__ void tma_load_4d_pair(uint32_t dst, const CUtensorMap
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar & kPeerMask)
       : "memory");
 }
+__device__ __forceinline__ void tma_load_5d_pair(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
+                                                 int c4, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
+      "%4, %5, %6}], [%7];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(bar & kPeerMask)
+      : "memory");
+}
 // MMA completion -> the barrier at this offset in BOTH CTAs of the pair
 __device__ __forceinline__ void tc_commit_pair(uint32_t bar) {
   asm volatile(
@@ -785,11 +793,14 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
   // written) only after griddepcontrol.wait.  The next layer may start launching now.
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (p.mode == MODE_HALO && warp == kProdWarp && lane == 0) {
-    mbar_expect_tx(bfull, p.bres_bytes);
+    // PAIR: each CTA holds its half of the N tile's weights; both halves complete on the
+    // leader's barrier
+    if (!PAIR || rank == 0) mbar_expect_tx(bfull, (PAIR ? 2u : 1u) * p.bres_bytes);
+    const int nb0 = PAIR ? (int)rank * (p.bn >> 1) : (int)(blockIdx.x % (uint32_t)p.n_tiles) * p.bn;
     for (int kb = 0; kb < nk; ++kb) {
       const int tap = kb / p.cblocks, cb = kb % p.cblocks;
-      tma_load_2d(bres + kb * p.bblk_bytes, &maps.b, tap * (p.cblocks * p.kc) + cb * p.kc,
-                  (int)(blockIdx.x % (uint32_t)p.n_tiles) * p.bn, bfull);
+      if constexpr (PAIR) tma_load_2d_pair(bres + kb * p.bblk_bytes, &maps.b, tap * (p.cblocks * p.kc) + cb * p.kc, nb0, bfull);
+      else tma_load_2d(bres + kb * p.bblk_bytes, &maps.b, tap * (p.cblocks * p.kc) + cb * p.kc, nb0, bfull);
     }
   }
   if (warp < kEpiWarps) {
@@ -813,7 +824,7 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
       // ---------------- TMA producer
       uint32_t it = 0, s = 0, ph = 0;  // ring position, slot, phase
       if (p.mode == MODE_HALO) {
-        for (int t = blockIdx.x; t < total; t += gridDim.x, ++it) {
+        for (int t = tstart; t < total; t += tstride, ++it) {
           uint32_t mtu, ntu;
           tile_of((uint32_t)t, mtu, ntu);  // N tile: blockIdx.x % n_tiles for every t
           const int mt = (int)mtu;
@@ -831,18 +842,25 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
             continue;
           }
 #endif
-          mbar_expect_tx(full(s), p.halo_tx);
+          // PAIR: both CTAs' halos complete on the leader's barrier
+          if (!PAIR || rank == 0) mbar_expect_tx(full(s), (PAIR ? 2u : 1u) * p.halo_tx);
           const uint32_t slot = a_smem + s * p.a_bytes;
           if (p.stride == 1) {
-            if (p.hswz) tma_load_4d(slot, &maps.a[0], 0, ox0 - 1, oy0 - 1, tb, full(s));
-            else tma_load_5d(slot, &maps.a[0], 0, ox0 - 1, oy0 - 1, 0, tb, full(s));
+            if (p.hswz) {
+              if constexpr (PAIR) tma_load_4d_pair(slot, &maps.a[0], 0, ox0 - 1, oy0 - 1, tb, full(s));
+              else tma_load_4d(slot, &maps.a[0], 0, ox0 - 1, oy0 - 1, tb, full(s));
+            } else {
+              if constexpr (PAIR) tma_load_5d_pair(slot, &maps.a[0], 0, ox0 - 1, oy0 - 1, 0, tb, full(s));
+              else tma_load_5d(slot, &maps.a[0], 0, ox0 - 1, oy0 - 1, 0, tb, full(s));
+            }
           } else {
             // four parity planes (py, px): (16 + py) x (8 + px) pixels from (oy0 - py, ox0 - px)
             uint32_t off = 0;
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
               const int py = q >> 1, px = q & 1;
-              tma_load_5d(slot + off, &maps.a[q], 0, ox0 - px, oy0 - py, 0, tb, full(s));
+              if constexpr (PAIR) tma_load_5d_pair(slot + off, &maps.a[q], 0, ox0 - px, oy0 - py, 0, tb, full(s));
+              else tma_load_5d(slot + off, &maps.a[q], 0, ox0 - px, oy0 - py, 0, tb, full(s));
               off += (uint32_t)((16 + py) * (8 + px)) * p.cin_bytes;
             }
           }
@@ -943,11 +961,12 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
         if constexpr (kHoistB) return b_lo_tap[tap * (CINB / 32) + k];
         else return b_lo0 + (uint32_t)(tap * CB + (k * 32) / KCB) * bblk16 + (uint32_t)(((k * 32) % KCB) >> 4);
       };
-      mbar_wait(bfull, 0);
+      if (!PAIR || rank == 0) mbar_wait(bfull, 0);  // (PAIR: both halves land on the leader's barrier)
       tc_fence_after();
       if (lane == 0) PMX_TRACE(8, 2);
       uint32_t s = 0, ph = 0, acc = 0, aph = 0;  // smem stage / accumulator and their phases
-      for (int t = blockIdx.x; t < total; t += gridDim.x, ++i) {
+      // PAIR: only the leader issues (M = 256 over both CTAs' halos, N over both B halves)
+      for (int t = tstart; t < total && (!PAIR || rank == 0); t += tstride, ++i) {
         if (lane == 0) PMX_TRACE(9, i);
         mbar_spin(tempty(acc), aph ^ 1);
         tc_fence_after();
@@ -976,11 +995,17 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
                 const uint32_t aoff = (uint32_t)((((dy + 1) * (int)kHaloW + dx + 1) * CINB + 32 * k) >> 4);
                 const uint64_t ad = ((uint64_t)a_hi << 32) | (a_lo + aoff);
                 const uint64_t bd = ((uint64_t)b_hi << 32) | b_lo_of(tap, k);
-                tc_mma<DT>(d, ad, bd, idesc, (tap | k) != 0);
+                if constexpr (PAIR) tc_mma_pair<DT>(d, ad, bd, idesc, (tap | k) != 0);
+                else tc_mma<DT>(d, ad, bd, idesc, (tap | k) != 0);
               }
             }
-            tc_commit(empty(s));
-            tc_commit(tfull(acc));
+            if constexpr (PAIR) {
+              tc_commit_pair(empty(s));
+              tc_commit_pair(tfull(acc));
+            } else {
+              tc_commit(empty(s));
+              tc_commit(tfull(acc));
+            }
           }
         } else if (elect_one()) {
           PMX_TRACE(3, i);
@@ -1005,11 +1030,17 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
               const uint32_t aoff = (uint32_t)(plane_px * CINB + ((2 * k) * HPX + pix0) * 16);
               const uint64_t ad = ((uint64_t)a_hi << 32) | (alo + ((a_lbo << 16) + (aoff >> 4)));
               const uint64_t bd = ((uint64_t)b_hi << 32) | b_lo_of(tap, k);
-              tc_mma<DT>(d, ad, bd, idesc, (tap | k) != 0);
+              if constexpr (PAIR) tc_mma_pair<DT>(d, ad, bd, idesc, (tap | k) != 0);
+              else tc_mma<DT>(d, ad, bd, idesc, (tap | k) != 0);
             }
           }
-          tc_commit(empty(s));
-          tc_commit(tfull(acc));
+          if constexpr (PAIR) {
+            tc_commit_pair(empty(s));
+            tc_commit_pair(tfull(acc));
+          } else {
+            tc_commit(empty(s));
+            tc_commit(tfull(acc));
+          }
           PMX_TRACE(4, i);
         }
         __syncwarp();
@@ -1631,6 +1662,14 @@ bool halo_swz_enabled() {
 
 uint32_t halo_swz_width() { return kHaloW; }  // swizzled halo row width (16 px; 10 measured slower)
 
+bool halo_pair_enabled() {  // PMX_HALO_PAIR=1: 2-CTA pairs in the halo mode (experiment, off)
+  static const bool on = [] {
+    const char* e = getenv("PMX_HALO_PAIR");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 bool small_halo_enabled() {  // PMX_SMALL_HALO=0: no halo for N-split / 256-byte layers (A/B runs)
   static const bool on = [] {
     const char* e = getenv("PMX_SMALL_HALO");
@@ -1825,7 +1864,13 @@ Plan plan_for(const pmx_conv_desc& d, bool gather = false, bool want_stage = fal
     const uint32_t hw = p.hswz ? swz_w : 10, hp = p.stride == 1 ? (p.hswz ? 18u * swz_w : 180u) : 561u;
     const uint32_t halo = hp * (uint32_t)cin_bytes;
     const uint32_t halo_al = (halo + 1023u) & ~1023u;
-    const uint32_t bblk = (uint32_t)bn * kc_bytes;
+    // CTA pairs (cta_group::2, M = 256, int8): each CTA keeps half of the N tile's
+    // weights resident and reads its halo plus half of B per MMA
+    // (measured slower on blocks 0 / 1 -- 79 -> 89 us, 54 -> 61 us -- except the (int8, f16)
+    // pair-output layer 1.15; opt-in PMX_HALO_PAIR=1)
+    const bool hpair = halo_pair_enabled() && !gather && !heads && d.in_dtype == PMX_I8 && pair_enabled() && !one_tile &&
+                       p.n_tiles == 1 && bn % 32 == 0 && tiles >= 2LL * num_sms() && num_sms() >= 2;
+    const uint32_t bblk = (uint32_t)(hpair ? bn / 2 : bn) * kc_bytes;
     const uint32_t bres_total = 9u * p.cblocks * bblk;
     // dynamic smem minus alignment, barriers and the alpha / bias copies
     const uint32_t budget0 = 227u * 1024u - 2048u - 8u * (uint32_t)((d.out_c + 3) & ~3) - (gather ? (uint32_t)kGatherSmem : 0u);
@@ -1852,6 +1897,12 @@ Plan plan_for(const pmx_conv_desc& d, bool gather = false, bool want_stage = fal
       const int64_t t2 = (int64_t)p.m_tiles * p.n_tiles;
       const int gmax = (num_sms() / p.n_tiles) * p.n_tiles;  // CTA b keeps N tile b % n_tiles
       pl.grid_x = (int)(t2 < gmax ? t2 : gmax);
+      if (hpair) {
+        p.pair = 1;
+        const int64_t pt = (int64_t)((p.m_tiles + 1) / 2);
+        const int gm2 = num_sms() & ~1;
+        pl.grid_x = (int)(2 * pt < gm2 ? 2 * pt : gm2);
+      }
       p.a_bytes = halo_al;
       p.b_bytes = 0;
       int hs = (int)((budget - bres_total) / halo_al);
@@ -1886,18 +1937,18 @@ Plan plan_for(const pmx_conv_desc& d, bool gather = false, bool want_stage = fal
     p.idesc = (1u << 4) | (0u << 7) | (0u << 10) | (n_enc << 17) | (m_enc << 24);
   // CTA pairs for the TMA-ring modes with a wide N tile: each SM then reads its own A and
   // HALF of B from shared memory per MMA (operand bandwidth is what limits these layers)
-  p.pair = 0;
+  // (the halo mode decided its own pairing above)
   if (!gather && !heads && !x3 && p.mode == MODE_CONV3 && bn >= 128 && bn % 32 == 0 && pair_enabled() &&
       (int64_t)p.m_tiles * p.n_tiles >= 2LL * num_sms() && num_sms() >= 2) {
     p.pair = 1;
     p.b_bytes = (uint32_t)(bn / 2) * kc_bytes;
     int st2 = (int)((200u * 1024u - 8u * (uint32_t)d.out_c - estage_bytes) / (p.a_bytes + p.b_bytes));
     p.stages = st2 > 12 ? 12 : (st2 < 2 ? 2 : st2);
-    p.idesc = (p.idesc & ~(0x1Fu << 24)) | ((256u >> 4) << 24);  // M = 256 over the pair
     const int64_t pair_tiles = (int64_t)((p.m_tiles + 1) / 2) * p.n_tiles;
     const int gmax = num_sms() & ~1;
     pl.grid_x = (int)(2 * pair_tiles < gmax ? 2 * pair_tiles : gmax);
   }
+  if (p.pair) p.idesc = (p.idesc & ~(0x1Fu << 24)) | ((256u >> 4) << 24);  // M = 256 over the pair
   pl.smem = 1024 + (size_t)p.stages * (p.a_bytes + p.b_bytes) + p.bres_bytes + (2 * p.stages + 2 * p.nacc + 1) * 8 + 32 +
             8 * (size_t)((d.out_c + 3) & ~3) + (gather ? kGatherSmem : 0) + (estage_bytes ? 16 + estage_bytes : 0) +
             (heads ? 16 + kHeadsSmem : 0);
@@ -2095,6 +2146,9 @@ pmx_status conv_tc_try(const pmx_conv_desc& d, const void* x, const void* w, con
   else                                                                                                         \
     s = one_i8 ? launch(conv_tc_kernel<DTV, 1, KB, 0, 0, false>, kThreads)                                    \
                : launch(conv_tc_kernel<DTV, 0, KB, 0, 0, false>, kThreads)
+#define PMX_TC_HPAIR(DTV, KB, CB, HSV)                                                                         \
+  s = one_i8 ? launch(conv_tc_kernel<DTV, 1, KB, CB, HSV, false, true>, kThreads)                              \
+             : launch(conv_tc_kernel<DTV, 0, KB, CB, HSV, false, true>, kThreads)
 #define PMX_TC_SHAPES(DTV)                                          \
   if (cinb == 64 && hs == 1) { PMX_TC_LAUNCH(DTV, 64, 64, 1); }     \
   else if (cinb == 64) { PMX_TC_LAUNCH(DTV, 64, 64, 2); }           \
@@ -2105,7 +2159,12 @@ pmx_status conv_tc_try(const pmx_conv_desc& d, const void* x, const void* w, con
                : launch(conv_tc_kernel<DTV, 0, 128, 256, 1, false>, kThreads); }  \
   else if (kcb == 64) { PMX_TC_LAUNCH_NG(DTV, 64); }                \
   else { PMX_TC_LAUNCH_NG(DTV, 128); }
-  if (d.in_dtype == PMX_I8) {
+  if (d.in_dtype == PMX_I8 && pl.p.pair && pl.p.mode == MODE_HALO) {
+    if (cinb == 64 && hs == 1) { PMX_TC_HPAIR(PMX_I8, 64, 64, 1); }
+    else if (cinb == 64) { PMX_TC_HPAIR(PMX_I8, 64, 64, 2); }
+    else if (cinb == 128 && hs == 1) { PMX_TC_HPAIR(PMX_I8, 128, 128, 1); }
+    else { PMX_TC_HPAIR(PMX_I8, 128, 128, 2); }
+  } else if (d.in_dtype == PMX_I8) {
     PMX_TC_SHAPES(PMX_I8)
   } else if (d.in_dtype == PMX_F32X2) {
     PMX_TC_LAUNCH_NG(PMX_F32X2, 128);  // 3xTF32: TMA per K-block (no halo variants)
@@ -2113,6 +2172,7 @@ pmx_status conv_tc_try(const pmx_conv_desc& d, const void* x, const void* w, con
     PMX_TC_SHAPES(PMX_F16)
   }
 #undef PMX_TC_SHAPES
+#undef PMX_TC_HPAIR
 #undef PMX_TC_LAUNCH
 #undef PMX_TC_LAUNCH_NG
   if (s != PMX_OK) return s;

@@ -220,3 +220,45 @@ def test_pair_plan_selected(case):
         lib.pmx_set_conv_backend(0)
     assert code & 1 and code & 2, code
     assert (code >> 2) & 3 == 0  # the per-tap TMA ring (pairs are never planned for halo / GEMM)
+
+
+def test_halo_pair_opt_in_bit_exact():
+    """The opt-in 2-CTA halo path (PMX_HALO_PAIR=1, read once per process: a subprocess)
+    is planned for large int8 halo layers and matches the SIMT kernel bit for bit."""
+    import os
+    import subprocess
+    import sys
+
+    code = r'''
+import ctypes, numpy as np, torch
+from paper_2601_12638_b200 import _native as N
+lib = N.load()
+for (cin, cout, s, h, w, b) in [(64, 64, 1, 248, 216, 2), (64, 64, 2, 496, 432, 1), (128, 128, 1, 124, 108, 4)]:
+    oh, ow = (h - 1) // s + 1, (w - 1) // s + 1
+    d = N.ConvDesc(kind=N.PMX_CONV2D, in_dtype=N.PMX_I8, batch=b, in_h=h, in_w=w, in_c=cin, in_c_stride=cin,
+                   in_c_offset=0, out_c=cout, k_h=3, k_w=3, stride_h=s, stride_w=s, pad_h=1, pad_w=1, out_h=oh,
+                   out_w=ow, relu=1)
+    plan = lib.pmx_conv_tc_supported(ctypes.byref(d))
+    assert plan & 2 and (plan >> 2) & 3 == 2, plan
+    rng = np.random.default_rng(cin + s + h)
+    x = torch.from_numpy(rng.integers(-128, 128, size=(b, h, w, cin), dtype=np.int8)).cuda()
+    wt = torch.from_numpy(rng.integers(-128, 128, size=(cout, 9 * cin), dtype=np.int8)).cuda()
+    alpha = torch.full((cout,), 2.0 ** -12, device="cuda")
+    bias = torch.from_numpy((rng.integers(-8, 8, cout) / 8.0).astype(np.float32)).cuda()
+    outs = []
+    for mode in (0, 1):
+        y = torch.zeros((b, oh, ow, cout), dtype=torch.int8, device="cuda")
+        arr, n = N.outs_array([N.Out(ptr=y.data_ptr(), scale=0.5, dtype=N.PMX_I8, c_stride=cout, c_offset=0)])
+        lib.pmx_set_conv_backend(mode)
+        N.check(lib.pmx_conv(ctypes.byref(d), x.data_ptr(), wt.data_ptr(), alpha.data_ptr(), bias.data_ptr(), None,
+                             arr, n, None, None, 0, N.stream_ptr()))
+        torch.cuda.synchronize()
+        lib.pmx_set_conv_backend(0)
+        outs.append(y)
+    assert torch.equal(outs[0], outs[1]), (cin, s)
+print("halo pair ok")
+'''
+    env = dict(os.environ, PMX_HALO_PAIR="1", PMX_NO_BUILD="1")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600,
+                       cwd=str(__import__("pathlib").Path(__file__).resolve().parent.parent))
+    assert r.returncode == 0 and "halo pair ok" in r.stdout, r.stdout + r.stderr
