@@ -908,6 +908,7 @@ class CompiledGraph:
         ws_bytes = lib.pmx_decode_workspace(ctypes.byref(d), B, H, W)
         ws = self.torch.empty(max(ws_bytes, 1), dtype=self.torch.uint8, device="cuda")
         self._keep.append(ws)
+        self.decode_ws = ws  # (diagnostics: tools/decode_probe.py reads the candidate counts)
         ctot = self.head_ctot
         self.ops.append(("decode", lambda s: N.check(lib.pmx_decode_topk(
             ctypes.byref(d), B, H, W, self.heads_cat.data_ptr(), ctot, 0, A, 8 * A, self.topk_idx.data_ptr(),
