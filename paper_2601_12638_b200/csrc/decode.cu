@@ -59,14 +59,19 @@ __device__ __forceinline__ unsigned long long cand_key(const float* __restrict__
   return ((unsigned long long)f2key(logit) << 32) | (unsigned long long)(0xffffffffu - (uint32_t)i);
 }
 
-// last CTA of frame b to arrive on counter *ctr (all its global writes fenced)
+// last CTA of frame b to arrive on counter *ctr: the block barrier orders every thread's
+// writes before thread 0's gpu-scope acq_rel add (release is cumulative), and the last
+// arriver's acquire + the second barrier make the other CTAs' writes visible to all its
+// threads -- one fenced atomic per CTA instead of a membar.gl per thread
 __device__ __forceinline__ bool last_arrival(int* ctr, int n_ctas) {
   __shared__ int last;
-  __threadfence();
   __syncthreads();
-  if (threadIdx.x == 0) last = atomicAdd(ctr, 1) == n_ctas - 1;
+  if (threadIdx.x == 0) {
+    int old;
+    asm volatile("atom.add.acq_rel.gpu.s32 %0, [%1], 1;" : "=r"(old) : "l"(ctr) : "memory");
+    last = old == n_ctas - 1;
+  }
   __syncthreads();
-  if (last) __threadfence();
   return last;
 }
 
