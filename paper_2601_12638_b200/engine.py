@@ -463,16 +463,26 @@ class CompiledGraph:
                               out_h=Ho, out_w=Wo, relu=int(d.relu))
             if not self.lib.pmx_deconv_heads_supported(ctypes.byref(desc)):
                 return None
-        # all three run once the last of their inputs exists, largest stride first: the
-        # partial sums live in that deconv's sub-pixel-phase layout, and the stride-1 one
-        # finishes the heads into the NHWC heads block with contiguous rows
-        order = sorted(deconvs, key=lambda d: (-d.weight.shape[2], self.graph.layers.index(d)))
+        neck = os.environ.get("PMX_NECK_STREAM", "auto")
+        if neck == "1" or (neck == "auto" and self.B <= 8):
+            # small batches: graph order (stride 1, 2, 4), so the first two run on the neck
+            # side stream as soon as their block is done (_plan_branches) and the last one
+            # finishes the heads; the int32 partial sums are order-free (bit-identical)
+            order = sorted(deconvs, key=lambda d: self.graph.layers.index(d))
+            each = True
+        else:
+            # all three once the last of their inputs exists, largest stride first: the
+            # partial sums live in that deconv's sub-pixel-phase layout, and the stride-1
+            # one finishes the heads into the NHWC heads block with contiguous rows
+            order = sorted(deconvs, key=lambda d: (-d.weight.shape[2], self.graph.layers.index(d)))
+            each = False
         ps = order[0].weight.shape[2]
         _, Ho, Wo, _ = self.values[src].shape
         if ps & (ps - 1) or Ho % ps or Wo % ps:
             return None
         last = max(deconvs, key=lambda d: self.graph.layers.index(d))
-        return {"deconvs": order, "concat": src, "heads": hs, "fmt": next(iter(fmts)), "ps": ps, "emit_at": last}
+        return {"deconvs": order, "concat": src, "heads": hs, "fmt": next(iter(fmts)), "ps": ps, "emit_at": last,
+                "each": each}
 
     def _is_concat(self, name):
         for l in self.graph.layers:
@@ -680,7 +690,9 @@ class CompiledGraph:
                     self._op_heads_fused(fused)
                 continue
             if self.hfuse and l in self.hfuse["deconvs"]:
-                if l is self.hfuse["emit_at"]:
+                if self.hfuse["each"]:
+                    self._op_deconv_heads(l)
+                elif l is self.hfuse["emit_at"]:
                     for d in self.hfuse["deconvs"]:
                         self._op_deconv_heads(d)
                 continue
@@ -929,13 +941,22 @@ class CompiledGraph:
 
         self.branch_src, self.joins = {}, {}
         mode = os.environ.get("PMX_NECK_STREAM", "auto")
-        if mode == "0" or (mode == "auto" and self.B > 8) or self.anchors is None or self.hfuse:
+        if mode == "0" or (mode == "auto" and self.B > 8) or self.anchors is None:
+            return
+        if self.hfuse and not self.hfuse["each"]:
             return
         names = [n for n, _ in self.ops]
-        head_op = "conv heads(fused)"
+        if self.hfuse:
+            # fused deconv + heads stages: the first ones on the side stream (in stage order),
+            # the finishing stage joins them
+            suffix = "+heads"
+            head_op = f"conv {self.hfuse['deconvs'][-1].name}+heads"
+        else:
+            suffix = ""
+            head_op = "conv heads(fused)"
         if head_op not in names:
             return
-        deconvs = [l for l in self.graph.layers if l.kind == "deconv2d" and f"conv {l.name}" in names]
+        deconvs = [l for l in self.graph.layers if l.kind == "deconv2d" and f"conv {l.name}{suffix}" in names]
         if not deconvs:
             return
         last_src = max(names.index(f"conv {self.layer_src[d.name][0]}") for d in deconvs
@@ -943,7 +964,7 @@ class CompiledGraph:
         for d in deconvs:
             src = f"conv {self.layer_src[d.name][0]}"
             if src in names and names.index(src) < last_src:  # the last one gains nothing
-                self.branch_src[f"conv {d.name}"] = src
+                self.branch_src[f"conv {d.name}{suffix}"] = src
         if self.branch_src:
             self.joins[head_op] = list(self.branch_src)
             torch = self.torch
