@@ -26,6 +26,14 @@ int decode_chunk(int batch) {
   return batch >= 8 ? 16384 : (batch >= 2 ? 8192 : 4096);  // measured: b32 68 us, b1 23 us
 }
 constexpr int kThreads = 1024;
+
+bool fused_enabled() {  // PMX_DECODE_FUSED=0: always the two-kernel path (A/B runs)
+  static const bool on = [] {
+    const char* e = getenv("PMX_DECODE_FUSED");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 constexpr int kCap = 4096;    // candidates sorted in shared memory
 
 template <int N>
@@ -75,6 +83,38 @@ __device__ __forceinline__ bool last_arrival(int* ctr, int n_ctas) {
   return last;
 }
 
+// the bin (key >> 53) holding the k-th largest key of the frame's histogram -> *thr as
+// a 32-bit key prefix (0: fewer candidates than k, keep all); blockDim.x == kBins / 2
+__device__ void hist_threshold(const int* hb, int k, uint32_t* thr) {
+  __shared__ int sh[32];
+  // thread t owns bins (from the top) 2t, 2t+1; inclusive scan of counts from the top
+  const int t = threadIdx.x;
+  const int c0 = __ldcg(hb + kBins - 1 - 2 * t), c1 = __ldcg(hb + kBins - 2 - 2 * t);
+  int v = c0 + c1;
+  const int lane = t & 31, wid = t >> 5;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int u = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += u;
+  }
+  if (lane == 31) sh[wid] = v;
+  __syncthreads();
+  if (wid == 0) {
+    int s = sh[lane];
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(0xffffffffu, s, o);
+      if (lane >= o) s += u;
+    }
+    sh[lane] = s;
+  }
+  __syncthreads();
+  const int incl = v + (wid > 0 ? sh[wid - 1] : 0);
+  const int excl = incl - c0 - c1;
+  // the first bin (from the top) whose inclusive count reaches k
+  if (excl < k && excl + c0 >= k) *thr = (uint32_t)(kBins - 1 - 2 * t) << 21;
+  else if (excl + c0 < k && incl >= k) *thr = (uint32_t)(kBins - 2 - 2 * t) << 21;
+  if (t == blockDim.x - 1 && incl < k) *thr = 0u;  // fewer candidates than k: keep all
+}
+
 __global__ void __launch_bounds__(kThreads) topk_hist(const float* __restrict__ heads, int c_stride, int cls_off,
                                                       int n_anchors, int64_t ncand, int k, int* hist, int* arrive,
                                                       uint32_t* thresh, int chunk, unsigned long long* keys) {
@@ -100,32 +140,7 @@ __global__ void __launch_bounds__(kThreads) topk_hist(const float* __restrict__ 
   for (int t = threadIdx.x; t < kBins; t += blockDim.x)
     if (h[t]) atomicAdd(hb + t, h[t]);
   if (!last_arrival(arrive + b, gridDim.x)) return;
-  // thread t owns bins (from the top) 2t, 2t+1; inclusive scan of counts from the top
-  const int t = threadIdx.x;
-  const int c0 = __ldcg(hb + kBins - 1 - 2 * t), c1 = __ldcg(hb + kBins - 2 - 2 * t);
-  int v = c0 + c1;
-  const int lane = t & 31, wid = t >> 5;
-  for (int o = 1; o < 32; o <<= 1) {
-    const int u = __shfl_up_sync(0xffffffffu, v, o);
-    if (lane >= o) v += u;
-  }
-  if (lane == 31) sh[wid] = v;
-  __syncthreads();
-  if (wid == 0) {
-    int s = sh[lane];
-    for (int o = 1; o < 32; o <<= 1) {
-      const int u = __shfl_up_sync(0xffffffffu, s, o);
-      if (lane >= o) s += u;
-    }
-    sh[lane] = s;
-  }
-  __syncthreads();
-  const int incl = v + (wid > 0 ? sh[wid - 1] : 0);
-  const int excl = incl - c0 - c1;
-  // the first bin (from the top) whose inclusive count reaches k
-  if (excl < k && excl + c0 >= k) thresh[b] = (uint32_t)(kBins - 1 - 2 * t) << 21;
-  else if (excl + c0 < k && incl >= k) thresh[b] = (uint32_t)(kBins - 2 - 2 * t) << 21;
-  if (t == blockDim.x - 1 && incl < k) thresh[b] = 0u;  // fewer candidates than k: keep all
+  hist_threshold(hb, k, thresh + b);
 }
 
 __device__ void decode_one(const pmx_anchor_desc& d, unsigned long long key, int b, int r, int out_h, int out_w,
@@ -175,41 +190,12 @@ __device__ void decode_one(const pmx_anchor_desc& d, unsigned long long key, int
   dir_label[o] = label;
 }
 
-__global__ void __launch_bounds__(kThreads) topk_select(
-    const pmx_anchor_desc d, const float* __restrict__ heads, int c_stride, int cls_off, int box_off, int dir_off,
-    int out_h, int out_w, const uint32_t* __restrict__ thresh, unsigned long long* cand, int* cnt, int* arrive,
-    int32_t* topk_idx, float* topk_logit, float* boxes, int32_t* dir_label, int chunk,
-    const unsigned long long* __restrict__ keys) {
-  pdl_begin();
-  __shared__ unsigned long long s[kCap];
+// last CTA of frame b: rank the frame's n candidate keys (cb) and decode the top k
+__device__ void finish_frame(const pmx_anchor_desc& d, int b, int n, const unsigned long long* cb, unsigned long long* s,
+                             const float* __restrict__ heads, int c_stride, int box_off, int dir_off, int out_h,
+                             int out_w, int32_t* topk_idx, float* topk_logit, float* boxes, int32_t* dir_label) {
   __shared__ int sh_hist[256];
   __shared__ int sh_n, sh_sel[2];
-  const int b = blockIdx.y;
-  const int n_anchors = d.n_anchors;
-  const int64_t ncand = (int64_t)out_h * out_w * n_anchors;
-  const uint32_t T = thresh[b];
-  const int lane = threadIdx.x & 31;
-  unsigned long long* cb = cand + (int64_t)b * ncand;
-  const int64_t base = (int64_t)blockIdx.x * chunk;
-  for (int t0 = 0; t0 < chunk; t0 += blockDim.x) {
-    const int64_t i = base + t0 + threadIdx.x;
-    unsigned long long key = 0ull;
-    bool keep = false;
-    if (i < ncand) {
-      key = __ldcs(keys + (int64_t)b * ncand + i);  // written by pass 1 (streaming: read once)
-      keep = (uint32_t)(key >> 32) >= T;
-    }
-    const unsigned m = __ballot_sync(0xffffffffu, keep);
-    if (!m) continue;
-    int slot = 0;
-    if (lane == 0) slot = atomicAdd(cnt + b, __popc(m));
-    slot = __shfl_sync(0xffffffffu, slot, 0);
-    if (keep) cb[slot + __popc(m & ((1u << lane) - 1u))] = key;
-  }
-  if (!last_arrival(arrive + b, gridDim.x)) return;
-
-  // ---- last CTA of the frame: rank the n candidates, decode the top k
-  const int n = __ldcg(cnt + b);
   const int k = d.k;
   if (n <= kCap) {
     int np = 2;
@@ -261,6 +247,112 @@ __global__ void __launch_bounds__(kThreads) topk_select(
                dir_label);
 }
 
+__global__ void __launch_bounds__(kThreads) topk_select(
+    const pmx_anchor_desc d, const float* __restrict__ heads, int c_stride, int cls_off, int box_off, int dir_off,
+    int out_h, int out_w, const uint32_t* __restrict__ thresh, unsigned long long* cand, int* cnt, int* arrive,
+    int32_t* topk_idx, float* topk_logit, float* boxes, int32_t* dir_label, int chunk,
+    const unsigned long long* __restrict__ keys) {
+  pdl_begin();
+  __shared__ unsigned long long s[kCap];
+  const int b = blockIdx.y;
+  const int n_anchors = d.n_anchors;
+  const int64_t ncand = (int64_t)out_h * out_w * n_anchors;
+  const uint32_t T = thresh[b];
+  const int lane = threadIdx.x & 31;
+  unsigned long long* cb = cand + (int64_t)b * ncand;
+  const int64_t base = (int64_t)blockIdx.x * chunk;
+  for (int t0 = 0; t0 < chunk; t0 += blockDim.x) {
+    const int64_t i = base + t0 + threadIdx.x;
+    unsigned long long key = 0ull;
+    bool keep = false;
+    if (i < ncand) {
+      key = __ldcs(keys + (int64_t)b * ncand + i);  // written by pass 1 (streaming: read once)
+      keep = (uint32_t)(key >> 32) >= T;
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, keep);
+    if (!m) continue;
+    int slot = 0;
+    if (lane == 0) slot = atomicAdd(cnt + b, __popc(m));
+    slot = __shfl_sync(0xffffffffu, slot, 0);
+    if (keep) cb[slot + __popc(m & ((1u << lane) - 1u))] = key;
+  }
+  if (!last_arrival(arrive + b, gridDim.x)) return;
+
+  finish_frame(d, b, __ldcg(cnt + b), cb, s, heads, c_stride, box_off, dir_off, out_h, out_w, topk_idx, topk_logit,
+               boxes, dir_label);
+}
+
+// Small grids (every CTA of the call resident at once, chunk <= kCap): both passes in
+// one kernel.  A CTA keeps its chunk's keys in shared memory, adds its histogram, and
+// meets the frame's other CTAs at a flag the last arriving one raises after computing
+// the threshold; then it appends its candidates and the last CTA to arrive ranks and
+// decodes -- one launch and no key round trip through HBM (batch 1: 27 CTAs).
+__global__ void __launch_bounds__(kThreads) topk_fused(
+    const pmx_anchor_desc d, const float* __restrict__ heads, int c_stride, int cls_off, int box_off, int dir_off,
+    int out_h, int out_w, int* hist, int* arrive, int* flag, uint32_t* thresh, unsigned long long* cand, int* cnt,
+    int32_t* topk_idx, float* topk_logit, float* boxes, int32_t* dir_label, int chunk) {
+  pdl_begin();
+  __shared__ unsigned long long s[kCap];
+  __shared__ int h[kBins];
+  const int b = blockIdx.y;
+  const int n_anchors = d.n_anchors;
+  const int64_t ncand = (int64_t)out_h * out_w * n_anchors;
+  for (int t = threadIdx.x; t < kBins; t += blockDim.x) h[t] = 0;
+  __syncthreads();
+  const int64_t base = (int64_t)blockIdx.x * chunk;
+  for (int t = threadIdx.x; t < chunk; t += blockDim.x) {
+    const int64_t i = base + t;
+    unsigned long long key = 0ull;
+    if (i < ncand) {
+      key = cand_key(heads, c_stride, cls_off, n_anchors, ncand, b, i);
+      atomicAdd(&h[(int)(key >> 53)], 1);
+    }
+    s[t] = key;
+  }
+  __syncthreads();
+  int* hb = hist + (int64_t)b * kBins;
+  for (int t = threadIdx.x; t < kBins; t += blockDim.x)
+    if (h[t]) atomicAdd(hb + t, h[t]);
+  if (last_arrival(arrive + b, gridDim.x)) {
+    hist_threshold(hb, d.k, thresh + b);
+    __syncthreads();
+    if (threadIdx.x == 0) asm volatile("st.release.gpu.b32 [%0], %1;" ::"l"(flag + b), "r"(1) : "memory");
+  } else {
+    if (threadIdx.x == 0) {
+      int f = 0;
+      do {
+        asm volatile("ld.acquire.gpu.b32 %0, [%1];" : "=r"(f) : "l"(flag + b) : "memory");
+        if (!f) __nanosleep(64);
+      } while (!f);
+    }
+    __syncthreads();
+  }
+  const uint32_t T = __ldcg(thresh + b);
+  const int lane = threadIdx.x & 31;
+  unsigned long long* cb = cand + (int64_t)b * ncand;
+  for (int t0 = 0; t0 < chunk; t0 += blockDim.x) {
+    const int t = t0 + threadIdx.x;
+    const unsigned long long key = t < chunk ? s[t] : 0ull;
+    const bool keep = key != 0ull && (uint32_t)(key >> 32) >= T;
+    const unsigned m = __ballot_sync(0xffffffffu, keep);
+    if (!m) continue;
+    int slot = 0;
+    if (lane == 0) slot = atomicAdd(cnt + b, __popc(m));
+    slot = __shfl_sync(0xffffffffu, slot, 0);
+    if (keep) cb[slot + __popc(m & ((1u << lane) - 1u))] = key;
+  }
+  if (!last_arrival(arrive + gridDim.y + b, gridDim.x)) return;
+  finish_frame(d, b, __ldcg(cnt + b), cb, s, heads, c_stride, box_off, dir_off, out_h, out_w, topk_idx, topk_logit,
+               boxes, dir_label);
+}
+
+// per-call zeroing of the counters as a kernel (keeps the programmatic launch chain,
+// which a memset node would break)
+__global__ void zero_ws_kernel(int* p, int n) {
+  pdl_begin();
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) p[i] = 0;
+}
+
 __global__ void pack_records_kernel(int n, const int32_t* __restrict__ idx, const float* __restrict__ logit,
                                     const float* __restrict__ boxes, const int32_t* __restrict__ dir, float* rec) {
   pdl_begin();
@@ -280,6 +372,7 @@ struct DecodeWs {
   int* hist;     // [B, kBins]
   int* cnt;      // [B]
   int* arrive;   // [2, B]
+  int* flag;     // [B] fused path: threshold ready
   uint32_t* thresh;
   size_t zero_bytes;  // hist .. arrive are contiguous and zeroed per call
   size_t bytes;
@@ -300,6 +393,7 @@ DecodeWs carve_ws(void* base, int32_t batch, int64_t ncand) {
   w.hist = (int*)take(sizeof(int) * batch * kBins);
   w.cnt = (int*)take(sizeof(int) * batch);
   w.arrive = (int*)take(sizeof(int) * 2 * batch);
+  w.flag = (int*)take(sizeof(int) * batch);
   w.zero_bytes = off - z0;
   w.thresh = (uint32_t*)take(sizeof(uint32_t) * batch);
   w.bytes = off;
@@ -335,9 +429,17 @@ pmx_status pmx_decode_topk(const pmx_anchor_desc* desc, int32_t batch, int32_t o
   PMX_REQUIRE(ncand < 0x7fffffff, "too many anchors");
   DecodeWs w = carve_ws(ws, batch, ncand);
   PMX_REQUIRE(ws && ws_bytes >= w.bytes, "decode workspace too small");
-  PMX_CUDA(cudaMemsetAsync(w.hist, 0, w.zero_bytes, stream));
   const int chunk = decode_chunk(batch);
   const int nch = (int)ceil_div(ncand, chunk);
+  const int nz = (int)(w.zero_bytes / sizeof(int));
+  PMX_CUDA(launch_pdl(zero_ws_kernel, dim3((unsigned)(nz < 65536 ? ceil_div(nz, 1024) : 64)), dim3(1024), 0, stream,
+                      w.hist, nz));
+  if (chunk <= kCap && (int64_t)nch * batch <= num_sms() && fused_enabled()) {
+    PMX_CUDA(launch_pdl(topk_fused, dim3(nch, batch), dim3(kThreads), 0, stream, d, heads, head_c_stride, cls_off,
+                        box_off, dir_off, out_h, out_w, w.hist, w.arrive, w.flag, w.thresh, w.cand, w.cnt, topk_idx,
+                        topk_logit, boxes, dir_label, chunk));
+    return check_launch("pmx_decode_topk");
+  }
   PMX_CUDA(launch_pdl(topk_hist, dim3(nch, batch), dim3(kThreads), 0, stream, heads, head_c_stride, cls_off,
                       d.n_anchors, ncand, d.k, w.hist, w.arrive, w.thresh, chunk, w.keys));
   PMX_CUDA(launch_pdl(topk_select, dim3(nch, batch), dim3(kThreads), 0, stream, d, heads, head_c_stride, cls_off,

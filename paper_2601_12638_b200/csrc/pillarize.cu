@@ -1,16 +1,20 @@
 // K3 pillarize (pm/scenes.py:155-193 + KITTI cap) and feature materialisation.
 //
-// Deterministic with atomics:
+// Deterministic with atomics; six kernels per call (five at batch <= 8):
+//  0 init     the per-call workspace counters and cell arrays
 //  1 bin      per point: cell (IEEE f32 divide, trunc, clamp), atomicMin(first[cell], i),
 //             atomicAdd(cnt[cell], 1)                           -- coalesced float4 loads
-//  2 flags    per point block: #points that are the first of their cell
-//  3 thresh   per frame: T = index of the P_max-th first-seen point (cap rule), or INT_MAX
+//  2 hist     per cell block: occupied cells counted into the 1024-point block of their
+//             first point
+//  3 thresh   per frame: T = index of the P_max-th first-seen point (cap rule) or
+//             INT_MAX -- at small batches done by the hist kernel's last CTA per frame
 //  4 emit     per cell block (single pass, decoupled look-back): kept = cnt>0 &&
 //             first<=T; pillar id in ascending flat order, coords, segment offsets,
 //             n_pillars
 //  5 slot     per point: atomic slot in its pillar's CSR segment (arbitrary order)
-//  6 select   warp per pillar: the first M points of the segment by scene index
-//             (shuffle ranks; a warp threshold search when the cell holds > 32 points)
+//  6 select   thread per pillar: the first M points of the segment by scene index
+//             (rank counts; the pillar's warp runs a threshold search when a cell holds
+//             more than 32 points)
 #include <climits>
 
 #include "pmx_common.cuh"
@@ -34,10 +38,9 @@ struct PillarWs {
   int32_t* segoff;  // [B*Pcap]
   int32_t* fill;    // [B*Pcap]
   int32_t* csr;     // [B*Nmax]
-  int32_t* ovf_n;   // [1] pillars with > 32 points (rare: dense clusters)
-  int2* ovf;        // [B*Pcap] (frame, pillar) of those
   unsigned long long* look;  // [B*CB] single-pass emit: per-block (flag, kept, points) look-back words
   int32_t* ticket;           // [B] single-pass emit: block order per frame
+  int32_t* hdone;            // [B] firsthist (small batches): CTAs done per frame
 };
 
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -64,10 +67,9 @@ size_t carve(const pmx_grid* g, int32_t B, int64_t nmax, int32_t pcap, void* bas
   w.segoff = (int32_t*)take(sizeof(int32_t) * B * pcap);
   w.fill = (int32_t*)take(sizeof(int32_t) * B * pcap);
   w.csr = (int32_t*)take(sizeof(int32_t) * B * (nmax > 0 ? nmax : 1));
-  w.ovf_n = (int32_t*)take(sizeof(int32_t));
-  w.ovf = (int2*)take(sizeof(int2) * B * pcap);
   w.look = (unsigned long long*)take(sizeof(unsigned long long) * B * cb);
   w.ticket = (int32_t*)take(sizeof(int32_t) * B);
+  w.hdone = (int32_t*)take(sizeof(int32_t) * B);
   if (ws) *ws = w;
   return off;
 }
@@ -92,9 +94,8 @@ __global__ void init_ws_kernel(PillarWs w, int64_t n_cells, int64_t n_fill, int6
   }
   for (int64_t i = tid; i < n_fill; i += nt) w.fill[i] = 0;
   for (int64_t i = tid; i < n_look; i += nt) w.look[i] = 0ull;
-  for (int64_t i = tid; i < batch; i += nt) w.ticket[i] = 0;
+  for (int64_t i = tid; i < batch; i += nt) w.ticket[i] = 0, w.hdone[i] = 0;
   for (int64_t i = tid; i < n_ptblk; i += nt) w.ptblk[i] = 0;
-  if (tid == 0) *w.ovf_n = 0;
 }
 
 __device__ __forceinline__ int bin_cell(float x, float y, const pmx_grid g) {
@@ -145,7 +146,11 @@ __global__ void __launch_bounds__(kPtBlock) flag_kernel(const int64_t* __restric
 // 1024-point block holding its first point (shared-memory histogram per CTA, then one
 // atomic per non-empty bin) -- a coalesced pass over first[] instead of a random
 // first[cell[i]] read per point.  ptblk is zeroed by init_ws_kernel.
-__global__ void __launch_bounds__(1024) firsthist_kernel(const pmx_grid g, PillarWs w, int nb) {
+__device__ void cap_threshold(const int64_t* __restrict__ offs, int64_t nmax, const pmx_grid& g, PillarWs& w, int nb,
+                              int b);
+
+__global__ void __launch_bounds__(1024) firsthist_kernel(const int64_t* __restrict__ offs, int64_t nmax,
+                                                        const pmx_grid g, PillarWs w, int nb, int fold) {
   pdl_begin();
   extern __shared__ int h[];  // [nb]
   const int b = blockIdx.y;
@@ -167,6 +172,19 @@ __global__ void __launch_bounds__(1024) firsthist_kernel(const pmx_grid g, Pilla
   __syncthreads();
   for (int t = threadIdx.x; t < nb; t += blockDim.x)
     if (h[t]) atomicAdd(w.ptblk + (int64_t)b * nb + t, h[t]);
+  if (!fold) return;
+  // small batches: the frame's last CTA to arrive computes the cap threshold (one launch
+  // less on the latency path; the block barrier + one acq_rel add per CTA order the counts)
+  __shared__ int s_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int old;
+    asm volatile("atom.add.acq_rel.gpu.s32 %0, [%1], 1;" : "=r"(old) : "l"(w.hdone + b) : "memory");
+    s_last = old == (int)gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  cap_threshold(offs, nmax, g, w, nb, b);
 }
 
 // inclusive block scan of one int per thread (blockDim.x == 1024)
@@ -218,12 +236,12 @@ __device__ unsigned long long block_incl_scan2(unsigned long long v, unsigned lo
   return v;
 }
 
-__global__ void __launch_bounds__(1024) thresh_kernel(const int64_t* __restrict__ offs, int64_t nmax,
-                                                      const pmx_grid g, PillarWs w, int nb) {
-  pdl_begin();
+// cap rule: T = index of the P_max-th first-seen point of frame b, or INT_MAX when the
+// cap does not bind (block counts of first-seen points, then one block's flags)
+__device__ void cap_threshold(const int64_t* __restrict__ offs, int64_t nmax, const pmx_grid& g, PillarWs& w, int nb,
+                              int b) {
   __shared__ int sh[32];
   __shared__ int s_blk, s_need;
-  const int b = blockIdx.x;
   const int64_t n = offs[b + 1] - offs[b];
   const int64_t hw = (int64_t)g.grid_h * g.grid_w;
   if (g.max_pillars <= 0) {
@@ -238,13 +256,13 @@ __global__ void __launch_bounds__(1024) thresh_kernel(const int64_t* __restrict_
   const int per = (nb + (int)blockDim.x - 1) / (int)blockDim.x;
   const int k0 = threadIdx.x * per;
   int run = 0;
-  for (int k = k0; k < k0 + per && k < nb; ++k) run += w.ptblk[b * nb + k];
+  for (int k = k0; k < k0 + per && k < nb; ++k) run += __ldcg(w.ptblk + b * nb + k);
   const int incl = block_incl_scan(run, sh);  // (synchronises the s_blk reset too)
   const int excl = incl - run;
   if (excl < g.max_pillars + 1 && incl >= g.max_pillars + 1) {  // exactly one thread
     int cum = excl;
     for (int k = k0; k < k0 + per && k < nb; ++k) {
-      const int c = w.ptblk[b * nb + k];
+      const int c = __ldcg(w.ptblk + b * nb + k);
       if (cum + c >= g.max_pillars + 1) {
         s_blk = k;
         s_need = g.max_pillars - cum;  // the need-th first-seen point in this block is the last kept
@@ -265,9 +283,15 @@ __global__ void __launch_bounds__(1024) thresh_kernel(const int64_t* __restrict_
   }
   int64_t i = (int64_t)s_blk * kPtBlock + threadIdx.x;
   int flag = 0;
-  if (i < n) flag = w.first[b * hw + w.cell[b * nmax + i]] == (int)i;
+  if (i < n) flag = __ldcg(w.first + b * hw + w.cell[b * nmax + i]) == (int)i;
   int inc = block_incl_scan(flag, sh);
   if (flag && inc == s_need) w.thresh[b] = (int)i;
+}
+
+__global__ void __launch_bounds__(1024) thresh_kernel(const int64_t* __restrict__ offs, int64_t nmax,
+                                                      const pmx_grid g, PillarWs w, int nb) {
+  pdl_begin();
+  cap_threshold(offs, nmax, g, w, nb, blockIdx.x);
 }
 
 // Single pass of cellcount + cellscan + emit: every block reads its 4096 cells
@@ -380,45 +404,90 @@ __global__ void slot_kernel(const int64_t* __restrict__ offs, int64_t nmax, cons
   }
 }
 
+// One pillar whose segment holds c > 32 points, warp-cooperatively: the first M points
+// by scene index via a threshold search (t = the M-th smallest index; indices are
+// distinct), compaction of the indices <= t, then a shuffle rank sort.  buf: 32 ints
+// of this warp's shared memory.  All 32 lanes call it.
+__device__ void warp_select_long(int64_t n_frame, int64_t nmax, int M, const PillarWs& w, int b, int64_t q,
+                                 int32_t* dst, int* buf) {
+  const int lane = threadIdx.x & 31;
+  const int c = w.fill[q];
+  const int* seg = w.csr + b * nmax + w.segoff[q];
+  const int kept = c < M ? c : M;
+  if (lane < M && lane >= kept) dst[lane] = -1;
+  int lo = 0, hi = (int)n_frame - 1;
+  while (lo < hi) {
+    const int mid = lo + ((hi - lo) >> 1);
+    int cntle = 0;
+    for (int k = lane; k < c; k += 32) cntle += seg[k] <= mid;
+    cntle = __reduce_add_sync(0xffffffffu, cntle);
+    if (cntle >= M) hi = mid; else lo = mid + 1;
+  }
+  const int t = lo;
+  int off = 0;
+  for (int k0 = 0; k0 < c; k0 += 32) {
+    const int k = k0 + lane;
+    const int val = k < c ? seg[k] : INT_MAX;
+    const bool sel = k < c && val <= t;
+    const unsigned m = __ballot_sync(0xffffffffu, sel);
+    if (sel) buf[off + __popc(m & ((1u << lane) - 1u))] = val;
+    off += __popc(m);
+  }
+  __syncwarp();
+  const int v = lane < M ? buf[lane] : INT_MAX;
+  int rank = 0;
+  for (int j = 0; j < 32; ++j) rank += __shfl_sync(0xffffffffu, v, j) < v;
+  if (v != INT_MAX && rank < M) dst[rank] = v;
+  __syncwarp();
+}
+
 // Thread per pillar: a KITTI pillar holds 1-3 points, so the first-M-by-scene-index
-// selection is a tiny rank count over the segment.  Segments longer than 32 points
-// go to an overflow list handled warp-wide by select_kernel below.
-__global__ void __launch_bounds__(256) select_small_kernel(int64_t nmax, const pmx_grid g, PillarWs w, int32_t pcap,
+// selection is a tiny rank count over the segment; a pillar with more than 32 points
+// (dense clusters) is handled by its whole warp afterwards (warp_select_long).
+__global__ void __launch_bounds__(256) select_small_kernel(const int64_t* __restrict__ offs, int64_t nmax,
+                                                           const pmx_grid g, PillarWs w, int32_t pcap,
                                                            const int32_t* __restrict__ n_pillars, int32_t* pt_idx) {
   pdl_begin();
+  __shared__ int buf[8][32];
   const int b = blockIdx.y;
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= n_pillars[b]) return;
+  const int P = n_pillars[b];
   const int M = g.max_points;
   const int64_t q = (int64_t)b * pcap + p;
-  const int c = w.fill[q];
-  if (c > 32) {
-    w.ovf[atomicAdd(w.ovf_n, 1)] = make_int2(b, p);
-    return;
+  const int c = p < P ? w.fill[q] : 0;
+  if (p < P && c <= 32) {
+    const int* seg = w.csr + b * nmax + w.segoff[q];
+    int32_t* dst = pt_idx + q * M;
+    if ((M & 3) == 0) {
+      for (int s = 0; s < M; s += 4) *reinterpret_cast<int4*>(dst + s) = make_int4(-1, -1, -1, -1);
+    } else {
+      for (int s = 0; s < M; ++s) dst[s] = -1;
+    }
+    for (int i = 0; i < c; ++i) {
+      const int v = seg[i];
+      int r = 0;
+      for (int j = 0; j < c; ++j) r += seg[j] < v;
+      if (r < M) dst[r] = v;
+    }
   }
-  const int* seg = w.csr + b * nmax + w.segoff[q];
-  int32_t* dst = pt_idx + q * M;
-  if ((M & 3) == 0) {
-    for (int s = 0; s < M; s += 4) *reinterpret_cast<int4*>(dst + s) = make_int4(-1, -1, -1, -1);
-  } else {
-    for (int s = 0; s < M; ++s) dst[s] = -1;
-  }
-  for (int i = 0; i < c; ++i) {
-    const int v = seg[i];
-    int r = 0;
-    for (int j = 0; j < c; ++j) r += seg[j] < v;
-    if (r < M) dst[r] = v;
+  unsigned long_m = __ballot_sync(0xffffffffu, p < P && c > 32);
+  while (long_m) {
+    const int l = __ffs(long_m) - 1;
+    long_m &= long_m - 1;
+    const int64_t ql = __shfl_sync(0xffffffffu, q, l);
+    warp_select_long(offs[b + 1] - offs[b], nmax, M, w, b, ql, pt_idx + ql * M, buf[threadIdx.x >> 5]);
   }
 }
 
 // M == 32 variant: lane = pillar builds its 128-byte row in shared memory (16-byte
 // chunks XOR-swizzled by lane % 8: conflict-free), then the warp writes 4 whole rows
 // per store instruction (a thread-per-row store scatters over 32 lines).
-__global__ void __launch_bounds__(256) select_small32_kernel(int64_t nmax, const pmx_grid g, PillarWs w,
-                                                             int32_t pcap, const int32_t* __restrict__ n_pillars,
-                                                             int32_t* pt_idx) {
+__global__ void __launch_bounds__(256) select_small32_kernel(const int64_t* __restrict__ offs, int64_t nmax,
+                                                             const pmx_grid g, PillarWs w, int32_t pcap,
+                                                             const int32_t* __restrict__ n_pillars, int32_t* pt_idx) {
   pdl_begin();
   __shared__ int4 rows[8][32][8];  // [warp][pillar][16-byte chunk]
+  __shared__ int buf[8][32];
   const int b = blockIdx.y;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int p0 = (blockIdx.x * 8 + wid) * 32;
@@ -428,10 +497,8 @@ __global__ void __launch_bounds__(256) select_small32_kernel(int64_t nmax, const
   bool mine = p < P;
   const int64_t q = (int64_t)b * pcap + p;
   const int c = mine ? w.fill[q] : 0;
-  if (mine && c > 32) {  // dense cluster: the warp-per-pillar kernel writes this row
-    w.ovf[atomicAdd(w.ovf_n, 1)] = make_int2(b, p);
-    mine = false;
-  }
+  const bool longp = mine && c > 32;  // dense cluster: the warp handles it below
+  if (longp) mine = false;
   const int sw = lane & 7;
 #pragma unroll
   for (int k = 0; k < 8; ++k) rows[wid][lane][k ^ sw] = make_int4(-1, -1, -1, -1);
@@ -453,58 +520,12 @@ __global__ void __launch_bounds__(256) select_small32_kernel(int64_t nmax, const
     if ((keep >> r) & 1)
       reinterpret_cast<int4*>(pt_idx + ((int64_t)b * pcap + p0 + r) * 32)[k] = rows[wid][r][k ^ (r & 7)];
   }
-}
-
-__global__ void __launch_bounds__(256) select_kernel(const int64_t* __restrict__ offs, int64_t nmax,
-                                                     const pmx_grid g, PillarWs w, int32_t pcap,
-                                                     const int32_t* __restrict__ n_pillars, int32_t* pt_idx) {
-  pdl_begin();
-  __shared__ int buf[8][32];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int n_items = *w.ovf_n;
-  for (int item = blockIdx.x * 8 + wid; item < n_items; item += gridDim.x * 8) {
-  const int b = w.ovf[item].x, p = w.ovf[item].y;
-  const int M = g.max_points;
-  const int64_t q = (int64_t)b * pcap + p;
-  const int c = w.fill[q];
-  const int* seg = w.csr + b * nmax + w.segoff[q];
-  int32_t* dst = pt_idx + q * M;
-  const int kept = c < M ? c : M;
-  if (lane < M && lane >= kept) dst[lane] = -1;
-  int v = INT_MAX;
-  if (c <= 32) {
-    if (lane < c) v = seg[lane];
-  } else {
-    // threshold search: t = the M-th smallest index (indices are distinct)
-    const int n = (int)(offs[b + 1] - offs[b]);
-    int lo = 0, hi = n - 1;
-    while (lo < hi) {
-      int mid = lo + ((hi - lo) >> 1);
-      int cntle = 0;
-      for (int k = lane; k < c; k += 32) cntle += seg[k] <= mid;
-      cntle = __reduce_add_sync(0xffffffffu, cntle);
-      if (cntle >= M) hi = mid; else lo = mid + 1;
-    }
-    const int t = lo;
-    int off = 0;
-    for (int k0 = 0; k0 < c; k0 += 32) {
-      int k = k0 + lane;
-      int val = k < c ? seg[k] : INT_MAX;
-      bool sel = k < c && val <= t;
-      unsigned m = __ballot_sync(0xffffffffu, sel);
-      if (sel) buf[wid][off + __popc(m & ((1u << lane) - 1u))] = val;
-      off += __popc(m);
-    }
-    __syncwarp();
-    if (lane < M) v = buf[wid][lane];
-  }
-  int rank = 0;
-  for (int j = 0; j < 32; ++j) {
-    int u = __shfl_sync(0xffffffffu, v, j);
-    rank += u < v;
-  }
-  if (v != INT_MAX && rank < M) dst[rank] = v;
-  __syncwarp();
+  unsigned long_m = __ballot_sync(0xffffffffu, longp);
+  while (long_m) {
+    const int l = __ffs(long_m) - 1;
+    long_m &= long_m - 1;
+    const int64_t ql = (int64_t)b * pcap + p0 + l;
+    warp_select_long(offs[b + 1] - offs[b], nmax, 32, w, b, ql, pt_idx + ql * 32, buf[wid]);
   }
 }
 
@@ -624,23 +645,27 @@ pmx_status pmx_pillarize(const float* points, const int64_t* frame_offsets, int3
                       frame_offsets, nmax, g, w));
   if (nb <= 16384) {  // the per-frame bins fit in shared memory
     PMX_CUDA(cudaFuncSetAttribute(firsthist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, nb * 4));
-    PMX_CUDA(launch_pdl(firsthist_kernel, dim3(cb, batch), dim3(1024), (size_t)nb * 4, stream, g, w, nb));
+    // small batches: its last CTA per frame also computes the cap threshold (measured:
+    // batch 1 one launch less on the latency path; batch 32 faster as a separate kernel)
+    const int fold = batch <= 8 ? 1 : 0;
+    PMX_CUDA(launch_pdl(firsthist_kernel, dim3(cb, batch), dim3(1024), (size_t)nb * 4, stream, frame_offsets, nmax,
+                        g, w, nb, fold));
+    if (!fold)
+      PMX_CUDA(launch_pdl(thresh_kernel, dim3(batch), dim3(1024), 0, stream, frame_offsets, nmax, g, w, nb));
   } else {
     PMX_CUDA(launch_pdl(flag_kernel, dim3(nb, batch), dim3(kPtBlock), 0, stream, frame_offsets, nmax, g, w, nb));
+    PMX_CUDA(launch_pdl(thresh_kernel, dim3(batch), dim3(1024), 0, stream, frame_offsets, nmax, g, w, nb));
   }
-  PMX_CUDA(launch_pdl(thresh_kernel, dim3(batch), dim3(1024), 0, stream, frame_offsets, nmax, g, w, nb));
   PMX_CUDA(launch_pdl(emit_fused_kernel, dim3(cb, batch), dim3(1024), 0, stream, g, w, cb, pcap, coords, counts,
                       n_pillars));
   PMX_CUDA(launch_pdl(slot_kernel, dim3(ptx, batch), dim3(256), 0, stream, frame_offsets, nmax, g, w, pcap));
+  // (pillars with more than 32 points: their warp, inside the same kernels)
   if (g.max_points == 32)
-    PMX_CUDA(launch_pdl(select_small32_kernel, dim3((int)ceil_div(pcap, 256), batch), dim3(256), 0, stream, nmax, g,
-                        w, pcap, n_pillars, pt_idx));
+    PMX_CUDA(launch_pdl(select_small32_kernel, dim3((int)ceil_div(pcap, 256), batch), dim3(256), 0, stream,
+                        frame_offsets, nmax, g, w, pcap, n_pillars, pt_idx));
   else
-    PMX_CUDA(launch_pdl(select_small_kernel, dim3((int)ceil_div(pcap, 256), batch), dim3(256), 0, stream, nmax, g,
-                        w, pcap, n_pillars, pt_idx));
-  // overflow pillars (> 32 points): one warp each, grid-stride over the device-side list
-  PMX_CUDA(launch_pdl(select_kernel, dim3(num_sms()), dim3(256), 0, stream, frame_offsets, nmax, g, w, pcap, n_pillars,
-                      pt_idx));
+    PMX_CUDA(launch_pdl(select_small_kernel, dim3((int)ceil_div(pcap, 256), batch), dim3(256), 0, stream,
+                        frame_offsets, nmax, g, w, pcap, n_pillars, pt_idx));
   return check_launch("pmx_pillarize");
 }
 
