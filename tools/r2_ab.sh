@@ -4,7 +4,7 @@ export PMX_NO_BUILD=1
 mkdir -p gpurun_out
 O=gpurun_out/r2_ab.log
 : > $O
-timeout 1200 python -m pytest tests/test_gpu_kernels.py tests/test_gpu_forward.py tests/test_gpu_decode_nms.py tests/test_gpu_fullsize_parity.py -x -q 2>&1 | tail -2 >> $O
+timeout 1200 python -m pytest tests/test_gpu_kernels.py tests/test_gpu_forward.py tests/test_gpu_gather.py -x -q 2>&1 | tail -2 >> $O
 for lib in libpmx.so libpmx_prev.so libpmx.so libpmx_prev.so; do
   PMX_LIB=paper_2601_12638_b200/$lib timeout 400 python bench.py --steps 20 --warmup 5 --no-cpu-baseline > gpurun_out/r2_ab.json 2>gpurun_out/r2_ab.err
   echo "== $lib rc=$?" >> $O
