@@ -48,12 +48,15 @@ def build(force: bool = False, verbose: bool = False, ptxas_verbose: bool = Fals
     if out == LIB and not force and up_to_date():
         return LIB
     # PMX_BUILD_OUT: a variant library (trace / ablation builds) with its own object dir
-    bdir = BUILD if out == LIB else BUILD.parent / ("pmx_" + out.stem)
+    bdir = BUILD if out == LIB else BUILD.parent / ("pmx_" + out.parent.name + "_" + out.stem)
+    out.parent.mkdir(parents=True, exist_ok=True)
     bdir.mkdir(parents=True, exist_ok=True)
     nvcc = _nvcc()
     extra = ["-Xptxas", "-v"] if ptxas_verbose else []
     if os.environ.get("PMX_TRACE_BUILD") == "1":  # per-role conv timeline (tools/op_profile.py --trace)
         extra += ["-DPMX_CONV_TRACE"]
+    if os.environ.get("PMX_DECODE_TRACE") == "1":  # per-phase decode timeline (experiments only)
+        extra += ["-DPMX_DECODE_TRACE"]
     if os.environ.get("PMX_ABLATE"):  # epilogue ablation builds (experiments only)
         extra += [f"-DPMX_ABLATE={int(os.environ['PMX_ABLATE'])}"]
 

@@ -792,7 +792,7 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
   // overlap the previous layer's tail; the activations are read (and the outputs
   // written) only after griddepcontrol.wait.  The next layer may start launching now.
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  if (p.mode == MODE_HALO && warp == kProdWarp && lane == 0) {
+  if (p.bres_bytes && warp == kProdWarp && lane == 0) {
     // PAIR: each CTA holds its half of the N tile's weights; both halves complete on the
     // leader's barrier
     if (!PAIR || rank == 0) mbar_expect_tx(bfull, (PAIR ? 2u : 1u) * p.bres_bytes);
@@ -884,10 +884,12 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
           m0 = mt * 128;
         }
         for (int kb = 0; kb < nk; ++kb, ++it) {
+          PMX_TRACE(0, it);
           mbar_wait(empty(s), ph ^ 1);
           // PAIR: the leader's full barrier counts the bytes of both CTAs' loads
           if (!PAIR || rank == 0) mbar_expect_tx(full(s), (PAIR ? 2u : 1u) * (p.a_bytes + p.b_bytes));
           const int tap = kb / p.cblocks, cb = kb % p.cblocks;
+          const bool load_b = p.b_bytes != 0;  // 0: the GEMM mode's weights are resident
           const int c0 = cb * p.kc;
           int ac = c0;  // A channel coordinate
           if (p.seg_n) {
@@ -922,8 +924,9 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
           } else {
             tma_load_2d(adst, &maps.a[0], ac, m0, full(s));
           }
-          tma_load_2d(bdst, &maps.b, tap * (p.cblocks * p.kc) + c0, n0, full(s));
+          if (load_b) tma_load_2d(bdst, &maps.b, tap * (p.cblocks * p.kc) + c0, n0, full(s));
           }
+          PMX_TRACE(1, it);
           if (++s == (uint32_t)p.stages) s = 0, ph ^= 1;
         }
       }
@@ -1051,6 +1054,13 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
       constexpr int ksteps = KCB / 32;  // 32 bytes of K per instruction
       const uint32_t hi = (uint32_t)(sdesc(0, p.sbo, p.layout) >> 32), lo0 = (uint32_t)sdesc(0, p.sbo, p.layout);
       uint32_t s = 0, ph = 0, acc = 0, aph = 0;
+      // GEMM with resident weights (b_bytes == 0): K-block kb of this CTA's N tile sits
+      // at bres + kb * bblk_bytes for the whole kernel
+      const bool bres_on = p.b_bytes == 0;
+      if (bres_on) {
+        mbar_wait(bfull, 0);
+        tc_fence_after();
+      }
       // PAIR: only the leader issues (M = 256 over both CTAs' A, N over both B halves)
       for (int t = tstart; t < total && (!PAIR || rank == 0); t += tstride, ++i) {
         if (lane == 0) PMX_TRACE(9, i);
@@ -1063,7 +1073,8 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
           tc_fence_after();
           if (elect_one()) {
             if (kb == 0) PMX_TRACE(3, i);
-            const uint32_t alo = lo0 + ((a_smem + s * p.a_bytes) >> 4), blo = lo0 + ((b_smem + s * p.b_bytes) >> 4);
+            const uint32_t alo = lo0 + ((a_smem + s * p.a_bytes) >> 4);
+            const uint32_t blo = lo0 + ((bres_on ? bres + (uint32_t)kb * p.bblk_bytes : b_smem + s * p.b_bytes) >> 4);
             uint32_t dk = d;
             bool first = kb == 0;
             if constexpr (DT == PMX_F32X2) {
@@ -1446,7 +1457,19 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
             uint32_t v[16];
             acc_ld16<DT>(trow + 16 * (c_begin + k), p.lo_col, v);
             if (!valid || !live) continue;
+#if defined(PMX_ABLATE) && PMX_ABLATE == 1
+            continue;
+#endif
             const int cobase = cob0 + 16 * k;
+#if defined(PMX_ABLATE) && PMX_ABLATE == 3
+            {
+              const uint32_t sa3 = wstage + (uint32_t)lane * 64u + (((uint32_t)k ^ (((uint32_t)lane >> 1) & 3u)) << 4);
+              asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(sa3), "r"(v[0]), "r"(v[5]), "r"(v[10]),
+                           "r"(v[15])
+                           : "memory");
+              continue;
+            }
+#endif
             float y[16];
             const float4* b4p = reinterpret_cast<const float4*>(s_bias + cobase);
             const float4* a4p = reinterpret_cast<const float4*>(s_alpha + cobase);
@@ -1497,6 +1520,9 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
                            : "=r"(w.x), "=r"(w.y), "=r"(w.z), "=r"(w.w)
                            : "r"(la)
                            : "memory");
+#if defined(PMX_ABLATE) && PMX_ABLATE == 2
+              if ((w.x & w.y & w.z & w.w) == 0x7f7f7f7fu)
+#endif
               if (rp != 0xffffffffu) *reinterpret_cast<uint4*>(obase + (size_t)rp * ocs + 16 * cc) = w;
             }
           }
@@ -1670,6 +1696,13 @@ bool halo_pair_enabled() {  // PMX_HALO_PAIR=1: 2-CTA pairs in the halo mode (ex
   return on;
 }
 
+int gemm_res_mode() {  // PMX_GEMM_RES=1: resident weights in the GEMM mode (experiment, measured neutral: off)
+  static const int v = [] {
+    const char* e = getenv("PMX_GEMM_RES");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
 bool small_halo_enabled() {  // PMX_SMALL_HALO=0: no halo for N-split / 256-byte layers (A/B runs)
   static const bool on = [] {
     const char* e = getenv("PMX_SMALL_HALO");
@@ -1915,6 +1948,24 @@ Plan plan_for(const pmx_conv_desc& d, bool gather = false, bool want_stage = fal
       p.bres_bytes = bres_total;
     } else {
       p.hswz = 0;
+    }
+  }
+  // GEMM (1x1 convs, deconvs): one N tile's weights for all K resident in shared memory
+  // (CTA b keeps N tile b % n_tiles, grid a multiple of n_tiles) and the ring carries
+  // only A: the same shared memory then holds about twice the A bytes in flight (the
+  // deconvs' producer otherwise waits on stages their weight re-loads keep occupied)
+  if (p.mode == MODE_GEMM && !x3 && !heads && gemm_res_mode() != 0 && g_conv_backend_mode != 2) {
+    const uint32_t bblk = (uint32_t)bn * kc_bytes;
+    const uint32_t bslice = bblk * (uint32_t)p.cblocks;
+    const uint32_t budget = 227u * 1024u - 2048u - 8u * (uint32_t)((d.out_c + 3) & ~3) - estage_bytes;
+    const int gmax = (num_sms() / p.n_tiles) * p.n_tiles;
+    const int sa = bslice < budget ? (int)((budget - bslice) / p.a_bytes) : 0;
+    if (gmax >= 1 && sa >= 2 && (sa >= 2 * p.cblocks || sa >= 4 || gemm_res_mode() == 2)) {
+      p.b_bytes = 0;
+      p.bblk_bytes = bblk;
+      p.bres_bytes = bslice;
+      p.stages = sa > 16 ? 16 : sa;
+      pl.grid_x = (int)(tiles < gmax ? tiles : gmax);
     }
   }
   p.tw_shift = p.tw > 0 ? __builtin_ctz((unsigned)p.tw) : 0;

@@ -197,6 +197,32 @@ __device__ void finish_frame(const pmx_anchor_desc& d, int b, int n, const unsig
   __shared__ int sh_hist[256];
   __shared__ int sh_n, sh_sel[2];
   const int k = d.k;
+  if (n <= (int)blockDim.x && k <= kCap / 2) {
+    // few candidates (batch-1 frames: ~200): rank sort -- each key's rank is the number
+    // of larger keys (keys are unique), one pass over the list in shared memory instead
+    // of a bitonic network of log2(n)^2 / 2 barrier-separated stages
+    unsigned long long* out = s + kCap / 2;
+    const int t = threadIdx.x;
+    const unsigned long long key = t < n ? __ldcg(cb + t) : 0ull;
+    if (t < n) s[t] = key;
+    for (int r = n + t; r < k; r += blockDim.x) out[r] = 0ull;  // fewer than k candidates: empty ranks
+    __syncthreads();
+    if (t < n) {
+      int rank = 0;
+      int j = 0;
+      for (; j + 1 < n; j += 2) {
+        const ulonglong2 kk2 = *reinterpret_cast<const ulonglong2*>(s + j);
+        rank += (kk2.x > key) + (kk2.y > key);
+      }
+      if (j < n) rank += s[j] > key;
+      if (rank < k) out[rank] = key;
+    }
+    __syncthreads();
+    for (int r = threadIdx.x; r < k; r += blockDim.x)
+      decode_one(d, out[r], b, r, out_h, out_w, heads, c_stride, box_off, dir_off, topk_idx, topk_logit, boxes,
+                 dir_label);
+    return;
+  }
   if (n <= kCap) {
     int np = 2;
     while (np < n || np < k) np <<= 1;
@@ -253,7 +279,7 @@ __global__ void __launch_bounds__(kThreads) topk_select(
     int32_t* topk_idx, float* topk_logit, float* boxes, int32_t* dir_label, int chunk,
     const unsigned long long* __restrict__ keys) {
   pdl_begin();
-  __shared__ unsigned long long s[kCap];
+  __shared__ __align__(16) unsigned long long s[kCap];
   const int b = blockIdx.y;
   const int n_anchors = d.n_anchors;
   const int64_t ncand = (int64_t)out_h * out_w * n_anchors;
@@ -292,7 +318,14 @@ __global__ void __launch_bounds__(kThreads) topk_fused(
     int out_h, int out_w, int* hist, int* arrive, int* flag, uint32_t* thresh, unsigned long long* cand, int* cnt,
     int32_t* topk_idx, float* topk_logit, float* boxes, int32_t* dir_label, int chunk) {
   pdl_begin();
-  __shared__ unsigned long long s[kCap];
+#ifdef PMX_DECODE_TRACE
+  unsigned long long tt[6];
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt[0]));
+#define PMX_DT(i) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt[i]))
+#else
+#define PMX_DT(i)
+#endif
+  __shared__ __align__(16) unsigned long long s[kCap];
   __shared__ int h[kBins];
   const int b = blockIdx.y;
   const int n_anchors = d.n_anchors;
@@ -310,6 +343,7 @@ __global__ void __launch_bounds__(kThreads) topk_fused(
     s[t] = key;
   }
   __syncthreads();
+  PMX_DT(1);
   int* hb = hist + (int64_t)b * kBins;
   for (int t = threadIdx.x; t < kBins; t += blockDim.x)
     if (h[t]) atomicAdd(hb + t, h[t]);
@@ -327,6 +361,7 @@ __global__ void __launch_bounds__(kThreads) topk_fused(
     }
     __syncthreads();
   }
+  PMX_DT(2);
   const uint32_t T = __ldcg(thresh + b);
   const int lane = threadIdx.x & 31;
   unsigned long long* cb = cand + (int64_t)b * ncand;
@@ -341,9 +376,18 @@ __global__ void __launch_bounds__(kThreads) topk_fused(
     slot = __shfl_sync(0xffffffffu, slot, 0);
     if (keep) cb[slot + __popc(m & ((1u << lane) - 1u))] = key;
   }
+  PMX_DT(3);
   if (!last_arrival(arrive + gridDim.y + b, gridDim.x)) return;
+  PMX_DT(4);
   finish_frame(d, b, __ldcg(cnt + b), cb, s, heads, c_stride, box_off, dir_off, out_h, out_w, topk_idx, topk_logit,
                boxes, dir_label);
+#ifdef PMX_DECODE_TRACE
+  __syncthreads();
+  PMX_DT(5);
+  if (threadIdx.x == 0)
+    printf("decode trace b %d cta %d n %d: keys+hist %llu, thresh/flag %llu, append %llu, arrive %llu, finish %llu ns\n", b,
+           blockIdx.x, __ldcg(cnt + b), tt[1] - tt[0], tt[2] - tt[1], tt[3] - tt[2], tt[4] - tt[3], tt[5] - tt[4]);
+#endif
 }
 
 // per-call zeroing of the counters as a kernel (keeps the programmatic launch chain,

@@ -2,6 +2,7 @@
 golden vectors: quantize codes, fake_quant, fp16, observers, pillarize, top-k."""
 
 import json
+from pathlib import Path
 
 import numpy as np
 import pytest
@@ -183,6 +184,68 @@ def test_pillarize_out_of_range_points_clamp(pm):
     want = O.pillar_index(O.bin_points(pts[:, :2], spec.grid, spec.origin, spec.cell), spec.grid, 32, 5000)
     np.testing.assert_array_equal(got["coords"], want.coords)
     np.testing.assert_array_equal(got["pt_idx"], want.pt_idx)
+
+
+@pytest.mark.parametrize("sizes", [(3000, 0, 1, -4000, 2500),  # batch <= 8 (the persistent opt-in applies)
+                                   (3000, 0, 1, -4000, 2500, 7, 3100, 2900, 0, 2000)])  # batch 10
+def test_pillarize_batch_vs_oracle(pm, sizes):
+    """Frames of one batched pmx_pillarize call (ragged, empty, clustered (negative
+    size), capped) vs the oracle frame by frame."""
+    import ctypes
+
+    import torch
+
+    from paper_2601_12638_b200 import _native as N
+
+    lib = N.require_cuda()
+    cfg = pm.PointPillarsConfig.small(max_pillars=900)
+    spec = cfg.grid_spec()
+    frames = [(_kitti_case(pm, abs(n), 40 + i, cfg, n < 0) if n else np.zeros((0, 4), np.float32))
+              for i, n in enumerate(sizes)]
+    B = len(frames)
+    nmax = max(1, max(len(f) for f in frames))
+    h, w = spec.grid
+    pcap = spec.max_pillars
+    g = spec.to_c()
+    allp = np.concatenate(frames + [np.zeros((1, 4), np.float32)]).astype(np.float32)
+    offs = np.concatenate([[0], np.cumsum([len(f) for f in frames])]).astype(np.int64)
+    pts = torch.from_numpy(allp).cuda()
+    offs_d = torch.from_numpy(offs).cuda()
+    coords = torch.empty((B, pcap, 2), dtype=torch.int32, device="cuda")
+    counts = torch.empty((B, pcap), dtype=torch.int32, device="cuda")
+    pt_idx = torch.empty((B, pcap, spec.max_points), dtype=torch.int32, device="cuda")
+    n_pil = torch.zeros((B,), dtype=torch.int32, device="cuda")
+    ws_bytes = lib.pmx_pillarize_workspace(ctypes.byref(g), B, nmax)
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device="cuda")
+    for _ in range(2):  # twice: the workspace is re-initialised by every call
+        N.check(lib.pmx_pillarize(pts.data_ptr(), offs_d.data_ptr(), B, nmax, ctypes.byref(g), pcap,
+                                  coords.data_ptr(), counts.data_ptr(), pt_idx.data_ptr(), n_pil.data_ptr(),
+                                  ws.data_ptr(), ws_bytes, N.stream_ptr()), "pillarize")
+    torch.cuda.synchronize()
+    for b, f in enumerate(frames):
+        want = O.pillar_index(O.bin_points(f[:, :2], spec.grid, spec.origin, spec.cell), spec.grid,
+                              spec.max_points, pcap)
+        P = len(want.coords)
+        assert int(n_pil[b]) == P, (b, int(n_pil[b]), P)
+        np.testing.assert_array_equal(coords[b, :P].cpu().numpy(), want.coords)
+        np.testing.assert_array_equal(counts[b, :P].cpu().numpy(), want.counts)
+        np.testing.assert_array_equal(pt_idx[b, :P].cpu().numpy(), want.pt_idx)
+
+
+def test_pillarize_persistent_opt_in_subprocess(pm):
+    """The opt-in one-kernel pillarize (PMX_PILLARIZE_PERSIST=1, cooperative launch with
+    grid-wide barriers; read once per process: a subprocess) passes the batched parity."""
+    import os
+    import subprocess
+    import sys
+
+    root = Path(__file__).resolve().parent.parent
+    env = dict(os.environ, PMX_PILLARIZE_PERSIST="1", PMX_NO_BUILD="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
+                        str(Path(__file__)) + "::test_pillarize_batch_vs_oracle"], env=env, cwd=root,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "2 passed" in r.stdout, r.stdout[-2000:]
 
 
 @pytest.mark.slow
