@@ -1070,6 +1070,35 @@ class CompiledGraph:
         self.graph_exec = g
         return g
 
+    def capture_split(self, last: str = "pfn"):
+        """The launch list as TWO graphs: the ops up to and including `last` (pillarize and
+        the PFN, the only readers of the points / offsets slot) and the rest, so that a
+        streaming caller can refill the input slot as soon as the first one finished.
+        None when the list has side-stream branches (small batches) or no such op."""
+        if getattr(self, "branch_src", None):
+            return None
+        names = [n for n, _ in self.ops]
+        if last not in names:
+            return None
+        k = names.index(last) + 1
+        torch = self.torch
+        st = torch.cuda.Stream()
+        st.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(st):
+            self.launch(st)  # warm-up outside capture
+        torch.cuda.current_stream().wait_stream(st)
+        torch.cuda.synchronize()
+        graphs = []
+        for part in (self.ops[:k], self.ops[k:]):
+            g = torch.cuda.CUDAGraph()
+            with _capturing():
+                with torch.cuda.graph(g, stream=st):
+                    sp = N.stream_ptr(st)
+                    for _, fn in part:
+                        fn(sp)
+            graphs.append(g)
+        return graphs
+
     def replay(self):
         self.graph_exec.replay()
 

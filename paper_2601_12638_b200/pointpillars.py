@@ -17,6 +17,8 @@ z = -1.78, yaw {0, pi/2}, centred on the 0.32 m output cells.
 
 from __future__ import annotations
 
+import os
+
 import math
 from dataclasses import dataclass, field
 
@@ -266,6 +268,9 @@ class PipelinedEngine:
         if eng2 is not None and (eng2.batch != eng.batch or eng2.nmax != eng.nmax):
             raise ValueError("the two engines of a PipelinedEngine need the same batch and point capacity")
         self.slots, self.graphs = [], []
+        # per slot: (front graph reading the input slot, rest) or None -- the next H2D into a
+        # slot then waits only for the front part (pillarize + PFN) of the batch before
+        self.split = []
         for k, e in enumerate(self.engines):
             cg = e.cg
             # a shared engine's slot 1 starts as a copy of slot 0 (capture() warms up on whatever
@@ -279,6 +284,7 @@ class PipelinedEngine:
                 if rec is not None:
                     cg.records = rec
                 self.graphs.append(cg.capture())
+                self.split.append(cg.capture_split())
                 cg.points, cg.offsets = keep[0], keep[1]
                 if rec0 is not None:
                     cg.records = rec0
@@ -286,6 +292,7 @@ class PipelinedEngine:
                 self.slots.append((pts, offs, rec))
             else:
                 self.graphs.append(cg.capture())
+                self.split.append(cg.capture_split())
                 self.slots.append((cg.points, cg.offsets, rec0))
         self.h2d = torch.cuda.Stream()
         self.d2h = torch.cuda.Stream()
@@ -293,6 +300,9 @@ class PipelinedEngine:
         self.copied = [torch.cuda.Event(), torch.cuda.Event()]
         self.done = [torch.cuda.Event(), torch.cuda.Event()]
         self.fetched = [torch.cuda.Event(), torch.cuda.Event()]
+        self.read = [torch.cuda.Event(), torch.cuda.Event()]  # the slot's points / offsets consumed
+        if any(sp is None for sp in self.split) or os.environ.get("PMX_PIPE_SPLIT") == "0":  # (A/B runs)
+            self.split = [None, None]
 
     def _upload(self, i: int, host_points, host_offsets):
         import torch
@@ -301,7 +311,8 @@ class PipelinedEngine:
         pts, offs, _ = self.slots[slot]
         with torch.cuda.stream(self.h2d):
             if i >= 2:
-                self.h2d.wait_event(self.done[slot])  # batch i-2 finished reading this slot
+                # batch i-2 finished reading this slot (split graphs: its front part)
+                self.h2d.wait_event(self.read[slot] if self.split[slot] is not None else self.done[slot])
             pts[: host_points.shape[0]].copy_(host_points, non_blocking=True)
             offs.copy_(host_offsets, non_blocking=True)
             self.copied[slot].record(self.h2d)
@@ -334,7 +345,12 @@ class PipelinedEngine:
                 # records buffer before the graph rewrites it
                 comp.wait_event(self.fetched[slot])
             with torch.cuda.stream(comp):
-                self.graphs[slot].replay()
+                if self.split[slot] is not None:
+                    self.split[slot][0].replay()
+                    self.read[slot].record(comp)
+                    self.split[slot][1].replay()
+                else:
+                    self.graphs[slot].replay()
                 rec = pack(self.engines[slot].topk()) if pack is not None else self.slots[slot][2]
                 self.done[slot].record(comp)
             with torch.cuda.stream(self.d2h):

@@ -311,6 +311,43 @@ def test_pipelined_engine_matches_sequential(pm):
         assert torch.equal(o, w)
 
 
+def test_pipelined_engine_split_graphs_two_engines(pm):
+    """Batch 9 (no side-stream branches): each slot replays two graphs (pillarize + PFN,
+    then the rest) and the next H2D into a slot waits only for the first; two engines
+    alternate on their own streams.  Every batch's records equal its sequential run."""
+    import torch
+
+    from paper_2601_12638_b200 import distributed as D
+
+    cfg = pm.PointPillarsConfig.small(max_pillars=1500)
+    graph = pm.build_pointpillars(cfg, seed=6)
+    stats = pm.calibrate_frames(graph, [pm.make_frame(3000, 800 + i, cfg) for i in range(2)], cfg)
+    B = 9
+    batches_np = [[pm.make_frame(1500 + 100 * i + 37 * j, 900 + 10 * j + i, cfg) for i in range(B)] for j in range(7)]
+    ref = pm.PointPillarsEngine(graph, pm.MIXED_PLAN_LABEL, stats, cfg, batch=B, max_points_per_frame=3000)
+    want = []
+    for fr in batches_np:
+        ref.load_points(fr)
+        ref.run()
+        want.append(D.pack_topk(ref.topk()).cpu())
+    e1 = pm.PointPillarsEngine(graph, pm.MIXED_PLAN_LABEL, stats, cfg, batch=B, max_points_per_frame=3000)
+    e2 = pm.PointPillarsEngine(graph, pm.MIXED_PLAN_LABEL, stats, cfg, batch=B, max_points_per_frame=3000)
+    e1.load_points(batches_np[0])
+    e2.load_points(batches_np[0])
+    pipe = pm.PipelinedEngine(e1, e2)
+    assert all(sp is not None for sp in pipe.split)
+    batches = []
+    for fr in batches_np:
+        offs = np.zeros(B + 1, np.int64)
+        offs[1:] = np.cumsum([len(f) for f in fr])
+        batches.append((torch.from_numpy(np.concatenate(fr)).pin_memory(), torch.from_numpy(offs).pin_memory()))
+    outs = [torch.empty_like(w).pin_memory() for w in want]
+    pipe.run(batches, outs)
+    torch.cuda.synchronize()
+    for j, (o, w) in enumerate(zip(outs, want)):
+        assert torch.equal(o, w), j
+
+
 def test_pipelined_engine_batch1_many_distinct_frames(pm):
     """Batch 1 (short graphs) over many distinct frames: every slot's records buffer is
     rewritten only after the previous D2H copy of that slot finished (no WAR race)."""

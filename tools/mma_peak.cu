@@ -102,8 +102,8 @@ struct Result {
 };
 
 template <int KIND>
-Result measure(int sms, double seconds) {
-  const uint32_t m_enc = 128u >> 4, n_enc = 256u >> 3;
+Result measure(int sms, double seconds, int n = 256) {
+  const uint32_t m_enc = 128u >> 4, n_enc = (uint32_t)n >> 3;
   uint32_t idesc = (n_enc << 17) | (m_enc << 24);
   if (KIND == 0) idesc |= (2u << 4) | (1u << 7) | (1u << 10);  // s32 <- s8 x s8
   if (KIND == 1) idesc |= (1u << 4);                           // f32 <- f16 x f16
@@ -112,7 +112,7 @@ Result measure(int sms, double seconds) {
   cudaFuncSetAttribute(peak_kernel<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   // K elements per 32-byte step: i8 32, f16 16, tf32 8
   const double k_el = KIND == 0 ? 32.0 : (KIND == 1 ? 16.0 : 8.0);
-  const double ops_per_iter = 4.0 * 2.0 * 128.0 * 256.0 * k_el;
+  const double ops_per_iter = 4.0 * 2.0 * 128.0 * (double)n * k_el;
   const int iters = 40000;  // ~10 ms at full rate
   cudaEvent_t a, b;
   cudaEventCreate(&a);
@@ -130,6 +130,7 @@ Result measure(int sms, double seconds) {
     const double rate = ops_per_iter * iters * sms / (ms * 1e-3) / 1e12;
     if (rate > best) best = rate;
   }
+  if (seconds <= 0.0) return Result{best, 0.0};  // burst only (--by-n)
   // sustained: back to back for `seconds`, rate over the second half
   const auto t0 = std::chrono::steady_clock::now();
   double ops2 = 0.0, t_half = 0.0;
@@ -169,6 +170,17 @@ int main(int argc, char** argv) {
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  for (int i = 1; i < argc; ++i)
+    if (!strcmp(argv[i], "--by-n")) {
+      // burst rate of one instruction shape per N (the conv layers' N tiles: 64, 128, 256)
+      printf("{\"how\": \"tools/mma_peak.cu --by-n: burst (best of 5) back-to-back M=128 K=32B MMAs per N\"");
+      for (int n : {64, 128, 256}) {
+        const Result a = measure<0>(sms, 0.0, n), b = measure<1>(sms, 0.0, n);
+        printf(", \"int8_n%d_tops\": %.1f, \"f16_n%d_tflops\": %.1f", n, a.burst, n, b.burst);
+      }
+      printf("}\n");
+      return 0;
+    }
   const Result i8 = measure<0>(sms, seconds);
   const Result f16 = measure<1>(sms, seconds);
   const Result tf32 = measure<2>(sms, seconds);
