@@ -57,6 +57,8 @@ def build(force: bool = False, verbose: bool = False, ptxas_verbose: bool = Fals
         extra += ["-DPMX_CONV_TRACE"]
     if os.environ.get("PMX_DECODE_TRACE") == "1":  # per-phase decode timeline (experiments only)
         extra += ["-DPMX_DECODE_TRACE"]
+    if os.environ.get("PMX_PFN_TRACE") == "1":  # per-phase PFN timeline (experiments only)
+        extra += ["-DPMX_PFN_TRACE"]
     if os.environ.get("PMX_ABLATE"):  # epilogue ablation builds (experiments only)
         extra += [f"-DPMX_ABLATE={int(os.environ['PMX_ABLATE'])}"]
 

@@ -47,6 +47,7 @@ struct PfnArgs {
   uint32_t* in_keys;
   uint32_t* out_keys;
   int dense;  // pmx_pfn_pillars: rows are pillar slots (b * pcap + p), no canvas
+  int ppw;    // pfn_points_kernel: pillars per warp (32; 16 / 8 when one wave of 32 would leave SMs idle)
 };
 
 template <int DT>
@@ -249,6 +250,10 @@ template <int DT>
 #endif
 __global__ void __launch_bounds__(kThreads, PMX_PFN_MINB) pfn_points_kernel(const PfnArgs a, const Outs outs) {
   pdl_begin();
+#ifdef PMX_PFN_TRACE
+  unsigned long long pt0, pt1, pt2;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(pt0));
+#endif
   using R = Rec<DT>;
   using T = typename R::T;
   extern __shared__ __align__(16) uint8_t pfn_smem[];
@@ -304,8 +309,8 @@ __global__ void __launch_bounds__(kThreads, PMX_PFN_MINB) pfn_points_kernel(cons
   const float xoff = (float)((double)a.g.cell_w * 0.5 + (double)a.g.x_min);
   const float yoff = (float)((double)a.g.cell_h * 0.5 + (double)a.g.y_min);
   // ---------------- phase A: lane = pillar
-  const int p = (blockIdx.x * (kThreads / 32) + warp) * 32 + lane;
-  const bool live = p < P;
+  const int p = (blockIdx.x * (kThreads / 32) + warp) * a.ppw + lane;
+  const bool live = lane < a.ppw && p < P;
   const int64_t q = (int64_t)b * a.pcap + (live ? p : 0);
   const int k = live ? a.counts[q] : 0;
   const int32_t* idx = a.pt_idx + q * M;
@@ -379,6 +384,9 @@ __global__ void __launch_bounds__(kThreads, PMX_PFN_MINB) pfn_points_kernel(cons
     }
   }
   __syncwarp();
+#ifdef PMX_PFN_TRACE
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(pt1));
+#endif
   // ---------------- phase B: two pillars per step; lane = (pillar half, 4 channels)
   const int half = lane >> 4;
   const int c = 4 * (lane & 15);
@@ -406,7 +414,7 @@ __global__ void __launch_bounds__(kThreads, PMX_PFN_MINB) pfn_points_kernel(cons
   // single f16 consumer with 8-byte aligned 4-channel runs (kernel-uniform)
   const bool f16_only = outs.n == 1 && outs.o[0].dtype == PMX_F16 && (outs.o[0].c_stride & 3) == 0 &&
                         (outs.o[0].c_offset & 3) == 0;
-  for (int it = 0; it < 16; ++it) {
+  for (int it = 0; it < (a.ppw >> 1); ++it) {
     const int j = 2 * it + half;
     const int kj = __shfl_sync(0xffffffffu, k, j);
     const int kpair = max(kj, __shfl_xor_sync(0xffffffffu, kj, 16));
@@ -512,6 +520,12 @@ __global__ void __launch_bounds__(kThreads, PMX_PFN_MINB) pfn_points_kernel(cons
       for (int u = 0; u < nl; ++u) { o_lo = nmin(o_lo, y[u]); o_hi = nmax(o_hi, y[u]); }
     }
   }
+#ifdef PMX_PFN_TRACE
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(pt2));
+  if (lane == 0 && (blockIdx.x % 8 == 0) && warp == 0)
+    printf("pfn trace blk %d warp %d: start %llu phaseA %llu phaseB %llu keys %d/%d\n", blockIdx.x, warp, pt0 % 1000000,
+           pt1 - pt0, pt2 - pt1, a.in_keys != nullptr, a.out_keys != nullptr);
+#endif
   if (a.in_keys) block_minmax_commit<kThreads>(in_lo, in_hi, a.in_keys);
   if (a.out_keys) block_minmax_commit<kThreads>(o_lo, o_hi, a.out_keys);
 }
@@ -519,10 +533,26 @@ __global__ void __launch_bounds__(kThreads, PMX_PFN_MINB) pfn_points_kernel(cons
 template <int DT>
 pmx_status launch_dt(const PfnArgs& a, const Outs& outs, dim3 grid, cudaStream_t st) {
   if (a.d.source == PMX_PFN_FROM_POINTS9) {
-    const dim3 g2((unsigned)ceil_div(a.pcap, kThreads), grid.y);  // 32 pillars per warp
+    // 32 pillars per warp; small batches (one wave of those would leave SMs idle): 16 or
+    // 8, a shorter per-warp chain over more warps (batch 1: 63 -> 252 blocks)
+    PfnArgs a2 = a;
+    a2.ppw = 32;
+    {
+      static const int fixed = [] {
+        const char* e = getenv("PMX_PFN_PPW");  // A/B override: 8, 16 or 32
+        return e ? atoi(e) : 0;
+      }();
+      if (fixed == 8 || fixed == 16 || fixed == 32) {
+        a2.ppw = fixed;
+      } else {
+        while (a2.ppw > 8 && (int64_t)ceil_div(a.pcap, (kThreads / 32) * (a2.ppw / 2)) * grid.y <= 2LL * num_sms())
+          a2.ppw /= 2;
+      }
+    }
+    const dim3 g2((unsigned)ceil_div(a.pcap, (kThreads / 32) * a2.ppw), grid.y);
     const size_t sm = pfn_points_smem<DT>();
     PMX_CUDA(cudaFuncSetAttribute(pfn_points_kernel<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    PMX_CUDA(launch_pdl(pfn_points_kernel<DT>, g2, dim3(kThreads), sm, st, a, outs));
+    PMX_CUDA(launch_pdl(pfn_points_kernel<DT>, g2, dim3(kThreads), sm, st, a2, outs));
   } else {
     switch (a.d.n_features) {
 #define PMX_F_CASE(N) \
