@@ -55,13 +55,21 @@ def main():
     stats = pm.calibrate_frames(graph, [pm.make_frame(args.points, 900 + i, cfg, 0.01) for i in range(2)], cfg)
     names = {l.name: l.index for l in graph.weight_layers}
     table = {}
+    fused_plans = set()
     plans = args.plans.split(";")
     for label in plans:
         eng = pm.PointPillarsEngine(graph, label, stats if label != "FP32" and label != "FP16" else None, cfg,
                                     batch=args.batch, max_points_per_frame=args.points)
         eng.load_points(frames)
         eng.run()
-        table[label] = op_times(eng, args.reps)
+        t = op_times(eng, args.reps)
+        # small batches run the deconvs with the heads fused (ops "conv <deblock>+heads"):
+        # report each under its deconv row and the heads row as included there
+        if any(k.endswith("+heads") for k in t):
+            t = {(k[:-len("+heads")] if k.endswith("+heads") else k): v for k, v in t.items()}
+            t["conv heads(fused)"] = 0.0
+            fused_plans.add(label)
+        table[label] = t
     rows = []
     for op in table[plans[0]]:
         if op.startswith("conv "):
@@ -81,10 +89,15 @@ def main():
     print("|---|---|" + "---|" * len(plans))
     tot = [0.0] * len(plans)
     for r in rows:
-        print(f"| {r[0]} | {r[1]} | " + " | ".join(f"{v:.1f}" for v in r[2:]) + " |")
+        cells = [("in 18-20" if (p in fused_plans and "heads" in str(r[1]) and r[0] == "21-23") else f"{v:.1f}")
+                 for p, v in zip(plans, r[2:])]
+        print(f"| {r[0]} | {r[1]} | " + " | ".join(cells) + " |")
         for i in range(len(plans)):
             tot[i] += r[2 + i]
     print("| | **sum** | " + " | ".join(f"**{t:.1f}**" for t in tot) + " |")
+    if fused_plans:
+        print(f"\n{', '.join(sorted(fused_plans))}: deconvs 18-20 run fused with the 1x1 heads at this batch "
+              "(`pmx_deconv_heads`, the engine's choice at batch <= 2); each deconv row includes its head slice.")
 
 
 if __name__ == "__main__":
