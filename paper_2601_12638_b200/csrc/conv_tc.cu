@@ -455,6 +455,51 @@ __device__ __forceinline__ bool quant16_noclamp(const float (&y)[16], float inv,
   return dm < kTieBand && rm < 127.5f;
 }
 
+// quant16_noclamp finished in place: when a chunk has a near-tie, NaN or saturating
+// value (a constant empty-region activation on a tie puts ~5% of a deconv's chunks
+// there), only the flagged values are redone on the exact path -- the others keep
+// their fast code -- instead of requantising all 16 with clamps and patching again
+// (batch 1: every layer's slowest CTA waits for this).  Bit-identical to quant16 with
+// lo = 0 (RELU) or -128: every value is clip(rint(f64(relu?(y)) / s)).
+template <bool RELU>
+__device__ __forceinline__ uint4 quant16_sel(const float (&y)[16], double s, float inv) {
+  const float2 M2 = make_float2(12582912.0f, 12582912.0f), I2 = make_float2(inv, inv);
+  uint32_t tb[16];
+  float dm = 0.0f, rm = 0.0f;
+#pragma unroll
+  for (int j = 0; j < 16; j += 2) {
+    const float2 yy = make_float2(y[j], y[j + 1]);
+    const float2 t = __ffma2_rn(yy, I2, M2);
+    const float2 r = __fadd2_rn(t, make_float2(-12582912.0f, -12582912.0f));
+    const float2 d = __ffma2_rn(yy, I2, make_float2(-r.x, -r.y));
+    dm = fmax3_nan(dm, fabsf(d.x), fabsf(d.y));
+    rm = fmax3_nan(rm, fabsf(r.x), fabsf(r.y));
+    tb[j] = __float_as_uint(t.x);
+    tb[j + 1] = __float_as_uint(t.y);
+  }
+  if (!(dm < kTieBand && rm < 127.5f)) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const float r = __fsub_rn(__uint_as_float(tb[j]), 12582912.0f);
+      const float d = __fmaf_rn(y[j], inv, -r);
+      if (!(fabsf(d) < kTieBand && fabsf(r) < 127.5f))
+        tb[j] = (uint32_t)quantize_exact(RELU ? fmaxf(y[j], 0.0f) : y[j], s, inv);
+    }
+  }
+  uint32_t w[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    w[k] = __byte_perm(__byte_perm(tb[4 * k], tb[4 * k + 1], 0x0040), __byte_perm(tb[4 * k + 2], tb[4 * k + 3], 0x0040),
+                       0x5410);
+    if (RELU) {
+      uint32_t sm;
+      asm("prmt.b32 %0, %1, 0, 0xBA98;" : "=r"(sm) : "r"(w[k]));
+      w[k] &= ~sm;
+    }
+  }
+  return make_uint4(w[0], w[1], w[2], w[3]);
+}
+
 // One chunk (16 accumulator columns of one pixel row): y = acc * alpha + bias (int8)
 // or acc + bias (f16), optional unfolded BN and ReLU, observer min/max, then every
 // consumer format.  alpha / bias come from the shared-memory copies.
@@ -1494,9 +1539,7 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
               y[4 * j4 + 2] = r1.x;
               y[4 * j4 + 3] = r1.y;
             }
-            uint4 code;
-            const bool ok = p.relu ? quant16_noclamp<true>(y, o_inv, code) : quant16_noclamp<false>(y, o_inv, code);
-            if (!ok) code = quant16(y, o_scale, o_inv, qlo);
+            const uint4 code = p.relu ? quant16_sel<true>(y, o_scale, o_inv) : quant16_sel<false>(y, o_scale, o_inv);
             const uint32_t sa = wstage + (uint32_t)lane * 64u + (((uint32_t)k ^ (((uint32_t)lane >> 1) & 3u)) << 4);
             asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(sa), "r"(code.x), "r"(code.y), "r"(code.z),
                          "r"(code.w)
@@ -1591,9 +1634,7 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
               y[4 * j4 + 2] = r1.x;
               y[4 * j4 + 3] = r1.y;
             }
-            uint4 code;
-            const bool ok = p.relu ? quant16_noclamp<true>(y, o_inv, code) : quant16_noclamp<false>(y, o_inv, code);
-            if (!ok) code = quant16(y, o_scale, o_inv, qlo);
+            const uint4 code = p.relu ? quant16_sel<true>(y, o_scale, o_inv) : quant16_sel<false>(y, o_scale, o_inv);
 #if defined(PMX_ABLATE) && PMX_ABLATE == 2
             if ((code.x & code.y & code.z & code.w) == 0x7f7f7f7fu)
 #endif
