@@ -550,7 +550,7 @@ __device__ __forceinline__ void epi_chunk(const TcParams& p, const Outs& outs, c
     if (full16 && !p.bn_post && !p.keys) {
       const OutDev& od = outs.o[0];
       *reinterpret_cast<uint4*>(reinterpret_cast<int8_t*>(od.ptr) + (size_t)pix * od.c_stride + od.c_offset + cobase) =
-          quant16(y, od.scale, od.inv, qlo);
+          (qlo == 0.0f ? quant16_sel<true>(y, od.scale, od.inv) : quant16_sel<false>(y, od.scale, od.inv));
       return;
     }
   }
@@ -578,7 +578,7 @@ __device__ __forceinline__ void epi_chunk(const TcParams& p, const Outs& outs, c
     const OutDev& od = outs.o[0];
     if (full16) {
       *reinterpret_cast<uint4*>(reinterpret_cast<int8_t*>(od.ptr) + (size_t)pix * od.c_stride + od.c_offset + cobase) =
-          quant16(y, od.scale, od.inv);
+          quant16_sel<false>(y, od.scale, od.inv);
     } else {
       for (int j = 0; j < 16; ++j)
         if (nbase + j < p.n_gemm) store_one(od, pix, cobase + j, y[j]);
@@ -590,7 +590,7 @@ __device__ __forceinline__ void epi_chunk(const TcParams& p, const Outs& outs, c
       const OutDev& od = outs.o[o];
       const int64_t off = (int64_t)pix * od.c_stride + od.c_offset + cobase;
       if (full16 && od.dtype == PMX_I8 && (off & 15) == 0) {
-        *reinterpret_cast<uint4*>(reinterpret_cast<int8_t*>(od.ptr) + off) = quant16(y, od.scale, od.inv);
+        *reinterpret_cast<uint4*>(reinterpret_cast<int8_t*>(od.ptr) + off) = quant16_sel<false>(y, od.scale, od.inv);
       } else if (full16 && od.dtype == PMX_F16 && (off & 7) == 0) {
         uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__half*>(od.ptr) + off);
         dst[0] = make_uint4(f16x2_sat(y[0], y[1]), f16x2_sat(y[2], y[3]), f16x2_sat(y[4], y[5]), f16x2_sat(y[6], y[7]));
@@ -1321,7 +1321,7 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
             else t = __fadd_rn(__uint_as_float(v[j]), s_bias[cobase + j]);
             y[j] = p.relu ? fmaxf(t, 0.f) : t;
           }
-          uint4 code = valid ? quant16(y, p.hscale, p.hinv) : make_uint4(0, 0, 0, 0);
+          uint4 code = valid ? quant16_sel<false>(y, p.hscale, p.hinv) : make_uint4(0, 0, 0, 0);
           const uint32_t jj = (uint32_t)(c_begin + k);  // 16-byte chunk of the 128-byte row
           asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(st + (uint32_t)row * 128u +
                                                                          ((jj ^ ((uint32_t)row & 7u)) << 4)),
@@ -1400,7 +1400,7 @@ __global__ void __launch_bounds__(GATHER ? kThreadsGather : kThreads, 1)
             // clamp-free fast quantizer (y is already ReLU'd when relu is set); ties,
             // saturation and NaN take the exact path
             uint4 code8;
-            if (!quant16_noclamp<false>(y, inv8, code8)) code8 = quant16(y, sc8, inv8);
+            code8 = quant16_sel<false>(y, sc8, inv8);
             *reinterpret_cast<uint4*>(p8 + (size_t)pix_in * cs8 + cobase) = code8;
           };
           auto sts_f16 = [&](uint32_t a0, uint32_t a1, const float (&y)[16]) {
