@@ -19,13 +19,14 @@ namespace pmx {
 namespace {
 
 // anchors per CTA, chosen per call: large batches want few, full CTAs (16384: 7 per
-// KITTI frame, 68 vs 76 us at batch 32), batch 1 wants more CTAs per frame (2048, 53
-// CTAs, with the rank-sort finish: b1 p50 mixed 0.2464 -> 0.2458 ms, INT8 0.2331 ->
-// 0.2312 vs 4096; 1024 no better, 8192 +6 us)
+// KITTI frame; batch 32: 0.058 ms vs 0.067 at 4096), batch 1 wants more CTAs per frame
+// (2048, 53 CTAs, with the rank-sort finish: b1 p50 mixed 0.2464 -> 0.2458 ms, INT8
+// 0.2331 -> 0.2312 vs 4096; 1024 no better, 8192 +6 us), batch 8 sits between (4096:
+// 0.673 ms per step vs 0.684 at 16384, 0.675 at 8192)
 int decode_chunk(int batch) {
   const char* e = getenv("PMX_DECODE_CHUNK");  // A/B override
   if (e && atoi(e) >= 1024) return atoi(e) & ~1023;
-  return batch >= 8 ? 16384 : (batch >= 2 ? 8192 : 2048);
+  return batch > 16 ? 16384 : (batch > 8 ? 8192 : (batch >= 2 ? 4096 : 2048));
 }
 constexpr int kThreads = 1024;
 
