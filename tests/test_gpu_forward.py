@@ -219,6 +219,10 @@ def test_kitti_small_end_to_end(pm, label):
             assert err <= max(1e-2, 2 * floor), (label, name, err, floor)
         if label == "INT8":  # exact int32 accumulation == the integer-execution semantics
             assert rel_l2(heads[name][0], ri[0]) <= 1e-5, (name, rel_l2(heads[name][0], ri[0]))
+        elif label not in ("FP32", "FP16"):
+            # mixed plans: a fixed bar against the integer-execution semantics (INT8 layers
+            # exact; the FP16 layers' f32 accumulation order is the only difference)
+            assert rel_l2(heads[name][0], ri[0]) <= 2e-4, (label, name, rel_l2(heads[name][0], ri[0]))
 
 
 def test_engine_calibration_matches_oracle(pm):
