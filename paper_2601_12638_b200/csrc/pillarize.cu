@@ -389,21 +389,31 @@ __device__ void emit_block(const pmx_grid& g, const PillarWs& w, int cb, int32_t
   __syncthreads();
   a += (int)((s_prefix >> 40) & kLookKeptMask);
   p += (int)(s_prefix & kLookPtsMask);
+  static_assert(kCellPerThr == 4, "the cell map row store below is one int4");
+  int pv[kCellPerThr];
 #pragma unroll
   for (int j = 0; j < kCellPerThr; ++j) {
     const int64_t c = c0 + j;
+    pv[j] = 0;
     if (c >= hw) break;
     if (keep[j]) {
       const int64_t q = (int64_t)b * pcap + a;
-      w.pid[b * hw + c] = a + 1;  // slot + 1 (0 = empty)
+      pv[j] = a + 1;  // slot + 1 (0 = empty)
       *reinterpret_cast<int2*>(coords + 2 * q) = make_int2((int)(c / g.grid_w), (int)(c % g.grid_w));
       counts[q] = n[j] < g.max_points ? n[j] : g.max_points;
       w.segoff[q] = p;
       a += 1;
       p += n[j];
-    } else {
-      w.pid[b * hw + c] = 0;
     }
+  }
+  // the cell map row as one 16-byte store per thread: four 4-byte stores 16 bytes apart
+  // per instruction left every L2 sector partially written (ncu: emit read ~2x its bytes)
+  if ((hw & 3) == 0 && c0 + kCellPerThr <= hw) {
+    *reinterpret_cast<int4*>(w.pid + b * hw + c0) = make_int4(pv[0], pv[1], pv[2], pv[3]);
+  } else {
+#pragma unroll
+    for (int j = 0; j < kCellPerThr; ++j)
+      if (c0 + j < hw) w.pid[b * hw + c0 + j] = pv[j];
   }
 }
 
